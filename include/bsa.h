@@ -1,0 +1,158 @@
+/*
+ * bsa.h — C ABI of libbsa.so, the B200 (sm_100a) implementation of the hot path of BSA,
+ * "Bidirectional Sparse Attention" (arXiv 2509.01085, /root/reference/PAPER.md).
+ *
+ * The path has five calls, in the order a training step uses them:
+ *   bsa_block_partition   3D block partition of the (T,H,W) token grid      (§3.2.1)
+ *   bsa_select_queries    query pruning by cosine to the unit centre (Eq.2)  (§3.2.2)
+ *   bsa_select_kv_blocks  statistical threshold (Eq.3) + cumulative admission (Eq.4) (§3.2.3)
+ *   bsa_attn_fwd          block-sparse attention over kept queries x admitted KV blocks (Eq.5)
+ *                         and the fill that restores length L
+ *   bsa_attn_bwd          its gradient (semantics in DESIGN.md reading C10)
+ *
+ * Conventions (all calls):
+ *  - Tensors Q, K, V, O, dO, dQ, dK, dV are bf16, contiguous [B, Hh, L, d] (d fastest), tokens in
+ *    raster order n = t*H*W + h*W + w. d must be 64 or 128. Device pointers must be 16-byte
+ *    aligned. Index arrays are int32, device memory.
+ *  - Ownership: the caller allocates every buffer (device unless stated) and passes a CUDA stream
+ *    (cudaStream_t, passed as void*; NULL = legacy default stream). The library never allocates,
+ *    frees or synchronises; every call only enqueues work on `stream` and returns. Calls are
+ *    reentrant; the only global state is the thread-local last-error string.
+ *  - Errors: every call returns BSA_OK (0) or an error code; argument validation happens before
+ *    any launch, so nothing is written on a validation error. bsa_last_error() gives the message.
+ *  - Geometry: grid (T,H,W), block (ct,ch,cw), query-selection unit (ut,uh,uw) (the paper's window
+ *    (w_t,w_h,w_w)); ut=uh=uw=0 means unit = block (block-centre selection, the north_star
+ *    default). Grids need not be divisible by the block: edge blocks are truncated (reading C1).
+ *    Block ids are row-major over (ceil(T/ct), ceil(H/ch), ceil(W/cw)). The attention kernels
+ *    require ct*ch*cw in {32, 64} and N = number of blocks <= 4096.
+ *  - r in (0,1] is the query keep ratio (Eq.2's retention ratio); a unit of n tokens keeps
+ *    clamp(ceil(r*n - 1e-9), 1, n) queries (reading C6). k in [1,N] is Eq.3's key count (k = N turns
+ *    the threshold off, reading C15); tau in (0,1] is Eq.4's cumulative-mass target (reading C17).
+ */
+#ifndef BSA_H_
+#define BSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum bsa_status {
+  BSA_OK = 0,
+  BSA_ERR_INVALID_SHAPE = 1,       /* zero extents, unsupported d or block size, misaligned pointer */
+  BSA_ERR_CONFIG = 2,              /* r, k, tau, unit dims or scale out of range */
+  BSA_ERR_SELECTION_MISMATCH = 3,  /* buffers/workspace sized for another geometry, or NULL */
+  BSA_ERR_UNSUPPORTED_DEVICE = 4,  /* current device is not sm_100 */
+  BSA_ERR_CUDA = 5                 /* a CUDA launch failed; message carries cudaGetErrorString */
+};
+
+typedef struct bsa_geom {
+  int32_t T, H, W;    /* latent token grid */
+  int32_t ct, ch, cw; /* cuboid block (C_t, C_h, C_w) */
+  int32_t ut, uh, uw; /* selection unit (window); 0,0,0 = whole block */
+} bsa_geom;
+
+/* Workspace-using operations (bsa_workspace_bytes `op`). */
+enum bsa_op { BSA_OP_SELECT_KV = 1, BSA_OP_ATTN_FWD = 2, BSA_OP_ATTN_BWD = 3 };
+
+int bsa_version(void);
+const char* bsa_strerror(int status);
+/* Message of the last error raised on the calling thread ("" if none). */
+const char* bsa_last_error(void);
+
+/* Host-only sizes for allocation: N blocks, Lq kept queries per (b,h) (= sum over blocks of the
+ * per-block kept counts, which depend only on geometry and r), and the largest per-block kept
+ * count. Any output pointer may be NULL. */
+int bsa_sizes(const bsa_geom* g, double r, int32_t* N, int32_t* Lq, int32_t* max_block_kept);
+
+/* Bytes of device workspace `op` needs for this problem (0 is possible). */
+int bsa_workspace_bytes(int op, const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, size_t* bytes);
+
+/* a1 — 3D block partition. Writes, for the geometry and r:
+ *   block_off[N+1]  prefix of block sizes (block b owns block_tok[block_off[b] .. block_off[b+1]))
+ *   block_tok[L]    tokens of each block, ascending raster index inside a block
+ *   block_ext[3N]   actual (truncated) extent (e_t, e_h, e_w) of each block
+ *   kept_off[N+1]   prefix of per-block kept-query counts (packed-query row ranges)
+ * Any output may be NULL (skipped). Deterministic; depends only on (g, r). */
+int bsa_block_partition(const bsa_geom* g, double r, int32_t* block_off, int32_t* block_tok, int32_t* block_ext,
+                        int32_t* kept_off, void* stream);
+
+/* a2+a3 — query pruning (Eq.2) in one pass over Q.
+ * For each unit: c_i = cos(q_centre, q_i) (centre = floor-midpoint of the unit's actual extent,
+ * c_centre = 1, zero norm -> 0); tokens ordered by (c ascending, index ascending) and the first
+ * clamp(ceil(r|u|-1e-9),1,|u|) are kept (rank of 1-cos descending, Eq.2 literal). Each pruned token
+ * gets a donor: the kept token of its unit with the largest cosine to it (ties -> lowest index).
+ * All decisions are taken in fp64 on the exact bf16 input values.
+ *   kept_off   [N+1]          from bsa_block_partition (same g, r)
+ *   kept_tok   [B,Hh,Lq] out  kept tokens, block-major, ascending inside each block
+ *   donor      [B,Hh,L]  out  donor token of every token (itself if kept)
+ *   q_pooled   [B,Hh,N,d] out fp64 block means of Q; may be NULL
+ *   q_packed   [B,Hh,Lq,d] out bf16 rows of the kept queries in kept_tok order (Q^s); may be NULL */
+int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q,
+                       const int32_t* kept_off, int32_t* kept_tok, int32_t* donor, double* q_pooled, void* q_packed,
+                       void* stream);
+
+/* a2+a4+a5+a6 — KV-block selection (Eq.3, Eq.4) per (b,h, query block i):
+ *   s_j = Qc[i].Kc[j]/sqrt(d) (fp64), mu/sigma population statistics over the N scores,
+ *   k < N: p = mu + sigma * Phi^-1(clamp(1-k/N, 1/(2N), 1-1/(2N))), candidates C = {j: s_j >= p}
+ *          (empty -> {argmax}); k == N: C = all blocks.
+ *   Admit the shortest prefix of C ordered by (s desc, j asc) whose exp(s - max) mass reaches
+ *   tau * total (tau >= 1: all of C).
+ *   q_pooled  [B,Hh,N,d] fp64 from bsa_select_queries, or NULL (then Q is pooled here)
+ *   q2k_num   [B,Hh,N]   out |S_i|;   q2k_idx [B,Hh,N,N] out S_i ascending in row i's first q2k_num
+ *                         entries (the rest is left unwritten)
+ *   k2q_num   [B,Hh,N]   out number of query blocks admitting KV block j; k2q_idx [B,Hh,N,N] out
+ *                         those query blocks ascending (the transpose, used by bsa_attn_bwd); both
+ *                         may be NULL
+ *   thresh    [B,Hh,N]   out p per row (-inf when k == N); may be NULL
+ *   ws/ws_bytes          device workspace of at least bsa_workspace_bytes(BSA_OP_SELECT_KV, ...) */
+int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q, const double* q_pooled,
+                         const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
+                         int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream);
+
+/* a7 — sparse attention forward (Eq.5) + fill:
+ *   for each kept query q of block i: O^s[q] = softmax(scale * q K_S^T) V_S over the tokens of the
+ *   KV blocks admitted by i; O[kept] = O^s, O[pruned t] = O^s[donor(t)]; lse[q] = natural-log
+ *   log-sum-exp of the scaled logits (packed order). bf16 tcgen05 MMAs, fp32 accumulation and
+ *   online softmax.
+ *   q_packed [B,Hh,Lq,d] Q^s from bsa_select_queries, or NULL (then gathered into ws)
+ *   O        [B,Hh,L,d] out;  lse [B,Hh,Lq] out fp32;  scale > 0 finite (1/sqrt(d) in the paper) */
+int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
+                 const void* V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
+                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, void* O,
+                 float* lse, void* ws, size_t ws_bytes, void* stream);
+
+/* a8 — backward of bsa_attn_fwd with the selection held fixed (reading C10):
+ *   dO^s[q] = dO[q] + sum of dO over the pruned tokens whose donor is q; D = rowsum(dO^s * O^s);
+ *   dV, dK accumulate over admitting query blocks; dQ[kept] = scale * dS K, dQ[pruned] = 0;
+ *   tokens of KV blocks no query block admitted get dK = dV = 0.
+ *   O and lse are the outputs of bsa_attn_fwd; k2q_* from bsa_select_kv_blocks.
+ *   dQ, dK, dV [B,Hh,L,d] out bf16. dQ accumulates through fp32 atomics (order not deterministic). */
+int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
+                 const void* V, const void* O, const void* dO, const void* q_packed, const int32_t* kept_off,
+                 const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
+                 const float* lse, float scale, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                 void* stream);
+
+/* ---------------------------------------------------------------- instrumentation (off the hot path)
+ * Kernel ids reported by bsa_timing_read / counted by bsa_launch_count. */
+enum bsa_kernel_id {
+  BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
+  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_COUNT
+};
+/* Total kernels this thread has launched through libbsa (always counted; cheap). */
+int64_t bsa_launch_count(void);
+/* When enabled on the calling thread, every libbsa kernel launch is bracketed by a CUDA event pair
+ * recorded on the launch stream (events are created lazily; this is a profiling aid, not for
+ * graph capture). */
+int bsa_timing_enable(int on);
+/* Synchronises on the recorded events, writes per-kernel-id summed milliseconds ms[id] and launch
+ * counts launches[id] for id < n (either may be NULL), then clears the record. */
+int bsa_timing_read(double* ms, int32_t* launches, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSA_H_ */

@@ -380,9 +380,16 @@ static void attn_row(const or_geom* g, int d, const double* Qh, const double* Kh
   *lse = mx + log(sum);
 }
 
-void or_attn_fwd(const or_geom* g, double r, int BH, int d, const double* Q, const double* K, const double* V,
-                 const int* kept_tok, const int* donor, const int* q2k_num, const int* q2k_idx, double scale,
-                 double* O, double* lse) {
+/* Query-block range [qb0, qb1) restricts the work to a sample of query blocks (bench cpu_baseline);
+ * or_attn_fwd / or_attn_bwd below are the full range. */
+static int token_block(const or_geom* g, int t) {
+  int tt = t / (g->H * g->W), h = (t / g->W) % g->H, w = t % g->W;
+  return ((tt / g->ct) * cdiv(g->H, g->ch) + h / g->ch) * cdiv(g->W, g->cw) + w / g->cw;
+}
+
+void or_attn_fwd_range(const or_geom* g, double r, int BH, int d, const double* Q, const double* K,
+                       const double* V, const int* kept_tok, const int* donor, const int* q2k_num,
+                       const int* q2k_idx, double scale, double* O, double* lse, int qb0, int qb1) {
   int N = or_num_blocks(g), L = g->T * g->H * g->W, Lq;
   int* kept_off = (int*)malloc(sizeof(int) * (N + 1));
   kept_off[0] = 0;
@@ -390,7 +397,7 @@ void or_attn_fwd(const or_geom* g, double r, int BH, int d, const double* Q, con
   Lq = kept_off[N];
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int bh = 0; bh < BH; ++bh)
-    for (int i = 0; i < N; ++i) {
+    for (int i = qb0; i < qb1; ++i) {
       double* lbuf = (double*)malloc(sizeof(double) * L);
       int* kbuf = (int*)malloc(sizeof(int) * L);
       size_t row = (size_t)bh * N + i;
@@ -407,9 +414,17 @@ void or_attn_fwd(const or_geom* g, double r, int BH, int d, const double* Q, con
   for (int bh = 0; bh < BH; ++bh)
     for (int t = 0; t < L; ++t) {
       int dn = donor[(size_t)bh * L + t];
-      if (dn != t) memcpy(O + ((size_t)bh * L + t) * d, O + ((size_t)bh * L + dn) * d, sizeof(double) * d);
+      int b = token_block(g, t);
+      if (dn != t && b >= qb0 && b < qb1)
+        memcpy(O + ((size_t)bh * L + t) * d, O + ((size_t)bh * L + dn) * d, sizeof(double) * d);
     }
   free(kept_off);
+}
+
+void or_attn_fwd(const or_geom* g, double r, int BH, int d, const double* Q, const double* K, const double* V,
+                 const int* kept_tok, const int* donor, const int* q2k_num, const int* q2k_idx, double scale,
+                 double* O, double* lse) {
+  or_attn_fwd_range(g, r, BH, d, Q, K, V, kept_tok, donor, q2k_num, q2k_idx, scale, O, lse, 0, or_num_blocks(g));
 }
 
 /* Forward for a sample of kept rows only (parity at full size): rows[n] = bh * Lq + packed index.
@@ -447,9 +462,9 @@ void or_attn_fwd_rows(const or_geom* g, double r, int BH, int d, const double* Q
  *   dK[k]  += scale dS_qk q            (keys never admitted get 0)
  * Pass 1 (parallel over query blocks) computes O^s, LSE, D and dQ; pass 2 (parallel over KV blocks
  * j) sums dK_j, dV_j over the admitting query blocks in ascending (block, row) order. */
-void or_attn_bwd(const or_geom* g, double r, int BH, int d, const double* Q, const double* K, const double* V,
-                 const double* dO, const int* kept_tok, const int* donor, const int* q2k_num, const int* q2k_idx,
-                 double scale, double* dQ, double* dK, double* dV) {
+void or_attn_bwd_range(const or_geom* g, double r, int BH, int d, const double* Q, const double* K,
+                       const double* V, const double* dO, const int* kept_tok, const int* donor, const int* q2k_num,
+                       const int* q2k_idx, double scale, double* dQ, double* dK, double* dV, int qb0, int qb1) {
   int N = or_num_blocks(g), L = g->T * g->H * g->W, Lq;
   int* kept_off = (int*)malloc(sizeof(int) * (N + 1));
   kept_off[0] = 0;
@@ -464,7 +479,7 @@ void or_attn_bwd(const or_geom* g, double r, int BH, int d, const double* Q, con
   /* pass 1: per kept row: O^s, LSE, dO^s, D, dQ */
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int bh = 0; bh < BH; ++bh)
-    for (int i = 0; i < N; ++i) {
+    for (int i = qb0; i < qb1; ++i) {
       const double *Qh = Q + (size_t)bh * L * d, *Kh = K + (size_t)bh * L * d, *Vh = V + (size_t)bh * L * d;
       double* lbuf = (double*)malloc(sizeof(double) * L);
       int* kbuf = (int*)malloc(sizeof(int) * L);
@@ -507,7 +522,7 @@ void or_attn_bwd(const or_geom* g, double r, int BH, int d, const double* Q, con
       const double *Qh = Q + (size_t)bh * L * d, *Kh = K + (size_t)bh * L * d, *Vh = V + (size_t)bh * L * d;
       int* ktok = (int*)malloc(sizeof(int) * g->ct * g->ch * g->cw);
       int nk = block_tokens(g, j, ktok);
-      for (int i = 0; i < N; ++i) {
+      for (int i = qb0; i < qb1; ++i) {
         size_t row = (size_t)bh * N + i;
         int adm = 0;
         for (int a = 0; a < q2k_num[row]; ++a) if (q2k_idx[row * N + a] == j) adm = 1;
@@ -531,6 +546,13 @@ void or_attn_bwd(const or_geom* g, double r, int BH, int d, const double* Q, con
       free(ktok);
     }
   free(dOs); free(Dv); free(lse); free(kept_off);
+}
+
+void or_attn_bwd(const or_geom* g, double r, int BH, int d, const double* Q, const double* K, const double* V,
+                 const double* dO, const int* kept_tok, const int* donor, const int* q2k_num, const int* q2k_idx,
+                 double scale, double* dQ, double* dK, double* dV) {
+  or_attn_bwd_range(g, r, BH, d, Q, K, V, dO, kept_tok, donor, q2k_num, q2k_idx, scale, dQ, dK, dV, 0,
+                    or_num_blocks(g));
 }
 
 int or_max_threads(void) {

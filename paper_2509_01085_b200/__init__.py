@@ -1,0 +1,252 @@
+"""paper_2509_01085_b200 — B200-native BSA (Bidirectional Sparse Attention, arXiv 2509.01085).
+
+Thin Python binding over the C ABI of libbsa.so (include/bsa.h). The functions below have the
+same names as the C entry points and only marshal arguments: every step of the hot path runs in
+the library's sm_100a kernels. PyTorch provides device memory and the current CUDA stream.
+There is no CPU fallback: if libbsa.so is missing or the device is not sm_100, calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = [
+    "BSAError", "Geometry", "lib", "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
+    "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "Selection", "select", "resolve_k",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbsa.so")
+
+OP_SELECT_KV, OP_ATTN_FWD, OP_ATTN_BWD = 1, 2, 3
+
+
+class BSAError(RuntimeError):
+    pass
+
+
+class _CGeom(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("T", "H", "W", "ct", "ch", "cw", "ut", "uh", "uw")]
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Latent grid (T,H,W), cuboid block (ct,ch,cw), selection unit/window (
+    0 = whole block, the north_star's block-centre selection)."""
+    T: int
+    H: int
+    W: int
+    ct: int = 4
+    ch: int = 4
+    cw: int = 4
+    ut: int = 0
+    uh: int = 0
+    uw: int = 0
+
+    @property
+    def L(self) -> int:
+        return self.T * self.H * self.W
+
+    def c(self) -> _CGeom:
+        return _CGeom(self.T, self.H, self.W, self.ct, self.ch, self.cw, self.ut, self.uh, self.uw)
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_D = ctypes.c_double
+_F = ctypes.c_float
+_S = ctypes.c_size_t
+
+
+def lib() -> ctypes.CDLL:
+    """Load libbsa.so (built by paper_2509_01085_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BSAError(f"{LIB_PATH} is missing: run `python -m paper_2509_01085_b200.build` (no fallback path)")
+        L = ctypes.CDLL(LIB_PATH)
+        gp = ctypes.POINTER(_CGeom)
+        L.bsa_version.restype = _I
+        L.bsa_strerror.restype = ctypes.c_char_p
+        L.bsa_strerror.argtypes = [_I]
+        L.bsa_last_error.restype = ctypes.c_char_p
+        L.bsa_sizes.argtypes = [gp, _D, _P, _P, _P]
+        L.bsa_workspace_bytes.argtypes = [_I, gp, _D, _I, _I, _I, ctypes.POINTER(_S)]
+        L.bsa_block_partition.argtypes = [gp, _D, _P, _P, _P, _P, _P]
+        L.bsa_select_queries.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]
+        L.bsa_select_kv_blocks.argtypes = [gp, _I, _I, _I, _P, _P, _P, _I, _D, _P, _P, _P, _P, _P, _P, _S, _P]
+        L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _S, _P]
+        L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P,
+                                   _P, _P, _S, _P]
+        for f in ("bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
+                  "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd"):
+            getattr(L, f).restype = _I
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise BSAError(f"{what}: {L.bsa_strerror(rc).decode()} — {L.bsa_last_error().decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise BSAError("libbsa expects contiguous CUDA tensors")
+
+
+def bsa_sizes(g: Geometry, r: float):
+    """(N, Lq, max_block_kept) for geometry g and keep ratio r (host only)."""
+    N, Lq, mk = _I(), _I(), _I()
+    _check(lib().bsa_sizes(ctypes.byref(g.c()), r, ctypes.byref(N), ctypes.byref(Lq), ctypes.byref(mk)), "bsa_sizes")
+    return N.value, Lq.value, mk.value
+
+
+def bsa_workspace_bytes(op: int, g: Geometry, r: float, B: int, Hh: int, d: int) -> int:
+    n = _S()
+    _check(lib().bsa_workspace_bytes(op, ctypes.byref(g.c()), r, B, Hh, d, ctypes.byref(n)), "bsa_workspace_bytes")
+    return n.value
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def bsa_block_partition(g: Geometry, r: float, device="cuda"):
+    """a1: dict of device int32 tensors block_off[N+1], block_tok[L], block_ext[N,3], kept_off[N+1]."""
+    N, Lq, _ = bsa_sizes(g, r)
+    dev = torch.device(device)
+    out = dict(
+        block_off=torch.empty(N + 1, dtype=torch.int32, device=dev),
+        block_tok=torch.empty(g.L, dtype=torch.int32, device=dev),
+        block_ext=torch.empty(N, 3, dtype=torch.int32, device=dev),
+        kept_off=torch.empty(N + 1, dtype=torch.int32, device=dev),
+    )
+    _check(lib().bsa_block_partition(ctypes.byref(g.c()), r, _ptr(out["block_off"]), _ptr(out["block_tok"]),
+                                     _ptr(out["block_ext"]), _ptr(out["kept_off"]), _stream(dev)),
+           "bsa_block_partition")
+    out["N"], out["Lq"] = N, Lq
+    return out
+
+
+def bsa_select_queries(g: Geometry, r: float, Q: torch.Tensor, kept_off: torch.Tensor, pooled: bool = True,
+                       packed: bool = True):
+    """a2+a3 (Eq.2): returns kept_tok [B,Hh,Lq], donor [B,Hh,L], q_pooled [B,Hh,N,d] fp64 or None,
+    q_packed [B,Hh,Lq,d] bf16 or None."""
+    _need_cuda(Q, kept_off)
+    B, Hh, L, d = Q.shape
+    N, Lq, _ = bsa_sizes(g, r)
+    dev = Q.device
+    kept = torch.empty(B, Hh, Lq, dtype=torch.int32, device=dev)
+    donor = torch.empty(B, Hh, L, dtype=torch.int32, device=dev)
+    qp = torch.empty(B, Hh, N, d, dtype=torch.float64, device=dev) if pooled else None
+    qs = torch.empty(B, Hh, Lq, d, dtype=torch.bfloat16, device=dev) if packed else None
+    _check(lib().bsa_select_queries(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(kept_off), _ptr(kept), _ptr(donor),
+                                    _ptr(qp), _ptr(qs), _stream(dev)), "bsa_select_queries")
+    return kept, donor, qp, qs
+
+
+def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, tau: float, q_pooled=None,
+                         with_k2q: bool = True, with_thresh: bool = False):
+    """a4-a6 (Eq.3, Eq.4): returns q2k_num [B,Hh,N], q2k_idx [B,Hh,N,N] (row i valid up to q2k_num),
+    k2q_num, k2q_idx (or None), thresh (or None)."""
+    _need_cuda(Q, K, q_pooled)
+    B, Hh, L, d = K.shape
+    N = bsa_sizes(g, 1.0)[0]
+    dev = K.device
+    num = torch.empty(B, Hh, N, dtype=torch.int32, device=dev)
+    idx = torch.empty(B, Hh, N, N, dtype=torch.int32, device=dev)
+    knum = torch.empty(B, Hh, N, dtype=torch.int32, device=dev) if with_k2q else None
+    kidx = torch.empty(B, Hh, N, N, dtype=torch.int32, device=dev) if with_k2q else None
+    th = torch.empty(B, Hh, N, dtype=torch.float64, device=dev) if with_thresh else None
+    nb = bsa_workspace_bytes(OP_SELECT_KV, g, 1.0, B, Hh, d)
+    ws = _ws(nb, dev)
+    _check(lib().bsa_select_kv_blocks(ctypes.byref(g.c()), B, Hh, d, _ptr(Q), _ptr(q_pooled), _ptr(K), int(k),
+                                      float(tau), _ptr(num), _ptr(idx), _ptr(knum), _ptr(kidx), _ptr(th), _ptr(ws),
+                                      nb, _stream(dev)), "bsa_select_kv_blocks")
+    return num, idx, knum, kidx, th
+
+
+def bsa_attn_fwd(g: Geometry, r: float, Q, K, V, kept_off, kept_tok, donor, q2k_num, q2k_idx, scale=None,
+                 q_packed=None, out=None, lse=None):
+    """a7 (Eq.5) + fill: returns O [B,Hh,L,d] bf16 and lse [B,Hh,Lq] fp32."""
+    _need_cuda(Q, K, V, kept_off, kept_tok, donor, q2k_num, q2k_idx, q_packed)
+    B, Hh, L, d = K.shape
+    Lq = kept_tok.shape[-1]
+    dev = K.device
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    O = torch.empty_like(K) if out is None else out
+    lse = torch.empty(B, Hh, Lq, dtype=torch.float32, device=dev) if lse is None else lse
+    nb = 0 if q_packed is not None else bsa_workspace_bytes(OP_ATTN_FWD, g, r, B, Hh, d)
+    ws = _ws(nb, dev) if nb else None
+    _check(lib().bsa_attn_fwd(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(q_packed),
+                              _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(q2k_num), _ptr(q2k_idx), float(scale),
+                              _ptr(O), _ptr(lse), _ptr(ws), nb, _stream(dev)), "bsa_attn_fwd")
+    return O, lse
+
+
+def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, donor, k2q_num, k2q_idx, lse,
+                 scale=None, q_packed=None, ws=None):
+    """a8: returns dQ, dK, dV [B,Hh,L,d] bf16."""
+    _need_cuda(Q, K, V, O, dO, kept_off, kept_tok, donor, k2q_num, k2q_idx, lse, q_packed)
+    B, Hh, L, d = K.shape
+    dev = K.device
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    dQ, dK, dV = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
+    nb = bsa_workspace_bytes(OP_ATTN_BWD, g, r, B, Hh, d)
+    if ws is None or ws.numel() < nb:
+        ws = _ws(nb, dev)
+    _check(lib().bsa_attn_bwd(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(dO),
+                              _ptr(q_packed), _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(k2q_num),
+                              _ptr(k2q_idx), _ptr(lse), float(scale), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(ws), nb,
+                              _stream(dev)), "bsa_attn_bwd")
+    return dQ, dK, dV
+
+
+def resolve_k(f: float, N: int) -> int:
+    """Eq.3 key count from a fraction: clamp(ceil(f*N - 1e-9), 1, N) (reading C6)."""
+    return max(1, min(N, math.ceil(f * N - 1e-9)))
+
+
+@dataclass
+class Selection:
+    """Everything the attention kernels consume, produced by `select` on the device."""
+    geom: Geometry
+    r: float
+    k: int
+    tau: float
+    part: dict
+    kept_tok: torch.Tensor
+    donor: torch.Tensor
+    q_pooled: torch.Tensor
+    q_packed: torch.Tensor
+    q2k_num: torch.Tensor
+    q2k_idx: torch.Tensor
+    k2q_num: torch.Tensor
+    k2q_idx: torch.Tensor
+
+
+def select(g: Geometry, r: float, k: int, tau: float, Q: torch.Tensor, K: torch.Tensor, part=None) -> Selection:
+    """a1-a6 on the device: partition, query pruning, KV-block admission (and its transpose)."""
+    part = part if part is not None else bsa_block_partition(g, r, Q.device)
+    kept, donor, qp, qs = bsa_select_queries(g, r, Q, part["kept_off"])
+    num, idx, knum, kidx, _ = bsa_select_kv_blocks(g, Q, K, k, tau, q_pooled=qp)
+    return Selection(g, r, k, tau, part, kept, donor, qp, qs, num, idx, knum, kidx)

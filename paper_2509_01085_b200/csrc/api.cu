@@ -1,0 +1,450 @@
+// api.cu — the extern "C" boundary of libbsa.so (declared and documented in include/bsa.h).
+// Validates every argument on the host, sizes workspaces, and enqueues the kernels of
+// select.cu / attn_fwd.cu / attn_bwd.cu on the caller's stream. Never allocates or synchronises.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "../../include/bsa.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(BSA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// ---- instrumentation: launch counter (always) and optional per-kernel CUDA events
+struct TimedRec {
+  int id;
+  cudaEvent_t a, b;
+};
+thread_local int64_t g_launches = 0;
+thread_local bool g_timing = false;
+thread_local std::vector<TimedRec> g_recs;
+
+// Runs one launcher (which may enqueue `nk` kernels) under kernel id `id`.
+template <class F>
+cudaError_t timed(int id, int nk, cudaStream_t st, F&& f) {
+  g_launches += nk;
+  if (!g_timing) return f();
+  TimedRec r{id, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  cudaError_t e = f();
+  cudaEventRecord(r.b, st);
+  g_recs.push_back(r);
+  return e;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Host geometry + validation shared by every entry point.
+int check_geom(const bsa_geom* g, bsa::Geo* out) {
+  if (!g) return fail(BSA_ERR_INVALID_SHAPE, "geometry is NULL");
+  if (g->T < 1 || g->H < 1 || g->W < 1 || g->ct < 1 || g->ch < 1 || g->cw < 1)
+    return fail(BSA_ERR_INVALID_SHAPE, "grid and block extents must be >= 1 (got T,H,W=%d,%d,%d block=%d,%d,%d)",
+                g->T, g->H, g->W, g->ct, g->ch, g->cw);
+  if (g->ut < 0 || g->uh < 0 || g->uw < 0) return fail(BSA_ERR_CONFIG, "unit dims must be >= 0");
+  int ut = g->ut ? g->ut : g->ct, uh = g->uh ? g->uh : g->ch, uw = g->uw ? g->uw : g->cw;
+  if (g->ct % ut || g->ch % uh || g->cw % uw)
+    return fail(BSA_ERR_CONFIG, "unit (%d,%d,%d) must divide the block (%d,%d,%d) (P:168 'evenly dividing')", ut, uh,
+                uw, g->ct, g->ch, g->cw);
+  long long L = 1LL * g->T * g->H * g->W;
+  if (L > (1LL << 30)) return fail(BSA_ERR_INVALID_SHAPE, "L too large");
+  if (g->ct * g->ch * g->cw > 128) return fail(BSA_ERR_INVALID_SHAPE, "block of more than 128 tokens");
+  *out = bsa::make_geo(g->T, g->H, g->W, g->ct, g->ch, g->cw, g->ut, g->uh, g->uw);
+  return BSA_OK;
+}
+
+int check_r(double r) {
+  if (!(r > 0.0 && r <= 1.0)) return fail(BSA_ERR_CONFIG, "r must be in (0,1] (got %g)", r);
+  return BSA_OK;
+}
+
+int check_dims(int B, int Hh, int d) {
+  if (B < 1 || Hh < 1) return fail(BSA_ERR_INVALID_SHAPE, "B and Hh must be >= 1");
+  if (d != 64 && d != 128) return fail(BSA_ERR_INVALID_SHAPE, "d must be 64 or 128 (got %d)", d);
+  return BSA_OK;
+}
+
+int check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(BSA_ERR_UNSUPPORTED_DEVICE, "libbsa is built for sm_100a (B200); device %d is sm_%d%d", dev, major,
+                minor);
+  return BSA_OK;
+}
+
+void host_sizes(const bsa::Geo& g, double r, int* Lq, int* maxk) {
+  int s = 0, m = 0;
+  for (int b = 0; b < g.N; ++b) {
+    int k = bsa::block_kept(g, bsa::block_box(g, b), r);
+    s += k;
+    if (k > m) m = k;
+  }
+  *Lq = s;
+  *maxk = m;
+}
+
+struct SelKvWs {
+  size_t kc, qc, s, bits, total;
+};
+SelKvWs selkv_ws(const bsa::Geo& g, size_t BH, int d) {
+  SelKvWs w;
+  size_t N = g.N, NW = (N + 31) / 32;
+  w.kc = 0;
+  w.qc = w.kc + align256(BH * N * d * 8);
+  w.s = w.qc + align256(BH * N * d * 8);
+  w.bits = w.s + align256(BH * N * N * 8);
+  w.total = w.bits + align256(BH * N * NW * 4);
+  return w;
+}
+
+struct BwdWs {
+  size_t qs, dos, dv, dq, total;
+};
+BwdWs bwd_ws(size_t BH, size_t Lq, int d) {
+  BwdWs w;
+  w.qs = 0;
+  w.dos = w.qs + align256(BH * Lq * d * 2);
+  w.dv = w.dos + align256(BH * Lq * d * 2);
+  w.dq = w.dv + align256(BH * Lq * 4);
+  w.total = w.dq + align256(BH * Lq * d * 4);
+  return w;
+}
+
+int check_attn_geom(const bsa::Geo& G, double r, int* Lq, int* SR) {
+  if (G.BT != 32 && G.BT != 64)
+    return fail(BSA_ERR_INVALID_SHAPE, "attention kernels need ct*ch*cw in {32, 64} (got %d)", G.BT);
+  if (G.N > 4096) return fail(BSA_ERR_INVALID_SHAPE, "attention kernels need N <= 4096 blocks (got %d)", G.N);
+  int maxk = 0;
+  host_sizes(G, r, Lq, &maxk);
+  *SR = bsa::slot_rows(maxk);
+  if (*SR > 128) return fail(BSA_ERR_INVALID_SHAPE, "more than 128 kept queries per block");
+  return BSA_OK;
+}
+
+}  // namespace
+
+#define CHECK(x)                 \
+  do {                           \
+    int _rc = (x);               \
+    if (_rc != BSA_OK) return _rc; \
+  } while (0)
+
+extern "C" {
+
+int bsa_version(void) { return 1; }
+
+const char* bsa_strerror(int s) {
+  switch (s) {
+    case BSA_OK: return "ok";
+    case BSA_ERR_INVALID_SHAPE: return "invalid shape";
+    case BSA_ERR_CONFIG: return "invalid configuration";
+    case BSA_ERR_SELECTION_MISMATCH: return "selection / buffer mismatch";
+    case BSA_ERR_UNSUPPORTED_DEVICE: return "unsupported device (needs sm_100a)";
+    case BSA_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* bsa_last_error(void) { return g_last_error.c_str(); }
+
+int bsa_sizes(const bsa_geom* g, double r, int32_t* N, int32_t* Lq, int32_t* max_block_kept) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_r(r));
+  int lq = 0, mk = 0;
+  host_sizes(G, r, &lq, &mk);
+  if (N) *N = G.N;
+  if (Lq) *Lq = lq;
+  if (max_block_kept) *max_block_kept = mk;
+  return BSA_OK;
+}
+
+int bsa_workspace_bytes(int op, const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, size_t* bytes) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_dims(B, Hh, d));
+  if (!bytes) return fail(BSA_ERR_SELECTION_MISMATCH, "bytes is NULL");
+  size_t BH = static_cast<size_t>(B) * Hh;
+  if (op == BSA_OP_SELECT_KV) {
+    *bytes = selkv_ws(G, BH, d).total;
+    return BSA_OK;
+  }
+  CHECK(check_r(r));
+  int lq = 0, mk = 0;
+  host_sizes(G, r, &lq, &mk);
+  if (op == BSA_OP_ATTN_FWD) {
+    *bytes = align256(BH * lq * d * 2);
+    return BSA_OK;
+  }
+  if (op == BSA_OP_ATTN_BWD) {
+    *bytes = bwd_ws(BH, lq, d).total;
+    return BSA_OK;
+  }
+  return fail(BSA_ERR_CONFIG, "unknown op %d", op);
+}
+
+int bsa_block_partition(const bsa_geom* g, double r, int32_t* block_off, int32_t* block_tok, int32_t* block_ext,
+                        int32_t* kept_off, void* stream) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_r(r));
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = timed(BSA_K_PARTITION, (block_tok ? 1 : 0) + ((block_off || block_ext || kept_off) ? 1 : 0), st,
+                        [&] { return bsa::launch_partition(G, r, block_off, block_tok, block_ext, kept_off, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "partition");
+  return BSA_OK;
+}
+
+int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q,
+                       const int32_t* kept_off, int32_t* kept_tok, int32_t* donor, double* q_pooled, void* q_packed,
+                       void* stream) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_r(r));
+  CHECK(check_dims(B, Hh, d));
+  if (!Q || !kept_off || !kept_tok || !donor)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "Q, kept_off, kept_tok and donor are required");
+  if (!aligned16(Q) || (q_packed && !aligned16(q_packed))) return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  CHECK(check_device());
+  int lq = 0, mk = 0;
+  host_sizes(G, r, &lq, &mk);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = timed(BSA_K_SELECT_Q, 1, st, [&] {
+    return bsa::launch_select_queries(G, r, B * Hh, d, lq, static_cast<const bsa::bf16*>(Q), kept_off, kept_tok, donor,
+                                      q_pooled, static_cast<bsa::bf16*>(q_packed), st);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "select_queries");
+  return BSA_OK;
+}
+
+int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q, const double* q_pooled,
+                         const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
+                         int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_dims(B, Hh, d));
+  if (k < 1 || k > G.N) return fail(BSA_ERR_CONFIG, "k must be in [1, N=%d] (got %d)", G.N, k);
+  if (!(tau > 0.0 && tau <= 1.0)) return fail(BSA_ERR_CONFIG, "tau must be in (0,1] (got %g)", tau);
+  if (!K || (!Q && !q_pooled) || !q2k_num || !q2k_idx)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "K, Q or q_pooled, q2k_num and q2k_idx are required");
+  if ((k2q_num == nullptr) != (k2q_idx == nullptr))
+    return fail(BSA_ERR_SELECTION_MISMATCH, "k2q_num and k2q_idx must be both given or both NULL");
+  size_t BH = static_cast<size_t>(B) * Hh;
+  SelKvWs w = selkv_ws(G, BH, d);
+  if (!ws || ws_bytes < w.total)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "workspace of %zu bytes < required %zu", ws_bytes, w.total);
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  double* Kc = reinterpret_cast<double*>(base + w.kc);
+  double* Qc = q_pooled ? const_cast<double*>(q_pooled) : reinterpret_cast<double*>(base + w.qc);
+  double* S = reinterpret_cast<double*>(base + w.s);
+  uint32_t* bits = k2q_num ? reinterpret_cast<uint32_t*>(base + w.bits) : nullptr;
+  cudaError_t e = timed(BSA_K_POOL, 1, st, [&] {
+    return bsa::launch_pool(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(K), Kc, st);
+  });
+  if (e == cudaSuccess && !q_pooled)
+    e = timed(BSA_K_POOL, 1, st, [&] {
+      return bsa::launch_pool(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(Q), Qc, st);
+    });
+  if (e == cudaSuccess)
+    e = timed(BSA_K_SCORES, 1, st, [&] { return bsa::launch_scores(G.N, static_cast<int>(BH), d, Qc, Kc, S, st); });
+  if (e == cudaSuccess && bits) e = cudaMemsetAsync(bits, 0, BH * G.N * ((G.N + 31) / 32) * 4, st);
+  double z = 0.0;
+  if (k < G.N) {
+    double u = 1.0 - static_cast<double>(k) / G.N;
+    double lo = 1.0 / (2.0 * G.N), hi = 1.0 - 1.0 / (2.0 * G.N);
+    u = u < lo ? lo : (u > hi ? hi : u);
+    z = bsa::normal_quantile(u);
+  }
+  if (e == cudaSuccess)
+    e = timed(BSA_K_ADMIT, 1, st, [&] {
+      return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, q2k_num, q2k_idx, thresh, bits, st);
+    });
+  if (e == cudaSuccess && bits)
+    e = timed(BSA_K_K2Q, 1, st, [&] { return bsa::launch_k2q(G.N, static_cast<int>(BH), bits, k2q_num, k2q_idx, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "select_kv_blocks");
+  return BSA_OK;
+}
+
+int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
+                 const void* V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
+                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, void* O,
+                 float* lse, void* ws, size_t ws_bytes, void* stream) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_r(r));
+  CHECK(check_dims(B, Hh, d));
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(BSA_ERR_CONFIG, "scale must be positive and finite");
+  if (!K || !V || !kept_off || !kept_tok || !donor || !q2k_num || !q2k_idx || !O || !lse || (!q_packed && !Q))
+    return fail(BSA_ERR_SELECTION_MISMATCH, "missing required pointer");
+  if (!aligned16(K) || !aligned16(V) || !aligned16(O) || (Q && !aligned16(Q)) || (q_packed && !aligned16(q_packed)))
+    return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  int Lq = 0, SR = 0;
+  CHECK(check_attn_geom(G, r, &Lq, &SR));
+  size_t BH = static_cast<size_t>(B) * Hh;
+  const bsa::bf16* Qs = static_cast<const bsa::bf16*>(q_packed);
+  if (!Qs) {
+    size_t need = align256(BH * Lq * d * 2);
+    if (!ws || ws_bytes < need)
+      return fail(BSA_ERR_SELECTION_MISMATCH, "q_packed is NULL and workspace %zu < %zu bytes", ws_bytes, need);
+  }
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (!Qs) {
+    bsa::bf16* dst = static_cast<bsa::bf16*>(ws);
+    e = timed(BSA_K_GATHER, 1, st, [&] {
+      return bsa::launch_gather_rows(static_cast<int>(BH), G.L, Lq, d, static_cast<const bsa::bf16*>(Q), kept_tok, dst,
+                                     st);
+    });
+    Qs = dst;
+  }
+  bsa::FwdArgs a;
+  a.g = G;
+  a.BH = static_cast<int>(BH);
+  a.d = d;
+  a.Lq = Lq;
+  a.SR = SR;
+  a.Q = static_cast<const bsa::bf16*>(Q);
+  a.K = static_cast<const bsa::bf16*>(K);
+  a.V = static_cast<const bsa::bf16*>(V);
+  a.Qs = Qs;
+  a.kept_off = kept_off;
+  a.kept_tok = kept_tok;
+  a.donor = donor;
+  a.q2k_num = q2k_num;
+  a.q2k_idx = q2k_idx;
+  a.scale = scale;
+  a.O = static_cast<bsa::bf16*>(O);
+  a.lse = lse;
+  if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
+  if (e == cudaSuccess) e = timed(BSA_K_FILL, 1, st, [&] { return bsa::launch_fill(a.BH, G.L, d, donor, a.O, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "attn_fwd");
+  return BSA_OK;
+}
+
+int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
+                 const void* V, const void* O, const void* dO, const void* q_packed, const int32_t* kept_off,
+                 const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
+                 const float* lse, float scale, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                 void* stream) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_r(r));
+  CHECK(check_dims(B, Hh, d));
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(BSA_ERR_CONFIG, "scale must be positive and finite");
+  if (!K || !V || !O || !dO || !kept_off || !kept_tok || !donor || !k2q_num || !k2q_idx || !lse || !dQ || !dK ||
+      !dV || (!q_packed && !Q))
+    return fail(BSA_ERR_SELECTION_MISMATCH, "missing required pointer");
+  const void* ptrs[] = {Q, K, V, O, dO, q_packed, dQ, dK, dV};
+  for (const void* ptr : ptrs)
+    if (ptr && !aligned16(ptr)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  int Lq = 0, SR = 0;
+  CHECK(check_attn_geom(G, r, &Lq, &SR));
+  size_t BH = static_cast<size_t>(B) * Hh;
+  BwdWs w = bwd_ws(BH, Lq, d);
+  if (!ws || ws_bytes < w.total)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "workspace of %zu bytes < required %zu", ws_bytes, w.total);
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  cudaError_t e = cudaSuccess;
+  const bsa::bf16* Qs = static_cast<const bsa::bf16*>(q_packed);
+  if (!Qs) {
+    bsa::bf16* dst = reinterpret_cast<bsa::bf16*>(base + w.qs);
+    e = timed(BSA_K_GATHER, 1, st, [&] {
+      return bsa::launch_gather_rows(static_cast<int>(BH), G.L, Lq, d, static_cast<const bsa::bf16*>(Q), kept_tok, dst,
+                                     st);
+    });
+    Qs = dst;
+  }
+  bsa::BwdArgs a;
+  a.g = G;
+  a.BH = static_cast<int>(BH);
+  a.d = d;
+  a.Lq = Lq;
+  a.SR = SR;
+  a.Q = static_cast<const bsa::bf16*>(Q);
+  a.K = static_cast<const bsa::bf16*>(K);
+  a.V = static_cast<const bsa::bf16*>(V);
+  a.O = static_cast<const bsa::bf16*>(O);
+  a.dO = static_cast<const bsa::bf16*>(dO);
+  a.Qs = Qs;
+  a.kept_off = kept_off;
+  a.kept_tok = kept_tok;
+  a.donor = donor;
+  a.k2q_num = k2q_num;
+  a.k2q_idx = k2q_idx;
+  a.lse = lse;
+  a.scale = scale;
+  a.dQ = static_cast<bsa::bf16*>(dQ);
+  a.dK = static_cast<bsa::bf16*>(dK);
+  a.dV = static_cast<bsa::bf16*>(dV);
+  a.dOs = reinterpret_cast<bsa::bf16*>(base + w.dos);
+  a.Dvec = reinterpret_cast<float*>(base + w.dv);
+  a.dQacc = reinterpret_cast<float*>(base + w.dq);
+  if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
+  if (e == cudaSuccess) e = timed(BSA_K_ATTN_BWD, 1, st, [&] { return bsa::launch_bwd_main(a, st); });
+  if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 2, st, [&] { return bsa::launch_bwd_finalize(a, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "attn_bwd");
+  return BSA_OK;
+}
+
+int64_t bsa_launch_count(void) { return g_launches; }
+
+int bsa_timing_enable(int on) {
+  g_timing = on != 0;
+  return BSA_OK;
+}
+
+int bsa_timing_read(double* ms, int32_t* launches, int32_t n) {
+  if (ms)
+    for (int i = 0; i < n; ++i) ms[i] = 0.0;
+  if (launches)
+    for (int i = 0; i < n; ++i) launches[i] = 0;
+  int rc = BSA_OK;
+  for (TimedRec& r : g_recs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess && rc == BSA_OK) rc = cuda_fail(e, "bsa_timing_read");
+    if (r.id < n) {
+      if (ms) ms[r.id] += t;
+      if (launches) launches[r.id] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_recs.clear();
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,452 @@
+// attn_fwd.cu — a7: block-sparse attention forward over kept queries x admitted KV blocks
+// (Eq.5; kernel design P:204-210: "each Q block records its attended KV blocks
+// with q2k_num and q2k_index"), followed by the fill that restores length L.
+//
+// B200 design:
+//  * One CTA per query tile = G consecutive query blocks, each in its own slot of SR = 128/G rows of
+//    the packed Q^s (kept queries, block-major). Q^s slots arrive by 2D TMA (128B swizzle).
+//  * The CTA walks the ascending UNION of its blocks' KV lists. Every KV block j is one 5D TMA box
+//    (64 channels x cw x ch x ct) straight from the raster [B,Hh,L,d] tensor: no permuted copy of
+//    K/V; out-of-grid (ragged edge) rows arrive as zeros and are masked to -inf.
+//  * S = Q^s K_j^T (M=128, N=BT) and O += P V_j (M=128, N=d) are tcgen05.mma kind::f16 with fp32
+//    accumulators in TMEM, issued by one thread; S is double-buffered in TMEM so QK(j+1) overlaps the
+//    softmax of j. Rows whose block did not admit j write P = 0 (their MMA work is the union waste).
+//  * Softmax: 128 threads, thread == TMEM lane == query row; online softmax in fp32 (log2 domain),
+//    O rescaled in TMEM only when the running max grows by more than 2^8 (exact: same final ratio).
+//  * Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 softmax/epilogue.
+#include <cmath>
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace bsa {
+
+struct FwdParams {
+  CUtensorMap mQs;  // 2D {d, BH*Lq}, box {64, SR}
+  CUtensorMap mK;   // 5D {d, W, H, T, BH}, box {64, cw, ch, ct, 1}
+  CUtensorMap mV;
+  Geo g;
+  int Lq, SR, G;
+  const int* kept_off;
+  const int* kept_tok;
+  const int* q2k_num;
+  const int* q2k_idx;
+  float scale_log2;  // scale * log2(e)
+  bf16* O;
+  float* lse;
+};
+
+constexpr int FWD_THREADS = 256;
+constexpr int FWD_STAGES = 3;
+constexpr int MAX_N = 4096;
+constexpr int MAX_G = 16;
+
+template <int D, int BT>
+struct FwdSmem {
+  static constexpr int NCB = D / 64;
+  static constexpr int Q_BYTES = 128 * D * 2;
+  static constexpr int KV_BYTES = BT * D * 2;  // one K or V tile
+  static constexpr int P_BYTES = 128 * 128;    // [128][64] bf16, 128B rows
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + FWD_STAGES * KV_BYTES;
+  static constexpr int OFF_P = OFF_V + FWD_STAGES * KV_BYTES;
+  static constexpr int OFF_BITS = OFF_P + 2 * P_BYTES;
+  static constexpr int BITS_BYTES = MAX_G * (MAX_N / 32) * 4;
+  static constexpr int OFF_ULIST = OFF_BITS + BITS_BYTES + 32 * 4;  // + union words
+  static constexpr int ULIST_BYTES = MAX_N * 2;
+  static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D, int BT>
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_constant__ FwdParams p) {
+  using SM = FwdSmem<D, BT>;
+  constexpr int NCB = SM::NCB;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm + SM::OFF_Q;
+  uint8_t* sK = sm + SM::OFF_K;
+  uint8_t* sV = sm + SM::OFF_V;
+  uint8_t* sP = sm + SM::OFF_P;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(sm + SM::OFF_BITS);
+  uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
+
+  __shared__ __align__(8) uint64_t bar_q, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
+      bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o, bar_o_final;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
+
+  const Geo& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, bh = blockIdx.y;
+  const int G = p.G, SR = p.SR;
+  const int NW = (g.N + 31) >> 5;
+
+  if (tid == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < FWD_STAGES; ++s) { mbar_init(&bar_kv_full[s], 1); mbar_init(&bar_kv_empty[s], 1); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_s_full[b], 1);
+      mbar_init(&bar_s_free[b], 128);
+      mbar_init(&bar_p_full[b], 128);
+      mbar_init(&bar_p_free[b], 1);
+    }
+    mbar_init(&bar_o, 1);
+    mbar_init(&bar_o_final, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&s_tmem, 256);
+  if (tid < G) {
+    int qb = tile * G + tid;
+    s_qb[tid] = qb < g.N ? qb : -1;
+    s_nk[tid] = qb < g.N ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
+    s_koff[tid] = qb < g.N ? p.kept_off[qb] : 0;
+  }
+  for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
+  __syncthreads();
+  // admission bitmap of each slot (q2k lists)
+  for (int gi = 0; gi < G; ++gi) {
+    int qb = s_qb[gi];
+    if (qb < 0) continue;
+    size_t row = static_cast<size_t>(bh) * g.N + qb;
+    int num = p.q2k_num[row];
+    const int* idx = p.q2k_idx + row * g.N;
+    for (int a = tid; a < num; a += FWD_THREADS) {
+      int j = idx[a];
+      atomicOr(&bits[gi * NW + (j >> 5)], 1u << (j & 31));
+    }
+  }
+  __syncthreads();
+  // ascending union list (one warp)
+  if (warp == 0) {
+    int cnt = 0;
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+      int w = w0 + lane;
+      uint32_t v = 0u;
+      if (w < NW)
+        for (int gi = 0; gi < G; ++gi) v |= bits[gi * NW + w];
+      int c = __popc(v), incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += a;
+      }
+      int pos = cnt + incl - c;
+      while (v) {
+        int bit = __ffs(v) - 1;
+        ulist[pos++] = static_cast<uint16_t>(w * 32 + bit);
+        v &= v - 1;
+      }
+      cnt += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_U = cnt;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = s_tmem;
+  const int U = s_U;
+  constexpr uint32_t KV_BYTES = SM::KV_BYTES;
+
+  if (warp == 0) {
+    // ============================ TMA producer
+    if (lane == 0) {
+      tma_prefetch(&p.mQs);
+      tma_prefetch(&p.mK);
+      tma_prefetch(&p.mV);
+      int nvalid = 0;
+      for (int gi = 0; gi < G; ++gi) nvalid += (s_qb[gi] >= 0);
+      mbar_expect_tx(&bar_q, static_cast<uint32_t>(nvalid * NCB * SR * 128));
+      for (int gi = 0; gi < G; ++gi) {
+        if (s_qb[gi] < 0) continue;
+        int row0 = bh * p.Lq + s_koff[gi];
+        for (int cb = 0; cb < NCB; ++cb) tma_load_2d(sQ + cb * 16384 + gi * SR * 128, &p.mQs, &bar_q, cb * 64, row0);
+      }
+      for (int u = 0; u < U; ++u) {
+        int s = u % FWD_STAGES;
+        mbar_wait(&bar_kv_empty[s], ((u / FWD_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&bar_kv_full[s], 2 * KV_BYTES);
+        int j = ulist[u];
+        int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+        for (int cb = 0; cb < NCB; ++cb) {
+          tma_load_5d(sK + s * KV_BYTES + cb * BT * 128, &p.mK, &bar_kv_full[s], cb * 64, bw * g.cw, bhh * g.ch,
+                      bt * g.ct, bh);
+          tma_load_5d(sV + s * KV_BYTES + cb * BT * 128, &p.mV, &bar_kv_full[s], cb * 64, bw * g.cw, bhh * g.ch,
+                      bt * g.ct, bh);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer (single thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = umma_idesc_bf16(128, BT, 0, 0);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, D, 0, 1);
+      const uint32_t tO = tbase, tS = tbase + D;
+      mbar_wait(&bar_q, 0);
+      auto issue_qk = [&](int u) {
+        int s = u % FWD_STAGES, sb = u & 1;
+        mbar_wait(&bar_kv_full[s], (u / FWD_STAGES) & 1);
+        if (u >= 2) mbar_wait(&bar_s_free[sb], ((u - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + s * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          int cb = kk >> 2, ko = (kk & 3) * 32;
+          uint64_t a = umma_desc_sw128(qa + cb * 16384 + ko, 16, 1024);
+          uint64_t b = umma_desc_sw128(kb + cb * BT * 128 + ko, 16, 1024);
+          umma_ss(tS + sb * BT, a, b, idesc_qk, kk > 0);
+        }
+        umma_commit(&bar_s_full[sb]);
+      };
+      issue_qk(0);
+      for (int u = 0; u < U; ++u) {
+        if (u + 1 < U) issue_qk(u + 1);
+        int pb = u & 1, s = u % FWD_STAGES;
+        mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sP + pb * SM::P_BYTES), vb = smem_u32(sV + s * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk) {
+          uint64_t a = umma_desc_sw128(pa + kk * 32, 16, 1024);
+          uint64_t b = umma_desc_sw128(vb + kk * 2048, BT * 128, 1024);
+          umma_ss(tO, a, b, idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&bar_kv_empty[s]);
+        umma_commit(&bar_p_free[pb]);
+        umma_commit(&bar_o);
+      }
+      umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
+    }
+  } else if (warp >= 4) {
+    // ============================ softmax + epilogue (thread == query row == TMEM lane)
+    const int q4 = warp - 4;
+    const int row = q4 * 32 + lane;
+    const int gi = row / SR, lr = row % SR;
+    const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
+    const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
+    const uint32_t* mybits = bits + (gi < G ? gi : 0) * NW;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int u = 0; u < U; ++u) {
+      const int sb = u & 1, pb = u & 1;
+      const int j = ulist[u];
+      const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
+      // key validity of block j (ragged edge blocks: only actual tokens, C23)
+      const Box xj = block_box(g, j);
+      mbar_wait(&bar_s_full[sb], (u >> 1) & 1);
+      tc_fence_after();
+      float sv[BT];
+#pragma unroll
+      for (int c = 0; c < BT; c += 16) tmem_ld16(trow + D + sb * BT + c, sv + c);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bar_s_free[sb]);
+      float alpha = 1.f;
+      bool need_rescale = false;
+      if (admit) {
+        float mx = -INFINITY;
+        const bool full = xj.e[0] == g.ct && xj.e[1] == g.ch && xj.e[2] == g.cw;
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < BT; ++c) {
+            sv[c] *= p.scale_log2;
+            mx = fmaxf(mx, sv[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BT; ++c) {
+            int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
+            bool kv = lt < xj.e[0] && lh < xj.e[1] && lw < xj.e[2];
+            sv[c] = kv ? sv[c] * p.scale_log2 : -INFINITY;
+            mx = fmaxf(mx, sv[c]);
+          }
+        }
+        if (mx > m_run + 8.f) {  // conditional rescale: keep the stale max unless it grew by > 2^8
+          if (m_run != -INFINITY) { alpha = ex2(m_run - mx); need_rescale = true; }
+          l_run *= alpha;
+          m_run = mx;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < BT; ++c) { sv[c] = ex2(sv[c] - m_run); sum += sv[c]; }
+        l_run += sum;
+      } else {
+#pragma unroll
+        for (int c = 0; c < BT; ++c) sv[c] = 0.f;
+      }
+      // P buffer pb is free once PV(u-2) completed. Waiting here first also bounds bar_o to at most
+      // one phase behind PV(u-1), which makes the parity wait below unambiguous.
+      if (u >= 2) mbar_wait(&bar_p_free[pb], ((u - 2) >> 1) & 1);
+      // O rescale in TMEM (needs PV(u-1) complete); warp-collective access
+      if (__any_sync(0xffffffffu, need_rescale)) {
+        mbar_wait(&bar_o, (u - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D; c += 16) {
+          float ov[16];
+          tmem_ld16(trow + c, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ov[e] *= alpha;
+          tmem_st16(trow + c, ov);
+        }
+        tmem_wait_st();
+      }
+      // P row -> smem (bf16, 128B-swizzled [128][64])
+      uint8_t* prow = sP + pb * SM::P_BYTES;
+#pragma unroll
+      for (int c16 = 0; c16 < BT / 8; ++c16) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(sv[c16 * 8 + 0], sv[c16 * 8 + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(sv[c16 * 8 + 2], sv[c16 * 8 + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(sv[c16 * 8 + 4], sv[c16 * 8 + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(sv[c16 * 8 + 6], sv[c16 * 8 + 7]);
+        uint4 v;
+        v.x = *reinterpret_cast<uint32_t*>(&h0);
+        v.y = *reinterpret_cast<uint32_t*>(&h1);
+        v.z = *reinterpret_cast<uint32_t*>(&h2);
+        v.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(prow + sw128_off(row, c16)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bar_p_full[pb]);
+    }
+    // epilogue: O^s = O / l, scattered to the kept token's raster row; LSE in natural log
+    mbar_wait(&bar_o_final, 0);
+    tc_fence_after();
+    const float inv = valid ? 1.f / l_run : 0.f;
+    size_t prow_idx = 0;
+    bf16* orow = nullptr;
+    if (valid) {
+      prow_idx = static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr;
+      int tok = p.kept_tok[prow_idx];
+      orow = p.O + (static_cast<size_t>(bh) * g.L + tok) * D;
+      p.lse[prow_idx] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+    }
+#pragma unroll 1
+    for (int c = 0; c < D; c += 16) {
+      float ov[16];
+      tmem_ld16(trow + c, ov);
+      tmem_wait_ld();
+      if (valid) {
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(ov[2 * e] * inv, ov[2 * e + 1] * inv);
+          w[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(orow + c) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tbase, 256);
+}
+
+// ------------------------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2D row map over a packed [rows, d] bf16 matrix, box {64, box_rows}, 128B swizzle.
+bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
+  cuuint64_t str[1] = {static_cast<cuuint64_t>(d) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 5D block map over a raster [BH, T, H, W, d] bf16 tensor, box {64, cw, ch, ct, 1}, 128B swizzle.
+bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int BH) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[5] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.H),
+                        static_cast<cuuint64_t>(g.T), static_cast<cuuint64_t>(BH)};
+  cuuint64_t rs = static_cast<cuuint64_t>(d) * 2;
+  cuuint64_t str[4] = {rs, rs * g.W, rs * g.W * g.H, rs * g.W * g.H * g.T};
+  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(g.cw), static_cast<cuuint32_t>(g.ch),
+                       static_cast<cuuint32_t>(g.ct), 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, int BT>
+static cudaError_t run_fwd(const FwdParams& p, int ntiles, int BH, cudaStream_t st) {
+  constexpr int smem = FwdSmem<D, BT>::TOTAL;
+  cudaError_t e = cudaFuncSetAttribute(k_attn_fwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_attn_fwd<D, BT><<<dim3(ntiles, BH), FWD_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
+  FwdParams p;
+  memset(&p, 0, sizeof(p));
+  p.g = a.g;
+  p.Lq = a.Lq;
+  p.SR = a.SR;
+  p.G = 128 / a.SR;
+  p.kept_off = a.kept_off;
+  p.kept_tok = a.kept_tok;
+  p.q2k_num = a.q2k_num;
+  p.q2k_idx = a.q2k_idx;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  p.O = a.O;
+  p.lse = a.lse;
+  if (!make_map_2d(&p.mQs, a.Qs, a.d, static_cast<size_t>(a.BH) * a.Lq, a.SR)) return cudaErrorInvalidValue;
+  if (!make_map_5d(&p.mK, a.K, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
+  if (!make_map_5d(&p.mV, a.V, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
+  int ntiles = (a.g.N + p.G - 1) / p.G;
+  if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
+  if (a.d == 128 && a.g.BT == 32) return run_fwd<128, 32>(p, ntiles, a.BH, st);
+  if (a.d == 64 && a.g.BT == 64) return run_fwd<64, 64>(p, ntiles, a.BH, st);
+  if (a.d == 64 && a.g.BT == 32) return run_fwd<64, 32>(p, ntiles, a.BH, st);
+  return cudaErrorInvalidValue;
+}
+
+// Fill (reading C9): O[t] = O^s[donor(t)] for pruned t; one 16-byte chunk per thread.
+__global__ void k_fill(int BH, int L, int d, const int* __restrict__ donor, bf16* __restrict__ O) {
+  size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int vpr = d / 8;
+  if (v >= static_cast<size_t>(BH) * L * vpr) return;
+  size_t rowi = v / vpr;
+  int c = static_cast<int>(v % vpr) * 8;
+  size_t bh = rowi / L;
+  int t = static_cast<int>(rowi % L);
+  int dn = donor[rowi];
+  if (dn != t)
+    *reinterpret_cast<uint4*>(O + rowi * d + c) = *reinterpret_cast<const uint4*>(O + (bh * L + dn) * d + c);
+}
+
+cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st) {
+  size_t total = static_cast<size_t>(BH) * L * (d / 8);
+  k_fill<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, L, d, donor, O);
+  return cudaGetLastError();
+}
+
+}  // namespace bsa

@@ -1,0 +1,86 @@
+// kernels.h — internal launchers of libbsa (not part of the C ABI; see include/bsa.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "geom.cuh"
+
+namespace bsa {
+
+using bf16 = __nv_bfloat16;
+
+// a1 partition
+cudaError_t launch_partition(const Geo& g, double r, int* block_off, int* block_tok, int* block_ext, int* kept_off,
+                             cudaStream_t st);
+// a2+a3 query selection (one pass over Q)
+cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, const bf16* Q, const int* kept_off,
+                                  int* kept_tok, int* donor, double* q_pooled, bf16* q_packed, cudaStream_t st);
+// a2 block pooling in fp64
+cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, cudaStream_t st);
+// a4 pooled block scores S[bh][i][j] = Qc[i].Kc[j] / sqrt(d)
+cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st);
+// a5+a6 threshold + admission per row; sets bit i of kvbits[bh][j] for every admitted (i, j)
+cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int* q2k_num, int* q2k_idx,
+                         double* thresh, uint32_t* kvbits, cudaStream_t st);
+// transpose of the admission: k2q lists (ascending query blocks per KV block)
+cudaError_t launch_k2q(int N, int BH, const uint32_t* kvbits, int* k2q_num, int* k2q_idx, cudaStream_t st);
+
+// gather Q^s rows (kept queries) into packed [BH, Lq, d]
+cudaError_t launch_gather_rows(int BH, int L, int Lq, int d, const bf16* X, const int* kept_tok, bf16* out,
+                               cudaStream_t st);
+
+// a7 forward: tcgen05 sparse attention over packed Q^s, then the donor fill
+struct FwdArgs {
+  Geo g;
+  int BH, d, Lq, SR;  // SR = query rows per slot (power of two >= max kept per block)
+  const bf16* Q;      // raster [BH, L, d]
+  const bf16* K;
+  const bf16* V;
+  const bf16* Qs;     // packed [BH, Lq, d]
+  const int* kept_off;
+  const int* kept_tok;
+  const int* donor;
+  const int* q2k_num;
+  const int* q2k_idx;
+  float scale;
+  bf16* O;
+  float* lse;
+};
+cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st);
+
+// a8 backward
+struct BwdArgs {
+  Geo g;
+  int BH, d, Lq, SR;
+  const bf16* Q;
+  const bf16* K;
+  const bf16* V;
+  const bf16* O;
+  const bf16* dO;
+  const bf16* Qs;      // packed
+  const int* kept_off;
+  const int* kept_tok;
+  const int* donor;
+  const int* k2q_num;
+  const int* k2q_idx;
+  const float* lse;
+  float scale;
+  bf16* dQ;
+  bf16* dK;
+  bf16* dV;
+  // workspace
+  bf16* dOs;     // packed [BH, Lq, d]
+  float* Dvec;   // [BH, Lq]
+  float* dQacc;  // [BH, Lq, d]
+};
+cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st);
+cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st);
+cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st);
+
+// host helpers
+double normal_quantile(double u);  // Phi^-1, Acklam initial guess + Halley refinement
+int slot_rows(int max_block_kept);  // power of two >= max(8, max_block_kept)
+
+}  // namespace bsa

@@ -1,0 +1,593 @@
+// select.cu — a1..a6 of the BSA hot path: partition, pooling, query selection (Eq.2),
+// pooled scores, statistical threshold (Eq.3) and cumulative admission (Eq.4).
+//
+// Precision contract: every decision that produces an integer (kept set, donor,
+// candidate set, admitted prefix) is taken in fp64 on the exact bf16 input values, with dot products
+// summed sequentially over channels with explicitly rounded multiply/add (no FMA contraction), so
+// pooled means, norms, cosines and pooled scores are bit-identical to a plain sequential fp64
+// evaluation. Row statistics (mean, std, softmax mass) use tree reductions; their last-ulp
+// differences are what the near-tie protocol (reading C24) counts.
+#include <cfloat>
+#include <cmath>
+#include "kernels.h"
+
+namespace bsa {
+
+// ------------------------------------------------------------------------------------ a1
+// One CTA scans the blocks: sizes, extents, per-block kept counts and their prefix sums.
+__global__ void __launch_bounds__(1024) k_partition_blocks(Geo g, double r, int* block_off, int* block_ext,
+                                                           int* kept_off) {
+  __shared__ int s_sz[32], s_kp[32];
+  __shared__ int carry_sz, carry_kp;
+  if (threadIdx.x == 0) { carry_sz = 0; carry_kp = 0; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < g.N; base += blockDim.x) {
+    int b = base + threadIdx.x;
+    int sz = 0, kp = 0;
+    if (b < g.N) {
+      Box x = block_box(g, b);
+      sz = box_size(x);
+      kp = block_kept(g, x, r);
+      if (block_ext) { block_ext[3 * b] = x.e[0]; block_ext[3 * b + 1] = x.e[1]; block_ext[3 * b + 2] = x.e[2]; }
+    }
+    int isz = sz, ikp = kp;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, isz, o), c = __shfl_up_sync(0xffffffffu, ikp, o);
+      if (lane >= o) { isz += a; ikp += c; }
+    }
+    if (lane == 31) { s_sz[warp] = isz; s_kp[warp] = ikp; }
+    __syncthreads();
+    if (warp == 0) {
+      int a = s_sz[lane], c = s_kp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a2 = __shfl_up_sync(0xffffffffu, a, o), c2 = __shfl_up_sync(0xffffffffu, c, o);
+        if (lane >= o) { a += a2; c += c2; }
+      }
+      s_sz[lane] = a; s_kp[lane] = c;
+    }
+    __syncthreads();
+    int wsz = warp ? s_sz[warp - 1] : 0, wkp = warp ? s_kp[warp - 1] : 0;
+    if (b < g.N) {
+      if (block_off) block_off[b + 1] = carry_sz + wsz + isz;
+      if (kept_off) kept_off[b + 1] = carry_kp + wkp + ikp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { carry_sz += s_sz[31]; carry_kp += s_kp[31]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (block_off) block_off[0] = 0;
+    if (kept_off) kept_off[0] = 0;
+  }
+}
+
+// Token n -> its slot in block_tok (closed-form block offsets: blocks before (bt,bh,bw) hold
+// bt*ct*H*W + et*(bh*ch*W) + et*eh*(bw*cw) tokens).
+__global__ void k_partition_tokens(Geo g, int* block_tok) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.L) return;
+  int t = n / (g.H * g.W), h = (n / g.W) % g.H, w = n % g.W;
+  int bt = t / g.ct, bh = h / g.ch, bw = w / g.cw;
+  int et = min_i(g.ct, g.T - bt * g.ct), eh = min_i(g.ch, g.H - bh * g.ch), ew = min_i(g.cw, g.W - bw * g.cw);
+  int off = bt * g.ct * g.H * g.W + et * (bh * g.ch) * g.W + et * eh * (bw * g.cw);
+  int local = ((t - bt * g.ct) * eh + (h - bh * g.ch)) * ew + (w - bw * g.cw);
+  block_tok[off + local] = n;
+}
+
+cudaError_t launch_partition(const Geo& g, double r, int* block_off, int* block_tok, int* block_ext, int* kept_off,
+                             cudaStream_t st) {
+  if (block_off || block_ext || kept_off) k_partition_blocks<<<1, 1024, 0, st>>>(g, r, block_off, block_ext, kept_off);
+  if (block_tok) k_partition_tokens<<<(g.L + 255) / 256, 256, 0, st>>>(g, block_tok);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ a2 + a3
+// Exactly rounded fp64 helpers (no FMA contraction): sequential sums over channels.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+template <int D>
+__device__ __forceinline__ double dot_rows(const bf16* a, const bf16* b) {
+  double s = 0.0;
+#pragma unroll 4
+  for (int c = 0; c < D; c += 8) {
+    uint4 va = *reinterpret_cast<const uint4*>(a + c);
+    uint4 vb = *reinterpret_cast<const uint4*>(b + c);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&va);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 fa = __bfloat1622float2(pa[k]), fb = __bfloat1622float2(pb[k]);
+      s = dadd(s, dmul((double)fa.x, (double)fb.x));
+      s = dadd(s, dmul((double)fa.y, (double)fb.y));
+    }
+  }
+  return s;
+}
+
+// One CTA (128 threads) per (bh, block). Shared layout: rows padded to D+8 bf16 so that
+// lane-strided 16-byte row reads are bank-conflict free.
+template <int D>
+__global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq, const bf16* __restrict__ Q,
+                                                        const int* __restrict__ kept_off, int* __restrict__ kept_tok,
+                                                        int* __restrict__ donor, double* __restrict__ q_pooled,
+                                                        bf16* __restrict__ q_packed) {
+  constexpr int DS = D + 8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int b = blockIdx.x, bh = blockIdx.y;
+  const int BTn = g.BT;
+  bf16* sq = reinterpret_cast<bf16*>(smem);                          // [BT][DS]
+  double* nrm = reinterpret_cast<double*>(sq + BTn * DS);            // [BT]
+  double* cs = nrm + BTn;                                            // [BT]
+  int* tok = reinterpret_cast<int*>(cs + BTn);                       // [BT]
+  int* unit = tok + BTn;                                             // [BT]
+  int* cen = unit + BTn;                                             // [BT] centre local idx of my unit
+  int* keep = cen + BTn;                                             // [BT] 1 if kept
+  int* mcnt = keep + BTn;                                            // [BT] keep count of my unit
+  int* plist = mcnt + BTn;                                           // [BT] pruned local indices
+  __shared__ int s_np;
+
+  const Box x = block_box(g, b);
+  const int n = box_size(x);
+  const size_t head = static_cast<size_t>(bh) * g.L;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tok[i] = box_token(g, x, i);
+  __syncthreads();
+  // rows -> smem (16-byte vectors)
+  constexpr int VPR = D / 8;
+  for (int v = threadIdx.x; v < n * VPR; v += blockDim.x) {
+    int i = v / VPR, c = (v % VPR) * 8;
+    *reinterpret_cast<uint4*>(sq + i * DS + c) = *reinterpret_cast<const uint4*>(Q + (head + tok[i]) * D + c);
+  }
+  __syncthreads();
+  // a2: pooled mean, summed in ascending token order
+  if (q_pooled) {
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s = dadd(s, (double)__bfloat162float(sq[i * DS + c]));
+      q_pooled[(static_cast<size_t>(bh) * g.N + b) * D + c] = s / (double)n;
+    }
+  }
+  // norms, unit membership, centre of the unit (C3: floor-midpoint of the unit's actual extent)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const bf16* qi = sq + i * DS;
+    nrm[i] = sqrt(dot_rows<D>(qi, qi));
+    int lw = i % x.e[2], lh = (i / x.e[2]) % x.e[1], lt = i / (x.e[2] * x.e[1]);
+    int nu[3];
+    unit_grid(g, x, nu);
+    int a = lt / g.ut, bb = lh / g.uh, c = lw / g.uw;
+    unit[i] = (a * nu[1] + bb) * nu[2] + c;
+    int et = min_i(g.ut, x.e[0] - a * g.ut), eh = min_i(g.uh, x.e[1] - bb * g.uh), ew = min_i(g.uw, x.e[2] - c * g.uw);
+    int ct_ = a * g.ut + et / 2, ch_ = bb * g.uh + eh / 2, cw_ = c * g.uw + ew / 2;
+    cen[i] = (ct_ * x.e[1] + ch_) * x.e[2] + cw_;
+    mcnt[i] = keep_count(r, et * eh * ew);
+  }
+  __syncthreads();
+  // Eq.2: c_i = cos(q_centre, q_i); c_centre := 1; zero norm -> 0 (C4)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int c0 = cen[i];
+    double c;
+    if (i == c0) c = 1.0;
+    else if (nrm[c0] == 0.0 || nrm[i] == 0.0) c = 0.0;
+    else c = dot_rows<D>(sq + c0 * DS, sq + i * DS) / (nrm[c0] * nrm[i]);
+    cs[i] = c;
+  }
+  __syncthreads();
+  // rank by (c ascending, token ascending) inside the unit; keep the first m_u (C5, C7)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < n; ++j)
+      if (unit[j] == unit[i] && (cs[j] < cs[i] || (cs[j] == cs[i] && j < i))) ++rank;  // local order == token order
+    keep[i] = rank < mcnt[i];
+  }
+  if (threadIdx.x == 0) s_np = 0;
+  __syncthreads();
+  // kept outputs: block-major, ascending token inside the block
+  const int koff = kept_off[b];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (keep[i]) {
+      int pos = 0;
+      for (int j = 0; j < i; ++j) pos += keep[j];
+      size_t prow = static_cast<size_t>(bh) * Lq + koff + pos;
+      kept_tok[prow] = tok[i];
+      donor[head + tok[i]] = tok[i];
+      if (q_packed)
+        for (int c = 0; c < D; c += 8)
+          *reinterpret_cast<uint4*>(q_packed + prow * D + c) = *reinterpret_cast<const uint4*>(sq + i * DS + c);
+    } else {
+      plist[atomicAdd(&s_np, 1)] = i;
+    }
+  }
+  __syncthreads();
+  // donors (C9): warp per pruned token, lanes over kept candidates of the same unit;
+  // argmax cos(q_p, q_j), ties -> lowest token
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pi = warp; pi < s_np; pi += 4) {
+    const int p = plist[pi];
+    double best = -DBL_MAX;
+    int arg = INT_MAX;
+    for (int j = lane; j < n; j += 32) {
+      if (!keep[j] || unit[j] != unit[p]) continue;
+      double c = (nrm[p] == 0.0 || nrm[j] == 0.0) ? 0.0 : dot_rows<D>(sq + p * DS, sq + j * DS) / (nrm[p] * nrm[j]);
+      if (c > best || (c == best && j < arg)) { best = c; arg = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    if (lane == 0) donor[head + tok[p]] = tok[arg];
+  }
+}
+
+static size_t select_smem(int BT, int D) {
+  return static_cast<size_t>(BT) * (D + 8) * 2 + static_cast<size_t>(BT) * 16 + static_cast<size_t>(BT) * 6 * 4;
+}
+
+cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, const bf16* Q, const int* kept_off,
+                                  int* kept_tok, int* donor, double* q_pooled, bf16* q_packed, cudaStream_t st) {
+  dim3 grid(g.N, BH);
+  size_t sm = select_smem(g.BT, d);
+  if (d == 128) {
+    cudaFuncSetAttribute(k_select_queries<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_select_queries<128><<<grid, 128, sm, st>>>(g, r, Lq, Q, kept_off, kept_tok, donor, q_pooled, q_packed);
+  } else {
+    cudaFuncSetAttribute(k_select_queries<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_select_queries<64><<<grid, 128, sm, st>>>(g, r, Lq, Q, kept_off, kept_tok, donor, q_pooled, q_packed);
+  }
+  return cudaGetLastError();
+}
+
+// a2 for K: fp64 block means (exact sums of bf16 in ascending token order)
+template <int D>
+__global__ void __launch_bounds__(D) k_pool(Geo g, const bf16* __restrict__ X, double* __restrict__ Xc) {
+  const int b = blockIdx.x, bh = blockIdx.y, c = threadIdx.x;
+  const Box x = block_box(g, b);
+  const int n = box_size(x);
+  const size_t head = static_cast<size_t>(bh) * g.L;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = dadd(s, (double)__bfloat162float(X[(head + box_token(g, x, i)) * D + c]));
+  Xc[(static_cast<size_t>(bh) * g.N + b) * D + c] = s / (double)n;
+}
+
+cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, cudaStream_t st) {
+  dim3 grid(g.N, BH);
+  if (d == 128) k_pool<128><<<grid, 128, 0, st>>>(g, X, Xc);
+  else k_pool<64><<<grid, 64, 0, st>>>(g, X, Xc);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ a4
+// S[bh][i][j] = (sum_c Qc[i][c] Kc[j][c]) / sqrt(d): 32x32 output tile per CTA, 256 threads x 4
+// outputs, channels summed sequentially with exactly rounded mul/add.
+__global__ void __launch_bounds__(256) k_scores(int N, int d, const double* __restrict__ Qc,
+                                                const double* __restrict__ Kc, double* __restrict__ S) {
+  __shared__ double sa[32][17], sb[32][17];
+  const int bh = blockIdx.z, i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // ty in 0..7 -> rows ty, ty+8, ty+16, ty+24
+  const double* qh = Qc + static_cast<size_t>(bh) * N * d;
+  const double* kh = Kc + static_cast<size_t>(bh) * N * d;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < d; c0 += 16) {
+    for (int v = threadIdx.x; v < 32 * 16; v += 256) {
+      int rr = v / 16, cc = v % 16;
+      sa[rr][cc] = (i0 + rr < N) ? qh[static_cast<size_t>(i0 + rr) * d + c0 + cc] : 0.0;
+      sb[rr][cc] = (j0 + rr < N) ? kh[static_cast<size_t>(j0 + rr) * d + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+      double kv = sb[tx][cc];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[a] = dadd(acc[a], dmul(sa[ty + 8 * a][cc], kv));
+    }
+    __syncthreads();
+  }
+  const double sd = sqrt((double)d);
+  for (int a = 0; a < 4; ++a) {
+    int i = i0 + ty + 8 * a, j = j0 + tx;
+    if (i < N && j < N) S[(static_cast<size_t>(bh) * N + i) * N + j] = acc[a] / sd;
+  }
+}
+
+cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (N + 31) / 32, BH);
+  k_scores<<<grid, 256, 0, st>>>(N, d, Qc, Kc, S);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ a5 + a6
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  return s;
+}
+
+// Sort key: descending s, ascending j. true if (sa, ja) goes before (sb, jb).
+__device__ __forceinline__ bool before(double sa, int ja, double sb, int jb) {
+  return sa > sb || (sa == sb && ja < jb);
+}
+
+// One CTA (256 threads) per (bh, query-block row i).
+__global__ void __launch_bounds__(256) k_admit(int N, const double* __restrict__ S, int k, double z, double tau,
+                                               int* __restrict__ q2k_num, int* __restrict__ q2k_idx,
+                                               double* __restrict__ thresh, uint32_t* __restrict__ kvbits) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int row = blockIdx.x;  // bh * N + i
+  const int bh = row / N, i = row % N;
+  int P2 = 1;
+  while (P2 < N) P2 <<= 1;
+  double* s = reinterpret_cast<double*>(smem);  // [N]
+  double* cs = s + N;                           // [P2] candidate scores (sorted)
+  int* cj = reinterpret_cast<int*>(cs + P2);    // [P2] candidate ids
+  int* flag = cj + P2;                          // [N] admitted flags / scan
+  __shared__ double red[32];
+  __shared__ int s_nc, s_wcnt[32], s_ell;
+
+  const double* srow = S + static_cast<size_t>(row) * N;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) s[j] = srow[j];
+  __syncthreads();
+  // Eq.3 statistics (C13: population std over the n = N raw scaled scores)
+  double part = 0.0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) part += s[j];
+  const double mu = block_sum(part, red) / (double)N;
+  part = 0.0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) part += (s[j] - mu) * (s[j] - mu);
+  const double sigma = sqrt(block_sum(part, red) / (double)N);
+  const bool all = (k >= N);  // C15 bypass
+  const double p = mu + sigma * z;
+  if (threadIdx.x == 0) {
+    if (thresh) thresh[row] = all ? -INFINITY : p;
+    s_nc = 0;
+  }
+  __syncthreads();
+  // candidate compaction in ascending j (order irrelevant: sorted next)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < N; base += blockDim.x) {
+    int j = base + threadIdx.x;
+    bool c = j < N && (all || s[j] >= p);
+    unsigned m = __ballot_sync(0xffffffffu, c);
+    if (lane == 0) s_wcnt[warp] = __popc(m);
+    __syncthreads();
+    int off = s_nc;
+    for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+    if (c) {
+      int pos = off + __popc(m & ((1u << lane) - 1u));
+      cs[pos] = s[j];
+      cj[pos] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_wcnt[w];
+      s_nc += t;
+    }
+    __syncthreads();
+  }
+  int nc = s_nc;
+  if (nc == 0) {  // C16: empty -> {argmax, lowest id}
+    if (threadIdx.x == 0) {
+      int arg = 0;
+      for (int j = 1; j < N; ++j) if (s[j] > s[arg]) arg = j;
+      cs[0] = s[arg]; cj[0] = arg; s_nc = 1;
+    }
+    __syncthreads();
+    nc = 1;
+  }
+  int ell = nc;
+  if (tau < 1.0 && nc > 1) {
+    // bitonic sort of the candidates by (s desc, j asc), padded to a power of two
+    int P = 1;
+    while (P < nc) P <<= 1;
+    for (int t = nc + threadIdx.x; t < P; t += blockDim.x) { cs[t] = -INFINITY; cj[t] = INT_MAX; }
+    __syncthreads();
+    for (int sz = 2; sz <= P; sz <<= 1) {
+      for (int st = sz >> 1; st > 0; st >>= 1) {
+        for (int t = threadIdx.x; t < P; t += blockDim.x) {
+          int u = t ^ st;
+          if (u > t) {
+            bool up = ((t & sz) == 0);
+            bool swap = up ? before(cs[u], cj[u], cs[t], cj[t]) : before(cs[t], cj[t], cs[u], cj[u]);
+            if (swap) {
+              double a = cs[t]; cs[t] = cs[u]; cs[u] = a;
+              int bb = cj[t]; cj[t] = cj[u]; cj[u] = bb;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // Eq.4: e_t = exp(s_t - s_max), shortest prefix with cumulative e >= tau * E (C18)
+    const double m = cs[0];
+    double* e = cs;  // overwrite scores with exp weights (in place, same order)
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) e[t] = exp(cs[t] - m);
+    __syncthreads();
+    // inclusive scan over nc elements, chunked by blockDim
+    double carry = 0.0;
+    __shared__ double s_carry;
+    __shared__ double wsum[32];
+    if (threadIdx.x == 0) s_ell = nc;
+    for (int base = 0; base < nc; base += blockDim.x) {
+      int t = base + threadIdx.x;
+      double v = (t < nc) ? e[t] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        double a = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += a;
+      }
+      if (lane == 31) wsum[warp] = v;
+      __syncthreads();
+      double wo = 0.0;
+      for (int w = 0; w < warp; ++w) wo += wsum[w];
+      double incl = carry + wo + v;
+      __syncthreads();
+      if (t < nc) e[t] = incl;  // cumulative mass
+      if (threadIdx.x == blockDim.x - 1) s_carry = incl;
+      __syncthreads();
+      carry = s_carry;
+      __syncthreads();
+    }
+    const double E = e[nc - 1];
+    const double target = tau * E;
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+      bool reach = e[t] >= target && (t == 0 || e[t - 1] < target);
+      if (reach) s_ell = t + 1;
+    }
+    __syncthreads();
+    ell = s_ell;
+  }
+  // admitted flags -> ascending list
+  for (int j = threadIdx.x; j < N; j += blockDim.x) flag[j] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < ell; t += blockDim.x) flag[cj[t]] = 1;
+  __syncthreads();
+  int* out = q2k_idx + static_cast<size_t>(row) * N;
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int base = 0; base < N; base += blockDim.x) {
+    int j = base + threadIdx.x;
+    bool a = j < N && flag[j];
+    unsigned m = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) s_wcnt[warp] = __popc(m);
+    __syncthreads();
+    int off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+    if (a) {
+      out[off + __popc(m & ((1u << lane) - 1u))] = j;
+      if (kvbits) {
+        const int NW = (N + 31) / 32;
+        atomicOr(kvbits + (static_cast<size_t>(bh) * N + j) * NW + i / 32, 1u << (i % 32));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_wcnt[w];
+      s_base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) q2k_num[row] = ell;
+}
+
+cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int* q2k_num, int* q2k_idx,
+                         double* thresh, uint32_t* kvbits, cudaStream_t st) {
+  int P2 = 1;
+  while (P2 < N) P2 <<= 1;
+  size_t sm = static_cast<size_t>(N) * 8 + static_cast<size_t>(P2) * 12 + static_cast<size_t>(N) * 4;
+  cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_admit<<<N * BH, 256, sm, st>>>(N, S, k, z, tau, q2k_num, q2k_idx, thresh, kvbits);
+  return cudaGetLastError();
+}
+
+// k2q: one warp per (bh, KV block j) reads the admission bitmap row and emits ascending i.
+__global__ void __launch_bounds__(128) k_k2q(int N, int BH, const uint32_t* __restrict__ kvbits,
+                                             int* __restrict__ k2q_num, int* __restrict__ k2q_idx) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= N * BH) return;
+  const int NW = (N + 31) / 32;
+  const uint32_t* bits = kvbits + static_cast<size_t>(wid) * NW;
+  int* out = k2q_idx + static_cast<size_t>(wid) * N;
+  int cnt = 0;
+  for (int w0 = 0; w0 < NW; w0 += 32) {
+    int w = w0 + lane;
+    uint32_t v = w < NW ? bits[w] : 0u;
+    int c = __popc(v), incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    int pos = cnt + incl - c;
+    while (v) {
+      int bit = __ffs(v) - 1;
+      out[pos++] = w * 32 + bit;
+      v &= v - 1;
+    }
+    cnt += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) k2q_num[wid] = cnt;
+}
+
+cudaError_t launch_k2q(int N, int BH, const uint32_t* kvbits, int* k2q_num, int* k2q_idx, cudaStream_t st) {
+  int warps = N * BH;
+  k_k2q<<<(warps + 3) / 4, 128, 0, st>>>(N, BH, kvbits, k2q_num, k2q_idx);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ gather
+__global__ void k_gather_rows(int BH, int L, int Lq, int d, const bf16* __restrict__ X, const int* __restrict__ kept_tok,
+                              bf16* __restrict__ out) {
+  size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int vpr = d / 8;
+  size_t rows = static_cast<size_t>(BH) * Lq;
+  if (v >= rows * vpr) return;
+  size_t prow = v / vpr;
+  int c = static_cast<int>(v % vpr) * 8;
+  size_t bh = prow / Lq;
+  int tok = kept_tok[prow];
+  *reinterpret_cast<uint4*>(out + prow * d + c) = *reinterpret_cast<const uint4*>(X + (bh * L + tok) * d + c);
+}
+
+cudaError_t launch_gather_rows(int BH, int L, int Lq, int d, const bf16* X, const int* kept_tok, bf16* out,
+                               cudaStream_t st) {
+  size_t total = static_cast<size_t>(BH) * Lq * (d / 8);
+  k_gather_rows<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, L, Lq, d, X, kept_tok, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ host z
+// Phi^-1 on the host: Acklam's rational approximation (|rel err| < 1.2e-9) refined by two Halley
+// steps on erfc. (The oracle uses plain bisection; the two share no code.)
+double normal_quantile(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  if (p == 0.5) return 0.0;
+  const double plow = 0.02425, phigh = 1 - plow;
+  double x;
+  if (p < plow) {
+    double q = sqrt(-2 * log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  } else if (p <= phigh) {
+    double q = p - 0.5, rr = q * q;
+    x = (((((a[0] * rr + a[1]) * rr + a[2]) * rr + a[3]) * rr + a[4]) * rr + a[5]) * q /
+        (((((b[0] * rr + b[1]) * rr + b[2]) * rr + b[3]) * rr + b[4]) * rr + 1);
+  } else {
+    double q = sqrt(-2 * log(1 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  }
+  for (int it = 0; it < 2; ++it) {
+    // lower- or upper-tail residual keeps relative precision in both tails
+    // e = Phi(x) - p, evaluated through the tail that keeps relative precision
+    double e = (x < 0) ? 0.5 * erfc(-x / sqrt(2.0)) - p : (1 - p) - 0.5 * erfc(x / sqrt(2.0));
+    double u = e * sqrt(2 * M_PI) * exp(x * x / 2);
+    x = x - u / (1 + x * u / 2);
+  }
+  return x;
+}
+
+int slot_rows(int mk) {
+  int s = 8;
+  while (s < mk) s <<= 1;
+  return s;
+}
+
+}  // namespace bsa

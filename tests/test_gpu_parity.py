@@ -1,0 +1,138 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on identical seeded inputs.
+
+Sizes span several tiles and ragged tails (grids not divisible by the block); the full BASELINE
+32k configuration is covered by sampled outputs in test_gpu_fullsize.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import bsa_gen
+import oracle as orc
+import paper_2509_01085_b200 as bsa
+from parity_util import assert_close, compare_selection
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # name, grid, block, unit, Hh, d, r, f (k = ceil(f N)), tau, kind
+    ("tiny_r05_k8", (4, 8, 8), (2, 4, 4), (0, 0, 0), 2, 64, 0.5, 1.0, 0.9, "iid"),
+    ("tiny_r05_k4", (4, 8, 8), (2, 4, 4), (0, 0, 0), 2, 64, 0.5, 0.5, 0.9, "video"),
+    ("tiny_dense", (4, 8, 8), (2, 4, 4), (0, 0, 0), 2, 64, 1.0, 1.0, 1.0, "iid"),
+    ("ragged_d128", (6, 10, 14), (4, 4, 4), (0, 0, 0), 2, 128, 0.5, 0.3, 0.9, "video"),
+    ("ragged_r025", (6, 10, 14), (4, 4, 4), (0, 0, 0), 2, 128, 0.25, 0.5, 0.95, "iid"),
+    ("ragged_r1", (6, 10, 14), (4, 4, 4), (0, 0, 0), 1, 128, 1.0, 0.4, 0.9, "video"),
+    ("window222", (8, 12, 12), (4, 4, 4), (2, 2, 2), 2, 128, 0.5, 0.25, 0.9, "video"),
+    ("multi_tile", (8, 16, 24), (4, 4, 4), (0, 0, 0), 3, 128, 0.5, 0.1, 0.9, "video"),
+    ("d64_bt64", (8, 12, 16), (4, 4, 4), (0, 0, 0), 2, 64, 0.5, 0.2, 0.9, "iid"),
+    ("d128_bt32", (6, 10, 12), (2, 4, 4), (0, 0, 0), 2, 128, 0.5, 0.3, 0.9, "video"),
+]
+
+
+def _run(case, seed=0):
+    name, grid, block, unit, Hh, d, r, f, tau, kind = case
+    og = orc.Geom(*grid, *block, *unit)
+    g = bsa.Geometry(*grid, *block, *unit)
+    Qc, Kc, Vc = bsa_gen.make_inputs(kind, seed, 1, Hh, grid, d)
+    Q, K, V = Qc.cuda(), Kc.cuda(), Vc.cuda()
+    N = orc.sizes(og, r)[0]
+    k = bsa.resolve_k(f, N)
+    sel = bsa.select(g, r, k, tau, Q, K)
+    torch.cuda.synchronize()
+    return og, g, (Qc, Kc, Vc), (Q, K, V), k, sel
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_partition_parity(case):
+    name, grid, block, unit, Hh, d, r, f, tau, kind = case
+    og = orc.Geom(*grid, *block, *unit)
+    g = bsa.Geometry(*grid, *block, *unit)
+    part = bsa.bsa_block_partition(g, r)
+    ref = orc.partition(og, r)
+    for key in ("block_off", "block_tok", "kept_off"):
+        assert np.array_equal(part[key].cpu().numpy(), ref[key]), key
+    assert np.array_equal(part["block_ext"].cpu().numpy(), ref["block_ext"])
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_selection_parity(case):
+    og, g, host, dev, k, sel = _run(case)
+    name, grid, block, unit, Hh, d, r, f, tau, kind = case
+    oq = orc.select_queries(og, r, host[0])
+    okv = orc.select_kv(og, host[0], host[1], k, tau)
+    near = compare_selection(og, r, sel.kept_tok, sel.donor, sel.q2k_num, sel.q2k_idx, oq, okv)
+    print(f"{name}: near-ties {near}")
+    # pooled Q is bit-exact (exact fp64 sums of bf16 values)
+    qp = orc.pool(og, host[0])
+    assert np.array_equal(sel.q_pooled.cpu().numpy().reshape(qp.shape), qp)
+    # packed Q^s rows are the kept rows of Q
+    Lq = sel.kept_tok.shape[-1]
+    kt = sel.kept_tok.long().view(Hh, Lq)
+    ref_packed = torch.stack([dev[0][0, h][kt[h]] for h in range(Hh)])
+    assert torch.equal(sel.q_packed.view(Hh, Lq, d), ref_packed)
+    # k2q is the exact transpose of the GPU's q2k
+    num, idx = sel.q2k_num.cpu().numpy()[0], sel.q2k_idx.cpu().numpy()[0]
+    knum, kidx = sel.k2q_num.cpu().numpy()[0], sel.k2q_idx.cpu().numpy()[0]
+    N = num.shape[1]
+    for h in range(Hh):
+        adm = np.zeros((N, N), bool)
+        for i in range(N):
+            adm[i, idx[h, i, :num[h, i]]] = True
+        for j in range(N):
+            assert np.array_equal(kidx[h, j, :knum[h, j]], np.nonzero(adm[:, j])[0])
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_attention_parity(case):
+    og, g, host, dev, k, sel = _run(case, seed=1)
+    name, grid, block, unit, Hh, d, r, f, tau, kind = case
+    Q, K, V = dev
+    scale = 1.0 / np.sqrt(d)
+    O, lse = bsa.bsa_attn_fwd(g, r, Q, K, V, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num,
+                              sel.q2k_idx, scale=scale, q_packed=sel.q_packed)
+    torch.cuda.synchronize()
+    # oracle on the GPU's selection (isolates attention parity from selection near-ties)
+    kt = sel.kept_tok.cpu().numpy()[0]
+    dn = sel.donor.cpu().numpy()[0]
+    qn = sel.q2k_num.cpu().numpy()[0]
+    qi = sel.q2k_idx.cpu().numpy()[0]
+    N = qn.shape[1]
+    qi = np.where(np.arange(N)[None, None, :] < qn[:, :, None], qi, -1)
+    Oref, lseref = orc.attn_fwd(og, r, host[0][0], host[1][0], host[2][0], kt, dn, qn, qi, float(np.float32(scale)))
+    assert_close("O", O[0], Oref)
+    assert np.max(np.abs(lse.cpu().double().numpy()[0] - lseref)) < 2e-2
+    # backward
+    dO = bsa_gen.grad_output(1, (1, Hh, og.L, d)).cuda()
+    dQ, dK, dV = bsa.bsa_attn_bwd(g, r, Q, K, V, O, dO, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.k2q_num,
+                                  sel.k2q_idx, lse, scale=scale, q_packed=sel.q_packed)
+    torch.cuda.synchronize()
+    dQr, dKr, dVr = orc.attn_bwd(og, r, host[0][0], host[1][0], host[2][0], dO.cpu()[0], kt, dn, qn, qi,
+                                 float(np.float32(scale)))
+    assert_close("dV", dV[0], dVr)
+    assert_close("dK", dK[0], dKr)
+    assert_close("dQ", dQ[0], dQr)
+    # exact structural properties: pruned dQ rows are 0; unadmitted key blocks get 0
+    pruned = dn != np.arange(og.L)[None, :]
+    assert torch.count_nonzero(dQ[0].cpu()[torch.from_numpy(pruned)]) == 0
+
+
+def test_dense_equivalence_d128():
+    """r = 1, k = N, tau = 1: BSA == dense attention against torch SDPA in fp32."""
+    grid, block, d, Hh = (4, 8, 16), (4, 4, 4), 128, 2
+    g = bsa.Geometry(*grid, *block)
+    Q, K, V = (x.cuda() for x in bsa_gen.make_inputs("iid", 5, 1, Hh, grid, d))
+    N = bsa.bsa_sizes(g, 1.0)[0]
+    sel = bsa.select(g, 1.0, N, 1.0, Q, K)
+    assert int(sel.q2k_num.min()) == N
+    O, _ = bsa.bsa_attn_fwd(g, 1.0, Q, K, V, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num, sel.q2k_idx,
+                            q_packed=sel.q_packed)
+    ref = torch.nn.functional.scaled_dot_product_attention(Q.float(), K.float(), V.float())
+    assert_close("O_dense", O[0], ref[0].double().cpu().numpy())
+
+
+def test_errors_fail_loudly():
+    g = bsa.Geometry(4, 8, 8, 2, 4, 4)
+    Q = torch.zeros(1, 1, 256, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(bsa.BSAError):
+        bsa.bsa_select_kv_blocks(g, Q, Q, 0, 0.9)
