@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — BSA (arXiv 2509.01085) sparse-attention fwd+bwd on B200.
+
+One "step" = the whole hot path over one batch of synthetic input:
+partition, query pruning (Eq.2), KV-block admission (Eq.3 + Eq.4), sparse attention forward + fill
+(Eq.5) and backward, all through the C ABI of libbsa.so.
+
+    python bench.py                        # N=1, Wan2.1-1.3B-shaped 32k workload (BASELINE configs[1])
+    python bench.py --config wan14b_75k    # 75,600 tokens, 40 heads
+    torchrun --nproc-per-node N bench.py --gpus N   # weak scaling: one independent problem per rank
+    python bench.py --impl reference       # the CPU fp64 oracle as the reference arm
+
+Metric (BASELINE.json): effective (executed) TFLOPS of fwd+bwd = 14*d*P / step time, where P is the
+number of admitted (query, key) pairs; also ms per step and the same library's own
+dense path (r = 1, k = N, tau = 1) for the speedup. Inputs are larger than L2 (4 x 100 MB) and L2
+is additionally flushed (256 MiB write) between timed steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: grid, block, B, Hh, d, r, f (k = ceil(f N)), tau, generator
+    "tiny": dict(grid=(4, 8, 8), block=(2, 4, 4), B=1, Hh=2, d=64, r=0.5, f=0.5, tau=0.9, kind="video"),
+    "wan1.3b_32k": dict(grid=(21, 30, 52), block=(4, 4, 4), B=1, Hh=12, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
+    "wan14b_75k": dict(grid=(21, 45, 80), block=(4, 4, 4), B=1, Hh=40, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
+    "long_147k": dict(grid=(41, 45, 80), block=(4, 4, 4), B=1, Hh=40, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
+}
+KERNEL_NAMES = ["partition", "select_queries", "pool", "scores", "admit", "k2q", "gather", "attn_fwd", "fill",
+                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image"]
+SELECTION_IDS = range(0, 7)
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained"),
+                    source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback")
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, dev_index: int, period=0.005):
+        self.samples, self.reasons, self.period = [], set(), period
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def oracle_sample(cfg, seed, heads, threads):
+    """The fp64 oracle as it stands on `heads` heads of the workload: selection + fwd + bwd.
+    Returns (seconds, executed fwd+bwd FLOPs of the sample)."""
+    import ctypes
+
+    import numpy as np
+
+    import bsa_gen
+    import oracle as orc
+    orc.set_threads(threads)
+    g = orc.Geom(*cfg["grid"], *cfg["block"])
+    d, r, tau = cfg["d"], cfg["r"], cfg["tau"]
+    N, Lq = orc.sizes(g, r)
+    k = orc.resolve_k(cfg["f"], N)
+    Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, 1, heads, cfg["grid"], d)
+    dO = bsa_gen.grad_output(seed, (1, heads, g.L, d))
+    Qd, Kd, Vd, dOd = (x.double().numpy().reshape(heads, g.L, d) for x in (Q, K, V, dO))
+    t0 = time.perf_counter()
+    qs = orc.select_queries(g, r, Qd)
+    kv = orc.select_kv(g, Qd, Kd, k, tau)
+    scale = 1.0 / math.sqrt(d)
+    O, lse = orc.attn_fwd(g, r, Qd, Kd, Vd, qs["kept_tok"], qs["donor"], kv["q2k_num"], kv["q2k_idx"], scale)
+    orc.attn_bwd(g, r, Qd, Kd, Vd, dOd, qs["kept_tok"], qs["donor"], kv["q2k_num"], kv["q2k_idx"], scale)
+    dt = time.perf_counter() - t0
+    p = orc.partition(g, r)
+    bsz = np.diff(p["block_off"]).astype(np.int64)
+    kept = np.diff(p["kept_off"]).astype(np.int64)
+    P = 0
+    for h in range(heads):
+        for i in range(N):
+            P += int(kept[i]) * int(bsz[kv["q2k_idx"][h, i, :kv["q2k_num"][h, i]]].sum())
+    return dt, 14 * d * P
+
+
+def run_reference(args, cfg, rank, world):
+    if world > 1 and rank != 0:
+        return
+    import oracle as orc
+    orc.build()
+    threads = os.cpu_count() or 1
+    heads = 1
+    times, flops = [], 0
+    for s in range(args.warmup + args.steps):
+        dt, fl = oracle_sample(cfg, args.seed, heads, threads)
+        if s >= args.warmup:
+            times.append(dt)
+            flops = fl
+    t = sum(times) / len(times)
+    val = flops / t / 1e12
+    sample = f"1 of {cfg['Hh']} heads of the {args.config} workload (full selection + fwd + bwd of that head), " \
+             f"fp64, {threads} threads"
+    line = {
+        "impl": "reference", "metric": "BSA attention fwd+bwd effective TFLOPS (executed FLOPs)", "value": val,
+        "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "sample": "1 head", **{k: v for k, v in cfg.items() if k != "kind"},
+                   "generator": cfg["kind"]},
+        "cpu_baseline": {"value": val, "unit": "TFLOPS", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="bsa", choices=["bsa", "reference"])
+    ap.add_argument("--config", default="wan1.3b_32k", choices=sorted(CONFIGS))
+    ap.add_argument("--r", type=float, default=None)
+    ap.add_argument("--f", type=float, default=None, help="Eq.3 key fraction: k = ceil(f N)")
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--kind", default=None, choices=["video", "iid"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    for key in ("r", "f", "tau", "kind"):
+        if getattr(args, key) is not None:
+            cfg[key] = getattr(args, key)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import bsa_gen
+    import paper_2509_01085_b200 as bsa
+    from paper_2509_01085_b200.runner import BSAAttention
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = bsa.lib()
+
+    g = bsa.Geometry(*cfg["grid"], *cfg["block"])
+    B, Hh, d = cfg["B"], cfg["Hh"], cfg["d"]
+    seed = args.seed + 1000 * rank  # weak scaling: each rank owns an independent problem (batch element)
+    Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, B, Hh, cfg["grid"], d, device=dev)
+    dO = bsa_gen.grad_output(seed, (B, Hh, g.L, d)).to(dev)
+    layer = BSAAttention(g, cfg["r"], cfg["f"], cfg["tau"], B, Hh, d, device=dev, cache_partition=False)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        layer.forward(Q, K, V)
+        layer.backward(dO)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    fl = layer.flops()
+
+    # ---------------------------------------------------------------- timed region
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    L.bsa_timing_read(None, None, 0)
+    L.bsa_timing_enable(1)
+    n0 = L.bsa_launch_count()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[s].record()
+            step()
+            ends[s].record()
+        torch.cuda.synchronize()
+    launches = L.bsa_launch_count() - n0
+    L.bsa_timing_enable(0)
+    if world > 1:
+        dist.barrier()
+    import ctypes
+    nk = len(KERNEL_NAMES)
+    kms = (ctypes.c_double * nk)()
+    kcnt = (ctypes.c_int32 * nk)()
+    L.bsa_timing_read(kms, kcnt, nk)
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    f_local = torch.tensor([fl["total"] * args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f_local, op=dist.ReduceOp.SUM)
+    t_max = float(t_local.item())
+    value = float(f_local.item()) / (t_max * 1e-3) / 1e12
+    ms_per_step = t_max / args.steps
+    kernel_ms = {KERNEL_NAMES[i]: kms[i] / max(1, args.steps) for i in range(nk) if kcnt[i]}
+    phases = {
+        "selection_ms": sum(kms[i] for i in SELECTION_IDS) / args.steps,
+        "fwd_ms": (kms[7] + kms[8] + kms[12]) / args.steps,
+        "bwd_ms": (kms[9] + kms[10] + kms[11]) / args.steps,
+    }
+
+    # ---------------------------------------------------------------- roofline (dominant kernel)
+    peaks = read_peaks()
+    dom = "attn_bwd" if kms[10] >= kms[7] else "attn_fwd"
+    dom_ms = kms[10 if dom == "attn_bwd" else 7] / max(1, kcnt[10 if dom == "attn_bwd" else 7])
+    dom_flops = fl["bwd"] if dom == "attn_bwd" else fl["fwd"]
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16"], "traffic": traffic, "peak_source": f"{peaks['source']} bf16 burst",
+                "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_ms}
+    # selection kernels against HBM (algorithmic bytes)
+    BH, Lq, N = B * Hh, layer.Lq, layer.N
+    sel_bytes = BH * (4 * g.L * d + 4 * Lq + 4 * g.L + 2 * Lq * d + 8 * N * d + 4 * N * (1 + fl["pairs"] / max(1, BH * Lq)))
+    sel_ms = phases["selection_ms"]
+
+    # ---------------------------------------------------------------- own dense path (r=1, k=N, tau=1)
+    dense = None
+    if args.dense_steps > 0:
+        dl = BSAAttention(g, 1.0, 1.0, 1.0, B, Hh, d, device=dev)
+        for _ in range(2):
+            dl.forward(Q, K, V)
+            dl.backward(dO)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.dense_steps)]
+        for s in range(args.dense_steps):
+            flush.zero_()
+            ev[2 * s].record()
+            dl.forward(Q, K, V)
+            dl.backward(dO)
+            ev[2 * s + 1].record()
+        torch.cuda.synchronize()
+        dms = sum(ev[2 * s].elapsed_time(ev[2 * s + 1]) for s in range(args.dense_steps)) / args.dense_steps
+        dfl = dl.flops()
+        dense = {"ms_per_step": dms, "tflops": dfl["total"] / (dms * 1e-3) / 1e12, "speedup": dms / ms_per_step}
+        del dl
+        torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- e2e: host buffers, copies inside the region
+    hQ, hK, hV, hdO = (x.cpu().pin_memory() for x in (Q, K, V, dO))
+    outs = [torch.empty(B, Hh, g.L, d, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    dQ2, dK2, dV2, dO2 = (torch.empty_like(Q) for _ in range(4))
+    e2e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.e2e_steps)]
+    for s in range(args.e2e_steps + 1):
+        if s > 0:
+            e2e_ev[2 * (s - 1)].record()
+        Qg, Kg, Vg = (h.to(dev, non_blocking=True) for h in (hQ, hK, hV))
+        dOg = hdO.to(dev, non_blocking=True)
+        O = layer.forward(Qg, Kg, Vg)
+        dq, dk, dv = layer.backward(dOg)
+        for o, src in zip(outs, (O, dq, dk, dv)):
+            o.copy_(src, non_blocking=True)
+        if s > 0:
+            e2e_ev[2 * (s - 1) + 1].record()
+        torch.cuda.synchronize()
+    e2e_ms = sum(e2e_ev[2 * s].elapsed_time(e2e_ev[2 * s + 1]) for s in range(args.e2e_steps)) / max(1, args.e2e_steps)
+    e_local = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_local, op=dist.ReduceOp.MAX)
+    e2e_val = fl["total"] * world / (float(e_local.item()) * 1e-3) / 1e12 if args.e2e_steps else None
+    tensor_bytes = B * Hh * g.L * d * 2
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as orc
+        orc.build()
+        threads = os.cpu_count() or 1
+        dt, cfl = oracle_sample(cfg, args.seed, 1, threads)
+        cpu = {"value": cfl / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": "oracle",
+               "sample": f"head 0 of {Hh} of the {args.config} workload: full selection + fwd + bwd, fp64, "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "BSA attention fwd+bwd effective TFLOPS (executed FLOPs) at 32k/75k tokens vs own dense",
+            "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded G_video latents, bsa_gen)",
+            "config": {"workload": args.config, "grid": list(cfg["grid"]), "block": list(cfg["block"]), "B": B,
+                       "heads": Hh, "d": d, "r": cfg["r"], "k": layer.k, "k_frac": cfg["f"], "tau": cfg["tau"],
+                       "generator": cfg["kind"], "tokens": g.L, "N_blocks": N,
+                       "l2": "inputs > L2 (4 x %.0f MB) and 256 MiB L2 flush between timed steps" % (tensor_bytes / 1e6),
+                       "parallelism": f"bh-shard x{world} (independent problems, no collective)"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "selection_hbm": {"bytes": sel_bytes, "ms": sel_ms, "achieved_gbs": sel_bytes / (sel_ms * 1e-3) / 1e9,
+                              "peak_gbs": peaks["hbm"], "frac": sel_bytes / (sel_ms * 1e-3) / 1e9 / peaks["hbm"]},
+            "phases_ms": phases, "kernel_ms": kernel_ms,
+            "executed": {"pairs": fl["pairs"], "density": fl["density"], "flops_per_step": fl["total"],
+                         "dense_equiv_tflops": fl["dense_total"] * world / (t_max * 1e-3 / args.steps) / 1e12},
+            "own_dense": dense,
+            "e2e": {"value": e2e_val, "unit": "TFLOPS", "ms_per_step": float(e_local.item()),
+                    "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": 4 * tensor_bytes},
+            "cpu_baseline": cpu,
+            "paper_context": "17.79x attention-training speedup and 20x FLOP reduction at 153,600 tokens on H100 "
+                             "(Triton, precision unstated; PAPER.md P:234, P:22) — context, not the target",
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

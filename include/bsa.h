@@ -140,7 +140,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
  * Kernel ids reported by bsa_timing_read / counted by bsa_launch_count. */
 enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
-  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_COUNT
+  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_COUNT
 };
 /* Total kernels this thread has launched through libbsa (always counted; cheap). */
 int64_t bsa_launch_count(void);

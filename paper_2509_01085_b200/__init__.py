@@ -21,7 +21,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbsa.so")
+LIB_PATH = os.environ.get("BSA_LIB_PATH") or os.path.join(_HERE, "libbsa.so")  # override: debug builds only
 
 OP_SELECT_KV, OP_ATTN_FWD, OP_ATTN_BWD = 1, 2, 3
 
@@ -84,7 +84,12 @@ def lib() -> ctypes.CDLL:
         L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _S, _P]
         L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P,
                                    _P, _P, _S, _P]
-        for f in ("bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
+        L.bsa_launch_count.restype = ctypes.c_int64
+        L.bsa_launch_count.argtypes = []
+        L.bsa_timing_enable.argtypes = [_I]
+        L.bsa_timing_read.argtypes = [_P, _P, _I]
+        for f in ("bsa_timing_enable", "bsa_timing_read",
+                  "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd"):
             getattr(L, f).restype = _I
         _lib = L
@@ -195,8 +200,8 @@ def bsa_attn_fwd(g: Geometry, r: float, Q, K, V, kept_off, kept_tok, donor, q2k_
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     O = torch.empty_like(K) if out is None else out
     lse = torch.empty(B, Hh, Lq, dtype=torch.float32, device=dev) if lse is None else lse
-    nb = 0 if q_packed is not None else bsa_workspace_bytes(OP_ATTN_FWD, g, r, B, Hh, d)
-    ws = _ws(nb, dev) if nb else None
+    nb = bsa_workspace_bytes(OP_ATTN_FWD, g, r, B, Hh, d)
+    ws = _ws(nb, dev)
     _check(lib().bsa_attn_fwd(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(q_packed),
                               _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(q2k_num), _ptr(q2k_idx), float(scale),
                               _ptr(O), _ptr(lse), _ptr(ws), nb, _stream(dev)), "bsa_attn_fwd")

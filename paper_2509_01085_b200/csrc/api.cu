@@ -123,14 +123,28 @@ SelKvWs selkv_ws(const bsa::Geo& g, size_t BH, int d) {
   return w;
 }
 
-struct BwdWs {
-  size_t qs, dos, dv, dq, total;
+// Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL).
+struct FwdWs {
+  size_t kv, qs, total;
 };
-BwdWs bwd_ws(size_t BH, size_t Lq, int d) {
+FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d) {
+  FwdWs w;
+  w.kv = 0;
+  w.qs = w.kv + align256(BH * g.N * 2 * static_cast<size_t>(g.BT) * d * 2);
+  w.total = w.qs + align256(BH * Lq * d * 2);
+  return w;
+}
+
+// Backward workspace: gathered Q^s (only when q_packed is NULL), Q^s|dO^s query-block images
+// (N * SR padded rows per head), D = rowsum(dO^s O^s), fp32 dQ accumulator.
+struct BwdWs {
+  size_t qs, img, dv, dq, total;
+};
+BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   BwdWs w;
   w.qs = 0;
-  w.dos = w.qs + align256(BH * Lq * d * 2);
-  w.dv = w.dos + align256(BH * Lq * d * 2);
+  w.img = w.qs + align256(BH * Lq * d * 2);
+  w.dv = w.img + align256(BH * g.N * static_cast<size_t>(SR) * d * 4);
   w.dq = w.dv + align256(BH * Lq * 4);
   w.total = w.dq + align256(BH * Lq * d * 4);
   return w;
@@ -199,11 +213,11 @@ int bsa_workspace_bytes(int op, const bsa_geom* g, double r, int32_t B, int32_t 
   int lq = 0, mk = 0;
   host_sizes(G, r, &lq, &mk);
   if (op == BSA_OP_ATTN_FWD) {
-    *bytes = align256(BH * lq * d * 2);
+    *bytes = fwd_ws(G, BH, lq, d).total;
     return BSA_OK;
   }
   if (op == BSA_OP_ATTN_BWD) {
-    *bytes = bwd_ws(BH, lq, d).total;
+    *bytes = bwd_ws(G, BH, lq, bsa::slot_rows(mk), d).total;
     return BSA_OK;
   }
   return fail(BSA_ERR_CONFIG, "unknown op %d", op);
@@ -311,16 +325,19 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   CHECK(check_attn_geom(G, r, &Lq, &SR));
   size_t BH = static_cast<size_t>(B) * Hh;
   const bsa::bf16* Qs = static_cast<const bsa::bf16*>(q_packed);
-  if (!Qs) {
-    size_t need = align256(BH * Lq * d * 2);
-    if (!ws || ws_bytes < need)
-      return fail(BSA_ERR_SELECTION_MISMATCH, "q_packed is NULL and workspace %zu < %zu bytes", ws_bytes, need);
-  }
+  FwdWs w = fwd_ws(G, BH, Lq, d);
+  if (!ws || ws_bytes < w.total)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "workspace %zu < required %zu bytes", ws_bytes, w.total);
   CHECK(check_device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaSuccess;
-  if (!Qs) {
-    bsa::bf16* dst = static_cast<bsa::bf16*>(ws);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* kv_img = base + w.kv;
+  cudaError_t e = timed(BSA_K_KV_IMAGE, 1, st, [&] {
+    return bsa::launch_kv_image(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(K),
+                                static_cast<const bsa::bf16*>(V), kv_img, st);
+  });
+  if (e == cudaSuccess && !Qs) {
+    bsa::bf16* dst = reinterpret_cast<bsa::bf16*>(base + w.qs);
     e = timed(BSA_K_GATHER, 1, st, [&] {
       return bsa::launch_gather_rows(static_cast<int>(BH), G.L, Lq, d, static_cast<const bsa::bf16*>(Q), kept_tok, dst,
                                      st);
@@ -345,6 +362,7 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.scale = scale;
   a.O = static_cast<bsa::bf16*>(O);
   a.lse = lse;
+  a.kv_img = kv_img;
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_FILL, 1, st, [&] { return bsa::launch_fill(a.BH, G.L, d, donor, a.O, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_fwd");
@@ -370,7 +388,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   int Lq = 0, SR = 0;
   CHECK(check_attn_geom(G, r, &Lq, &SR));
   size_t BH = static_cast<size_t>(B) * Hh;
-  BwdWs w = bwd_ws(BH, Lq, d);
+  BwdWs w = bwd_ws(G, BH, Lq, SR, d);
   if (!ws || ws_bytes < w.total)
     return fail(BSA_ERR_SELECTION_MISMATCH, "workspace of %zu bytes < required %zu", ws_bytes, w.total);
   CHECK(check_device());
@@ -408,7 +426,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.dQ = static_cast<bsa::bf16*>(dQ);
   a.dK = static_cast<bsa::bf16*>(dK);
   a.dV = static_cast<bsa::bf16*>(dV);
-  a.dOs = reinterpret_cast<bsa::bf16*>(base + w.dos);
+  a.qdo_img = base + w.img;
   a.Dvec = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
@@ -419,6 +437,16 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
 }
 
 int64_t bsa_launch_count(void) { return g_launches; }
+
+// Debug aid (not in bsa.h): per-step timeline of one forward CTA, see attn_fwd.cu FWD_TRACE.
+int bsa_debug_trace_fwd(void* dev_buf, int cta) {
+  cudaError_t e = bsa::debug_trace_fwd(dev_buf, cta);
+  return e == cudaSuccess ? BSA_OK : cuda_fail(e, "bsa_debug_trace_fwd");
+}
+int bsa_debug_trace_bwd(void* dev_buf, int cta) {
+  cudaError_t e = bsa::debug_trace_bwd(dev_buf, cta);
+  return e == cudaSuccess ? BSA_OK : cuda_fail(e, "bsa_debug_trace_bwd");
+}
 
 int bsa_timing_enable(int on) {
   g_timing = on != 0;

@@ -11,6 +11,12 @@
 //               dV_j^T += dO^s^T P, dK_j^T += Q^s^T dS      (M=d=128, N=BT, K=128 queries; TMEM-resident)
 //               dQ_part = dS K_j                            (M=128, N=d) -> fp32 vector reductions
 //   finalize: dQ[kept] = scale * dQacc (bf16), dQ[pruned] = 0.
+//
+// Warp roles of the main kernel (384 threads): w0 TMA producer (all lanes fetch the chunk's block
+// metadata in parallel; Q^s/dO^s tiles by 2D TMA, LSE/D rows by 1D TMA), w1 MMA issuer, w2 TMEM
+// allocator, w4-w7 gradient-softmax warpgroup (thread == query row), w8-w11 dQ warpgroup that drains
+// the double-buffered dQ accumulator (TMEM) into the packed fp32 dQ with red.global.add.v4.f32 while
+// the next chunk is computed.
 #include <cmath>
 #include "kernels.h"
 #include "ptx.cuh"
@@ -19,6 +25,7 @@ namespace bsa {
 
 bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
 bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int BH);
+bool make_map_1d_f32(CUtensorMap* m, const void* base, size_t n, int box);
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -27,19 +34,47 @@ __device__ __forceinline__ float ex2b(float x) {
 }
 
 // ------------------------------------------------------------------------------------ prep
-// One warp per packed kept row.
+// QdO image of a query block (what one chunk slot of the main kernel reads with ONE bulk copy):
+// SR/8 groups of 8 rows; group q holds [Q^s d-half 0][Q^s d-half 1][dO^s d-half 0][dO^s d-half 1], each
+// 8 rows x 128 B with the 128-byte swizzle. Consecutive groups (also across the blocks stacked in a
+// chunk) are 2*NCB KB apart, so every UMMA operand over the chunk's 128 rows has a uniform stride.
+// One warp per padded row (b,h, block, row < SR); rows beyond the block's kept count are zero.
 template <int D>
-__global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, const int* __restrict__ kept_tok,
-                                                  const int* __restrict__ donor, const bf16* __restrict__ dO,
-                                                  const bf16* __restrict__ O, bf16* __restrict__ dOs,
+__global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR, const int* __restrict__ kept_off,
+                                                  const int* __restrict__ kept_tok, const int* __restrict__ donor,
+                                                  const bf16* __restrict__ Qs, const bf16* __restrict__ dO,
+                                                  const bf16* __restrict__ O, uint8_t* __restrict__ qdo_img,
                                                   float* __restrict__ Dvec, float* __restrict__ dQacc) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
+  constexpr int NCB = D / 64;
   const size_t wid = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (wid >= static_cast<size_t>(BH) * Lq) return;
-  const size_t bh = wid / Lq;
-  const int tok = kept_tok[wid];
+  if (wid >= static_cast<size_t>(BH) * g.N * SR) return;
+  const int lr = static_cast<int>(wid % SR);
+  const size_t bi = wid / SR;
+  const int blk = static_cast<int>(bi % g.N);
+  const size_t bh = bi / g.N;
+  const int ko = kept_off[blk], nk = kept_off[blk + 1] - ko;
+  const int ch0 = lane * PER;
+  uint8_t* gbase = qdo_img + bi * static_cast<size_t>(SR) * D * 4 + (lr >> 3) * (2 * NCB * 1024);
+  const uint32_t inrow = sw128_off(lr & 7, (ch0 & 63) >> 3) + (ch0 & 7) * 2;
+  uint8_t* qdst = gbase + (ch0 >> 6) * 1024 + inrow;
+  uint8_t* ddst = gbase + (NCB + (ch0 >> 6)) * 1024 + inrow;
+  if (lr >= nk) {
+    if (PER == 4) {
+      *reinterpret_cast<uint2*>(qdst) = make_uint2(0, 0);
+      *reinterpret_cast<uint2*>(ddst) = make_uint2(0, 0);
+    } else {
+      *reinterpret_cast<uint32_t*>(qdst) = 0u;
+      *reinterpret_cast<uint32_t*>(ddst) = 0u;
+    }
+    return;
+  }
+  const size_t prow = bh * Lq + ko + lr;
+  const int tok = kept_tok[prow];
   const size_t head = bh * g.L;
+  if (PER == 4) *reinterpret_cast<uint2*>(qdst) = *reinterpret_cast<const uint2*>(Qs + prow * D + ch0);
+  else *reinterpret_cast<uint32_t*>(qdst) = *reinterpret_cast<const uint32_t*>(Qs + prow * D + ch0);
   float acc[PER];
   {
     const bf16* src = dO + (head + tok) * D + lane * PER;
@@ -67,34 +102,50 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, const i
   }
   float dsum = 0.f;
   const bf16* orow = O + (head + tok) * D + lane * PER;
-  bf16* out = dOs + wid * D + lane * PER;
+  bf16 hv[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) {
-    bf16 hv = __float2bfloat16_rn(acc[e]);
-    out[e] = hv;
-    dsum += __bfloat162float(hv) * __bfloat162float(orow[e]);
+    hv[e] = __float2bfloat16_rn(acc[e]);
+    dsum += __bfloat162float(hv[e]) * __bfloat162float(orow[e]);
   }
+  if (PER == 4) *reinterpret_cast<uint2*>(ddst) = *reinterpret_cast<const uint2*>(hv);
+  else *reinterpret_cast<uint32_t*>(ddst) = *reinterpret_cast<const uint32_t*>(hv);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-  if (lane == 0) Dvec[wid] = dsum;
-  float* dq = dQacc + wid * D + lane * PER;
+  if (lane == 0) Dvec[prow] = dsum;
+  float* dq = dQacc + prow * D + lane * PER;
 #pragma unroll
   for (int e = 0; e < PER; ++e) dq[e] = 0.f;
 }
 
 // ------------------------------------------------------------------------------------ main
+// Debug-only timeline of one CTA (bsa_debug_trace_bwd; null in production).
+__device__ unsigned long long* g_bwd_trace = nullptr;
+__device__ int g_bwd_trace_cta = 0;
+#ifdef BSA_TRACE
+#define BWD_TRACE(slot, u)                                                                              \
+  do {                                                                                                  \
+    unsigned long long* _t = g_bwd_trace;                                                               \
+    if (_t != nullptr && (int)(blockIdx.y * gridDim.x + blockIdx.x) == g_bwd_trace_cta && (u) < 1024) \
+      _t[(slot) * 1024 + (u)] = clock64();                                                              \
+  } while (0)
+#else
+#define BWD_TRACE(slot, u) \
+  do {                     \
+  } while (0)
+#endif
+
 struct BwdParams {
-  CUtensorMap mQs;   // 2D {d, BH*Lq}, box {64, SR}
-  CUtensorMap mdOs;  // 2D, same geometry
+  const uint8_t* qdo_img;  // per query block Q^s|dO^s images (k_bwd_prep), SR*d*4 bytes each
   CUtensorMap mK;    // 5D block map
   CUtensorMap mV;
   Geo g;
+  const float* lse;  // [BH*Lq] packed
+  const float* Dvec;
   int Lq, SR, G;
   const int* kept_off;
   const int* k2q_num;
   const int* k2q_idx;
-  const float* lse;
-  const float* Dvec;
   float* dQacc;
   bf16* dK;
   bf16* dV;
@@ -102,22 +153,24 @@ struct BwdParams {
   float scale;
 };
 
-constexpr int BWD_THREADS = 256;
+constexpr int BWD_THREADS = 384;
+constexpr int BWD_MAX_G = 16;
 
 template <int D, int BT>
 struct BwdSmem {
   static constexpr int NCB = D / 64;
   static constexpr int KV_BYTES = BT * D * 2;
-  static constexpr int TILE_BYTES = 128 * D * 2;  // Q^s or dO^s chunk tile
+  static constexpr int TILE_BYTES = 128 * D * 2;            // Q^s or dO^s rows of one chunk
+  static constexpr int PG = 2 * NCB * 1024;                 // stride of 8-row groups in a QdO image
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 2048;  // QdO images of the chunk's blocks, lse[128], D[128]
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
-  static constexpr int OFF_Q = OFF_V + KV_BYTES;          // 2 stages
-  static constexpr int OFF_DO = OFF_Q + 2 * TILE_BYTES;   // 2 stages
-  static constexpr int OFF_P = OFF_DO + 2 * TILE_BYTES;   // [128][64]
+  static constexpr int OFF_ST = OFF_V + KV_BYTES;           // 2 stages
+  static constexpr int OFF_P = OFF_ST + 2 * STAGE_BYTES;    // [128][64] bf16
   static constexpr int OFF_DS = OFF_P + 16384;
-  static constexpr int OFF_ZERO = OFF_DS + 16384;         // d=64 only: zero MN chunk for M=128 padding
+  static constexpr int OFF_ZERO = OFF_DS + 16384;           // d=64 only: zero MN chunk for M=128 padding
   static constexpr int TOTAL = OFF_ZERO + (D == 64 ? 16384 : 0) + 1024;
-  static constexpr int TMEM_COLS = (4 * BT + D) <= 256 ? 256 : 512;
+  static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
 template <int D, int BT>
@@ -128,14 +181,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm + SM::OFF_K;
   uint8_t* sV = sm + SM::OFF_V;
-  uint8_t* sQ = sm + SM::OFF_Q;
-  uint8_t* sdO = sm + SM::OFF_DO;
   uint8_t* sP = sm + SM::OFF_P;
   uint8_t* sdS = sm + SM::OFF_DS;
+  auto stage_q = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES; };  // Q^s d-half 0 of group 0
+  auto stage_do = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES + NCB * 1024; };
+  auto stage_lse = [&](int s) {
+    return reinterpret_cast<float*>(sm + SM::OFF_ST + s * SM::STAGE_BYTES + 2 * SM::TILE_BYTES);
+  };
+  auto stage_d = [&](int s) {
+    return reinterpret_cast<float*>(sm + SM::OFF_ST + s * SM::STAGE_BYTES + 2 * SM::TILE_BYTES + 1024);
+  };
 
   __shared__ __align__(8) uint64_t bar_kv, bar_c_full[2], bar_c_empty[2], bar_sd_full, bar_sd_free, bar_ps_full,
-      bar_ps_free, bar_dq_full, bar_dq_free;
+      bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc;
   __shared__ uint32_t s_tmem;
+  __shared__ int s_row0[2][BWD_MAX_G], s_nk[2][BWD_MAX_G], s_qb[2][BWD_MAX_G];
+  __shared__ int s_dqrow[2][128];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -145,22 +206,32 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   const int nq = p.k2q_num[jrow];
   const int* qlist = p.k2q_idx + jrow * g.N;
   const int nchunks = (nq + G - 1) / G;
+  const int crot = nchunks > 0 ? static_cast<int>((static_cast<unsigned>(j) * 2654435761u + bh * 40503u) % nchunks) : 0;
 
   if (tid == 0) {
     mbar_init(&bar_kv, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&bar_c_full[s], 1); mbar_init(&bar_c_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_c_full[s], 2);  // TMA transaction arrival + LSE/D arrival
+      mbar_init(&bar_c_empty[s], 1);
+      mbar_init(&bar_dq_full[s], 1);
+      mbar_init(&bar_dq_free[s], 128);
+    }
     mbar_init(&bar_sd_full, 1);
     mbar_init(&bar_sd_free, 128);
     mbar_init(&bar_ps_full, 128);
     mbar_init(&bar_ps_free, 1);
-    mbar_init(&bar_dq_full, 1);
-    mbar_init(&bar_dq_free, 128);
+    mbar_init(&bar_acc, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(&s_tmem, SM::TMEM_COLS);
-  // zero the Q/dO stages (rows of unused slots must be finite: they meet P = dS = 0 in the MMAs)
-  for (int o = tid * 16; o < 4 * SM::TILE_BYTES; o += BWD_THREADS * 16)
-    *reinterpret_cast<uint4*>(sQ + o) = make_uint4(0, 0, 0, 0);
+  // Warp roles (the warp arbiter favours higher ids, so the single-thread producer and MMA roles get the
+  // highest ones and are not starved by the math warps sharing their sub-partition):
+  // w0-3 gradient softmax (TMEM quadrant = warp), w4-7 dQ drain (quadrant = warp - 4), w8 TMEM allocator,
+  // w10 producer, w11 MMA issuer.
+  constexpr int W_ALLOC = 8, W_PROD = 10, W_MMA = 11;
+  if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
+  // zero both stages (rows of unused slots must be finite: they meet P = dS = 0 in the MMAs)
+  for (int o = tid * 16; o < 2 * SM::STAGE_BYTES; o += BWD_THREADS * 16)
+    *reinterpret_cast<uint4*>(sm + SM::OFF_ST + o) = make_uint4(0, 0, 0, 0);
   if (D == 64)
     for (int o = tid * 16; o < 16384; o += BWD_THREADS * 16)
       *reinterpret_cast<uint4*>(sm + SM::OFF_ZERO + o) = make_uint4(0, 0, 0, 0);
@@ -172,81 +243,135 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   const uint32_t tS = tbase, tdP = tbase + BT, tdV = tbase + 2 * BT, tdK = tbase + 3 * BT, tdQ = tbase + 4 * BT;
   const Box xj = block_box(g, j);
 
-  if (warp == 0) {
-    if (lane == 0 && nchunks > 0) {
-      tma_prefetch(&p.mQs);
-      tma_prefetch(&p.mdOs);
-      int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
-      mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
-      for (int cb = 0; cb < NCB; ++cb) {
-        tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-        tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-      }
-      for (int c = 0; c < nchunks; ++c) {
-        int s = c & 1;
-        mbar_wait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
-        int nb = min_i(G, nq - c * G);
-        mbar_expect_tx(&bar_c_full[s], static_cast<uint32_t>(2 * nb * NCB * SR * 128));
-        for (int gi = 0; gi < nb; ++gi) {
-          int qb = qlist[c * G + gi];
-          int row0 = bh * p.Lq + p.kept_off[qb];
-          for (int cb = 0; cb < NCB; ++cb) {
-            tma_load_2d(sQ + s * SM::TILE_BYTES + cb * 16384 + gi * SR * 128, &p.mQs, &bar_c_full[s], cb * 64, row0);
-            tma_load_2d(sdO + s * SM::TILE_BYTES + cb * 16384 + gi * SR * 128, &p.mdOs, &bar_c_full[s], cb * 64,
-                        row0);
-          }
+  if (warp == W_PROD) {
+    // ============================ producer (lane 0 issues TMA; all lanes fetch metadata)
+    if (nchunks > 0) {
+      if (lane == 0) {
+        int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+        mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
+        for (int cb = 0; cb < NCB; ++cb) {
+          tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+          tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
         }
       }
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1;
+        // rotated chunk order: concurrent CTAs start on different query blocks (no L2 hot spot)
+        const int cc = (c + crot) % nchunks;
+        const int nb = min_i(G, nq - cc * G);
+        int row0 = -1, nk = 0, qbl = 0;
+        if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
+          qbl = qlist[cc * G + lane];
+          int ko = p.kept_off[qbl];
+          nk = p.kept_off[qbl + 1] - ko;
+          row0 = bh * p.Lq + ko;
+        }
+        mbar_wait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
+        if (lane < G) {
+          s_row0[s][lane] = row0;
+          s_nk[s][lane] = nk;
+          s_qb[s][lane] = qbl;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4);
+          mbar_expect_tx(&bar_c_full[s], nb * blk_bytes);
+          BWD_TRACE(0, c);
+          for (int gi = 0; gi < nb; ++gi)  // one contiguous request per query block
+            bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + (static_cast<size_t>(bh) * g.N + s_qb[s][gi]) * blk_bytes,
+                      blk_bytes, &bar_c_full[s]);
+        }
+        // LSE and D of the chunk's rows (tiny, plain loads by all lanes); the second arrival on
+        // c_full publishes them together with the TMA bytes
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = lane + 32 * k, gi = r / SR, lr = r % SR;
+          float lv = 0.f, dv = 0.f;
+          if (gi < nb && lr < s_nk[s][gi]) {
+            lv = p.lse[s_row0[s][gi] + lr];
+            dv = p.Dvec[s_row0[s][gi] + lr];
+          }
+          stage_lse(s)[r] = lv;
+          stage_d(s)[r] = dv;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_c_full[s]);
+      }
     }
-  } else if (warp == 1) {
-    if (lane == 0 && nchunks > 0) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, BT, 0, 0);   // Q K^T / dO V^T
-      constexpr uint32_t idesc_t = umma_idesc_bf16(128, BT, 1, 1);   // dO^T P / Q^T dS (M = d padded to 128)
-      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);    // dS K
-      const uint32_t zero_lbo = (D == 64) ? 0u : 16384u;
+  } else if (warp == W_MMA) {
+    // ============================ MMA issuer: whole warp walks the schedule (uniform registers), one
+    // elected lane issues. Descriptors are precomputed bases advanced by (byte offset >> 4).
+    if (nchunks > 0) {
+      const bool leader = elect_one();
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, BT, 0, 0);  // Q K^T / dO V^T
+      constexpr uint32_t idesc_t = umma_idesc_bf16(128, BT, 1, 1);  // dO^T P / Q^T dS (M = d padded to 128)
+      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);   // dS K
+      const uint32_t zero = smem_u32(sm + SM::OFF_ZERO);
+      // K-major A over the chunk's 128 rows: 8-row groups SM::PG apart (QdO image layout)
+      const uint64_t dQa = umma_desc_sw128(smem_u32(stage_q(0)), 16, SM::PG);
+      const uint64_t dDa = umma_desc_sw128(smem_u32(stage_do(0)), 16, SM::PG);
+      // MN-major A over d (K = query rows, 16 per step = two 8-row groups, SBO = SM::PG); the second
+      // 64-channel chunk sits LBO = 1 KB after the first (d = 128)
+      const uint64_t dQt = umma_desc_sw128(smem_u32(stage_q(0)), 1024, SM::PG);
+      const uint64_t dDt = umma_desc_sw128(smem_u32(stage_do(0)), 1024, SM::PG);
+      const uint64_t dK = umma_desc_sw128(smem_u32(sK), 16, 1024), dV = umma_desc_sw128(smem_u32(sV), 16, 1024);
+      const uint64_t dKt = umma_desc_sw128(smem_u32(sK), BT * 128, 1024);
+      const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
+      const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
       mbar_wait(&bar_kv, 0);
       for (int c = 0; c < nchunks; ++c) {
-        int s = c & 1;
+        const int s = c & 1, qbuf = c & 1;
+        const uint32_t so = (s * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
         mbar_wait(&bar_c_full[s], (c >> 1) & 1);
         if (c >= 1) mbar_wait(&bar_sd_free, (c - 1) & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQ + s * SM::TILE_BYTES), da = smem_u32(sdO + s * SM::TILE_BYTES);
-        const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          int cb = kk >> 2, ko = (kk & 3) * 32;
-          umma_ss(tS, umma_desc_sw128(qa + cb * 16384 + ko, 16, 1024), umma_desc_sw128(kb + cb * BT * 128 + ko, 16, 1024),
-                  idesc_s, kk > 0);
-          umma_ss(tdP, umma_desc_sw128(da + cb * 16384 + ko, 16, 1024),
-                  umma_desc_sw128(vb + cb * BT * 128 + ko, 16, 1024), idesc_s, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const int cb = kk >> 2, ko = (kk & 3) * 32;
+            umma_ss(tS, dQa + so + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+            umma_ss(tdP, dDa + so + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+          }
+          umma_commit(&bar_sd_full);
         }
-        umma_commit(&bar_sd_full);
+        __syncwarp();
+        BWD_TRACE(1, c);
         mbar_wait(&bar_ps_full, c & 1);
-        if (c >= 1) mbar_wait(&bar_dq_free, (c - 1) & 1);
+        if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(sP), sa = smem_u32(sdS);
-        // MN-major A over d: chunk 2 (d 64..127) sits LBO bytes after chunk 1; for d = 64 it is the zero block
-        const uint32_t lbo_q = (D == 128) ? 16384u : (smem_u32(sm + SM::OFF_ZERO) - qa);
-        const uint32_t lbo_d = (D == 128) ? 16384u : (smem_u32(sm + SM::OFF_ZERO) - da);
-        (void)zero_lbo;
+        BWD_TRACE(2, c);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
-          umma_ss(tdV, umma_desc_sw128(da + kk * 2048, lbo_d, 1024), umma_desc_sw128(pa + kk * 2048, 8192, 1024),
-                  idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
-          umma_ss(tdK, umma_desc_sw128(qa + kk * 2048, lbo_q, 1024), umma_desc_sw128(sa + kk * 2048, 8192, 1024),
-                  idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
+            const uint32_t ko = (kk * 2 * SM::PG) >> 4;
+            uint64_t aq, ad;
+            if (D == 128) {
+              aq = dQt + so + ko;
+              ad = dDt + so + ko;
+            } else {  // d = 64: the missing second d-chunk reads the zero block
+              const uint32_t qk = smem_u32(stage_q(s)) + kk * 2 * SM::PG, dk = smem_u32(stage_do(s)) + kk * 2 * SM::PG;
+              aq = umma_desc_sw128(qk, zero - qk, SM::PG);
+              ad = umma_desc_sw128(dk, zero - dk, SM::PG);
+            }
+            umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+            umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < BT / 16; ++kk)
+            umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
+          umma_commit(&bar_dq_full[qbuf]);
+          umma_commit(&bar_c_empty[s]);
+          umma_commit(&bar_ps_free);
         }
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          umma_ss(tdQ, umma_desc_sw128(sa + kk * 32, 16, 1024), umma_desc_sw128(kb + kk * 2048, BT * 128, 1024),
-                  idesc_q, kk > 0);
-        umma_commit(&bar_dq_full);
-        umma_commit(&bar_c_empty[s]);
-        umma_commit(&bar_ps_free);
+        __syncwarp();
+        BWD_TRACE(3, c);
       }
+      if (leader) umma_commit(&bar_acc);
+      __syncwarp();
     }
-  } else if (warp >= 4) {
-    const int q4 = warp - 4;
+  } else if (warp < 4) {
+    // ============================ gradient softmax (thread == query row == TMEM lane)
+    const int q4 = warp;
     const int row = q4 * 32 + lane;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
     const int gi = row / SR, lr = row % SR;
@@ -257,94 +382,82 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       if (lt < xj.e[0] && lh < xj.e[1] && lw < xj.e[2]) kmask |= 1ull << c;
     }
     for (int c = 0; c < nchunks; ++c) {
-      int nb = min_i(G, nq - c * G);
-      bool valid = false;
-      size_t prow = 0;
-      float lse2 = 0.f, Dq = 0.f;
-      if (gi < nb) {
-        int qb = qlist[c * G + gi];
-        int nk = p.kept_off[qb + 1] - p.kept_off[qb];
-        if (lr < nk) {
-          valid = true;
-          prow = static_cast<size_t>(bh) * p.Lq + p.kept_off[qb] + lr;
-          lse2 = p.lse[prow] * 1.4426950408889634f;
-          Dq = p.Dvec[prow];
-        }
-      }
+      const int s = c & 1;
+      mbar_wait(&bar_c_full[s], (c >> 1) & 1);
+      const int nk = s_nk[s][gi];
+      const bool valid = lr < nk;
+      const int prow = s_row0[s][gi] + lr;
+      const float lse2 = stage_lse(s)[row] * 1.4426950408889634f;
+      const float Dq = stage_d(s)[row];
+      if (c >= 2) mbar_wait(&bar_dq_free[s], ((c - 2) >> 1) & 1);  // dQ WG done with s_dqrow[s] of chunk c-2
+      s_dqrow[s][row] = valid ? prow : -1;
       mbar_wait(&bar_sd_full, c & 1);
       tc_fence_after();
-      float sv[BT], dp[BT];
-#pragma unroll
-      for (int cc = 0; cc < BT; cc += 16) {
-        tmem_ld16(trow + cc, sv + cc);
-        tmem_ld16(trow + BT + cc, dp + cc);
-      }
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&bar_sd_free);
-#pragma unroll
-      for (int cc = 0; cc < BT; ++cc) {
-        float pr = (valid && ((kmask >> cc) & 1ull)) ? ex2b(sv[cc] * p.scale_log2 - lse2) : 0.f;
-        sv[cc] = pr;
-        dp[cc] = pr * (dp[cc] - Dq);
-      }
-      if (c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);
-#pragma unroll
-      for (int c16 = 0; c16 < BT / 8; ++c16) {
-        uint32_t wp[4], wd[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 hp = __floats2bfloat162_rn(sv[c16 * 8 + 2 * e], sv[c16 * 8 + 2 * e + 1]);
-          __nv_bfloat162 hd = __floats2bfloat162_rn(dp[c16 * 8 + 2 * e], dp[c16 * 8 + 2 * e + 1]);
-          wp[e] = *reinterpret_cast<uint32_t*>(&hp);
-          wd[e] = *reinterpret_cast<uint32_t*>(&hd);
+      if (row == 0) BWD_TRACE(4, c);
+#pragma unroll 1
+      for (int h = 0; h < BT / 32; ++h) {
+        float sv[32], dp[32];
+        tmem_ld16(trow + h * 32, sv);
+        tmem_ld16(trow + h * 32 + 16, sv + 16);
+        tmem_ld16(trow + BT + h * 32, dp);
+        tmem_ld16(trow + BT + h * 32 + 16, dp + 16);
+        tmem_wait_ld();
+        if (row == 0 && h == 0) BWD_TRACE(8, c);
+        if (h == BT / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&bar_sd_free);
         }
-        *reinterpret_cast<uint4*>(sP + sw128_off(row, c16)) = make_uint4(wp[0], wp[1], wp[2], wp[3]);
-        *reinterpret_cast<uint4*>(sdS + sw128_off(row, c16)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc) {
+          bool ok = valid && ((kmask >> (h * 32 + cc)) & 1ull);
+          float pr = ok ? ex2b(fmaf(sv[cc], p.scale_log2, -lse2)) : 0.f;
+          sv[cc] = pr;
+          dp[cc] = pr * (dp[cc] - Dq);
+        }
+        if (row == 0 && h == 0) BWD_TRACE(9, c);
+        if (h == 0 && c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+        if (row == 0 && h == 0) BWD_TRACE(10, c);
+#pragma unroll
+        for (int c8 = 0; c8 < 4; ++c8) {
+          uint32_t wp[4], wd[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 hp = __floats2bfloat162_rn(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]);
+            __nv_bfloat162 hd = __floats2bfloat162_rn(dp[c8 * 8 + 2 * e], dp[c8 * 8 + 2 * e + 1]);
+            wp[e] = *reinterpret_cast<uint32_t*>(&hp);
+            wd[e] = *reinterpret_cast<uint32_t*>(&hd);
+          }
+          *reinterpret_cast<uint4*>(sP + sw128_off(row, h * 4 + c8)) = make_uint4(wp[0], wp[1], wp[2], wp[3]);
+          *reinterpret_cast<uint4*>(sdS + sw128_off(row, h * 4 + c8)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
       }
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bar_ps_full);
-      // dQ partial of this chunk -> fp32 vector reductions into the packed accumulator
-      mbar_wait(&bar_dq_full, c & 1);
-      tc_fence_after();
-      float* dst = p.dQacc + prow * D;
-#pragma unroll 1
-      for (int cc = 0; cc < D; cc += 16) {
-        float v[16];
-        tmem_ld16(trow + 4 * BT + cc, v);
-        tmem_wait_ld();
-        if (valid) {
-#pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + cc + e), "f"(v[e]), "f"(v[e + 1]),
-                         "f"(v[e + 2]), "f"(v[e + 3])
-                         : "memory");
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&bar_dq_free);
+      if (row == 0) BWD_TRACE(5, c);
     }
     // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j
     const size_t head = static_cast<size_t>(bh) * g.L;
-    const int ch_ = row;  // channel
+    const int ch_ = row;
     if (nchunks > 0) {
-      // the last dq_full completion covers every MMA issued before it
-      float kv[BT], vv[BT];
+      mbar_wait(&bar_acc, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cc0 = 0; cc0 < BT; cc0 += 16) {
+        float kv[16], vv[16];
+        tmem_ld16(trow + 3 * BT + cc0, kv);
+        tmem_ld16(trow + 2 * BT + cc0, vv);
+        tmem_wait_ld();
+        if (ch_ < D) {
 #pragma unroll
-      for (int cc = 0; cc < BT; cc += 16) {
-        tmem_ld16(trow + 3 * BT + cc, kv + cc);
-        tmem_ld16(trow + 2 * BT + cc, vv + cc);
-      }
-      tmem_wait_ld();
-      if (ch_ < D) {
-#pragma unroll 4
-        for (int cc = 0; cc < BT; ++cc) {
-          if (!((kmask >> cc) & 1ull)) continue;
-          int lw = cc % g.cw, lh = (cc / g.cw) % g.ch, lt = cc / (g.cw * g.ch);
-          size_t tok = (static_cast<size_t>(xj.o[0] + lt) * g.H + (xj.o[1] + lh)) * g.W + (xj.o[2] + lw);
-          p.dK[(head + tok) * D + ch_] = __float2bfloat16_rn(kv[cc] * p.scale);
-          p.dV[(head + tok) * D + ch_] = __float2bfloat16_rn(vv[cc]);
+          for (int e = 0; e < 16; ++e) {
+            int cc = cc0 + e;
+            if (!((kmask >> cc) & 1ull)) continue;
+            int lw = cc % g.cw, lh = (cc / g.cw) % g.ch, lt = cc / (g.cw * g.ch);
+            size_t tok = (static_cast<size_t>(xj.o[0] + lt) * g.H + (xj.o[1] + lh)) * g.W + (xj.o[2] + lw);
+            p.dK[(head + tok) * D + ch_] = __float2bfloat16_rn(kv[e] * p.scale);
+            p.dV[(head + tok) * D + ch_] = __float2bfloat16_rn(vv[e]);
+          }
         }
       }
     } else if (ch_ < D) {
@@ -356,10 +469,43 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         p.dV[(head + tok) * D + ch_] = __float2bfloat16_rn(0.f);
       }
     }
+  } else if (warp < 8) {
+    // ============================ dQ drain: TMEM dQ partial -> fp32 vector reductions
+    const int q4 = warp - 4;
+    const int row = q4 * 32 + lane;
+    const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
+    for (int c = 0; c < nchunks; ++c) {
+      const int qbuf = c & 1;
+      mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
+      tc_fence_after();
+      if (row == 0) BWD_TRACE(6, c);
+      const int prow = s_dqrow[qbuf][row];
+      float* dst = p.dQacc + static_cast<size_t>(prow < 0 ? 0 : prow) * D;
+#pragma unroll 1
+      for (int cc = 0; cc < D; cc += 16) {
+        float v[16];
+        tmem_ld16(trow + 4 * BT + qbuf * D + cc, v);
+        tmem_wait_ld();
+#ifndef BSA_ABLATE_DQ_RED
+        if (prow >= 0) {
+#else
+        if (prow < -1) {
+#endif
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + cc + e), "f"(v[e]), "f"(v[e + 1]),
+                         "f"(v[e + 2]), "f"(v[e + 3])
+                         : "memory");
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_dq_free[qbuf]);
+      if (row == 0) BWD_TRACE(7, c);
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tbase, SM::TMEM_COLS);
+  if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------------------------ finalize
@@ -404,19 +550,18 @@ static cudaError_t run_bwd(const BwdParams& p, int BH, cudaStream_t st) {
 }
 
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
-  const size_t rows = static_cast<size_t>(a.BH) * a.Lq;
+  const size_t rows = static_cast<size_t>(a.BH) * a.g.N * a.SR;  // padded rows of the QdO images
   const unsigned prep_blocks = static_cast<unsigned>((rows * 32 + 255) / 256);
   if (a.d == 128)
-    k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.kept_tok, a.donor, a.dO, a.O, a.dOs, a.Dvec,
-                                                 a.dQacc);
+    k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
+                                                 a.O, a.qdo_img, a.Dvec, a.dQacc);
   else
-    k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.kept_tok, a.donor, a.dO, a.O, a.dOs, a.Dvec,
-                                                a.dQacc);
+    k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
+                                                a.O, a.qdo_img, a.Dvec, a.dQacc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
-  const size_t rows = static_cast<size_t>(a.BH) * a.Lq;
   BwdParams p;
   memset(&p, 0, sizeof(p));
   p.g = a.g;
@@ -426,17 +571,16 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.kept_off = a.kept_off;
   p.k2q_num = a.k2q_num;
   p.k2q_idx = a.k2q_idx;
-  p.lse = a.lse;
-  p.Dvec = a.Dvec;
   p.dQacc = a.dQacc;
   p.dK = a.dK;
   p.dV = a.dV;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.scale = a.scale;
-  if (!make_map_2d(&p.mQs, a.Qs, a.d, rows, a.SR)) return cudaErrorInvalidValue;
-  if (!make_map_2d(&p.mdOs, a.dOs, a.d, rows, a.SR)) return cudaErrorInvalidValue;
+  p.qdo_img = a.qdo_img;
   if (!make_map_5d(&p.mK, a.K, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
   if (!make_map_5d(&p.mV, a.V, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
+  p.lse = a.lse;
+  p.Dvec = a.Dvec;
   if (a.d == 128 && a.g.BT == 64) return run_bwd<128, 64>(p, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_bwd<128, 32>(p, a.BH, st);
   if (a.d == 64 && a.g.BT == 64) return run_bwd<64, 64>(p, a.BH, st);
@@ -452,6 +596,13 @@ cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
   k_bwd_finalize<<<static_cast<unsigned>((tf + 255) / 256), 256, 0, st>>>(a.BH, a.g.L, a.Lq, a.d, a.scale, a.kept_tok,
                                                                           a.dQacc, a.dQ);
   return cudaGetLastError();
+}
+
+cudaError_t debug_trace_bwd(void* dev_buf, int cta) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  cudaError_t e = cudaMemcpyToSymbol(g_bwd_trace, &p, sizeof(p));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_bwd_trace_cta, &cta, sizeof(int));
+  return e;
 }
 
 }  // namespace bsa

@@ -46,8 +46,13 @@ struct FwdArgs {
   float scale;
   bf16* O;
   float* lse;
+  const uint8_t* kv_img;  // workspace: K|V block images (launch_kv_image)
 };
+cudaError_t launch_kv_image(const Geo& g, int BH, int d, const bf16* K, const bf16* V, uint8_t* img,
+                            cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
+cudaError_t debug_trace_fwd(void* dev_buf, int cta);
+cudaError_t debug_trace_bwd(void* dev_buf, int cta);
 cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st);
 
 // a8 backward
@@ -71,8 +76,8 @@ struct BwdArgs {
   bf16* dK;
   bf16* dV;
   // workspace
-  bf16* dOs;     // packed [BH, Lq, d]
-  float* Dvec;   // [BH, Lq]
+  uint8_t* qdo_img;  // [BH, N] query-block images of Q^s|dO^s, SR*d*4 bytes each (k_bwd_prep)
+  float* Dvec;       // [BH, Lq]
   float* dQacc;  // [BH, Lq, d]
 };
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st);

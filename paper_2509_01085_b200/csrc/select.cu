@@ -108,6 +108,26 @@ __device__ __forceinline__ double dot_rows(const bf16* a, const bf16* b) {
   return s;
 }
 
+// fp32 dot of two bf16 rows (exact products, 4 independent FFMA chains; error <= gamma_D sum|a b|)
+template <int D>
+__device__ __forceinline__ float dot_rows_f32(const bf16* a, const bf16* b) {
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int c = 0; c < D; c += 8) {
+    uint4 va = *reinterpret_cast<const uint4*>(a + c);
+    uint4 vb = *reinterpret_cast<const uint4*>(b + c);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&va);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 fa = __bfloat1622float2(pa[k]), fb = __bfloat1622float2(pb[k]);
+      s[k] = fmaf(fa.x, fb.x, s[k]);
+      s[k] = fmaf(fa.y, fb.y, s[k]);
+    }
+  }
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
 // One CTA (128 threads) per (bh, block). Shared layout: rows padded to D+8 bf16 so that
 // lane-strided 16-byte row reads are bank-conflict free.
 template <int D>
@@ -203,21 +223,56 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
   __syncthreads();
   // donors (C9): warp per pruned token, lanes over kept candidates of the same unit;
   // argmax cos(q_p, q_j), ties -> lowest token
+  //
+  // Certified fp32 screening: bf16 x bf16 products are exact in fp32, so an fp32 FFMA dot over D
+  // channels is within gamma_D * sum|a_c b_c| <= gamma_D |a||b| of the exact dot (gamma_128 = 7.6e-6);
+  // with the fp64 norms the fp32 cosine is within EPS = 2e-5 of the fp64 one. A kept j whose fp32
+  // cosine is more than 2 EPS below the fp32 best can therefore not be the fp64 argmax; if only one
+  // candidate survives it IS the fp64 argmax, otherwise the survivors are re-scored with the exact
+  // fp64 formula. The decision is identical to a pure fp64 evaluation.
+  constexpr float EPS = 2e-5f;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int pi = warp; pi < s_np; pi += 4) {
     const int p = plist[pi];
-    double best = -DBL_MAX;
-    int arg = INT_MAX;
-    for (int j = lane; j < n; j += 32) {
-      if (!keep[j] || unit[j] != unit[p]) continue;
-      double c = (nrm[p] == 0.0 || nrm[j] == 0.0) ? 0.0 : dot_rows<D>(sq + p * DS, sq + j * DS) / (nrm[p] * nrm[j]);
-      if (c > best || (c == best && j < arg)) { best = c; arg = j; }
+    float cv[4];
+    float best32 = -FLT_MAX;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = lane + 32 * k;
+      cv[k] = -FLT_MAX;
+      if (j < n && keep[j] && unit[j] == unit[p]) {
+        if (nrm[p] == 0.0 || nrm[j] == 0.0) cv[k] = 0.f;
+        else cv[k] = dot_rows_f32<D>(sq + p * DS, sq + j * DS) / static_cast<float>(nrm[p] * nrm[j]);
+      }
+      best32 = fmaxf(best32, cv[k]);
     }
 #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best32 = fmaxf(best32, __shfl_xor_sync(0xffffffffu, best32, o));
+    int ncand = 0, arg = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (cv[k] >= best32 - 2.f * EPS) { ++ncand; arg = min(arg, lane + 32 * k); }
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+      ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+      arg = min(arg, __shfl_xor_sync(0xffffffffu, arg, o));
+    }
+    if (ncand > 1) {  // near tie in fp32: decide in fp64 exactly as the plain definition does
+      double best = -DBL_MAX;
+      arg = INT_MAX;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = lane + 32 * k;
+        if (cv[k] < best32 - 2.f * EPS) continue;
+        double c = (nrm[p] == 0.0 || nrm[j] == 0.0) ? 0.0 : dot_rows<D>(sq + p * DS, sq + j * DS) / (nrm[p] * nrm[j]);
+        if (c > best || (c == best && j < arg)) { best = c; arg = j; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+      }
     }
     if (lane == 0) donor[head + tok[p]] = tok[arg];
   }
@@ -242,21 +297,44 @@ cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq,
 }
 
 // a2 for K: fp64 block means (exact sums of bf16 in ascending token order)
+// 128 threads: thread = (token group tg in 0..TG-1, 8-channel chunk); 16-byte coalesced row reads.
+// Partial sums are fp64 sums of bf16 values, i.e. exact (bf16 has an 8-bit significand), so the
+// fixed-order combination below equals the sequential ascending-token sum of the oracle.
 template <int D>
-__global__ void __launch_bounds__(D) k_pool(Geo g, const bf16* __restrict__ X, double* __restrict__ Xc) {
-  const int b = blockIdx.x, bh = blockIdx.y, c = threadIdx.x;
+__global__ void __launch_bounds__(128) k_pool(Geo g, const bf16* __restrict__ X, double* __restrict__ Xc) {
+  constexpr int CH = D / 8;      // 8-channel chunks per row (16 or 8)
+  constexpr int TG = 128 / CH;   // token groups (8 or 16)
+  __shared__ double part[TG][D];
+  const int b = blockIdx.x, bh = blockIdx.y;
+  const int ck = threadIdx.x % CH, tg = threadIdx.x / CH;
   const Box x = block_box(g, b);
   const int n = box_size(x);
   const size_t head = static_cast<size_t>(bh) * g.L;
-  double s = 0.0;
-  for (int i = 0; i < n; ++i) s = dadd(s, (double)__bfloat162float(X[(head + box_token(g, x, i)) * D + c]));
-  Xc[(static_cast<size_t>(bh) * g.N + b) * D + c] = s / (double)n;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = tg; i < n; i += TG) {
+    uint4 v = *reinterpret_cast<const uint4*>(X + (head + box_token(g, x, i)) * D + ck * 8);
+    const __nv_bfloat162* pv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = __bfloat1622float2(pv[k]);
+      s[2 * k] = dadd(s[2 * k], (double)f.x);
+      s[2 * k + 1] = dadd(s[2 * k + 1], (double)f.y);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) part[tg][ck * 8 + k] = s[k];
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += 128) {
+    double t = 0.0;
+    for (int q = 0; q < TG; ++q) t = dadd(t, part[q][c]);
+    Xc[(static_cast<size_t>(bh) * g.N + b) * D + c] = t / (double)n;
+  }
 }
 
 cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, cudaStream_t st) {
   dim3 grid(g.N, BH);
   if (d == 128) k_pool<128><<<grid, 128, 0, st>>>(g, X, Xc);
-  else k_pool<64><<<grid, 64, 0, st>>>(g, X, Xc);
+  else k_pool<64><<<grid, 128, 0, st>>>(g, X, Xc);
   return cudaGetLastError();
 }
 

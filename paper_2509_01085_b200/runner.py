@@ -1,0 +1,128 @@
+"""BSAAttention: one BSA attention layer's forward + backward with every buffer preallocated.
+
+This is the call a training step makes (and what bench.py times): each method enqueues the
+C-ABI calls of include/bsa.h on the current CUDA stream; Python only passes pointers.
+
+    layer = BSAAttention(Geometry(21, 30, 52), r=0.5, f=0.1, tau=0.9, B=1, Hh=12, d=128)
+    O = layer.forward(Q, K, V)            # a1..a7: partition (cached), selection, sparse attention + fill
+    dQ, dK, dV = layer.backward(dO)       # a8
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import (OP_ATTN_BWD, OP_ATTN_FWD, OP_SELECT_KV, BSAError, Geometry, _check, _ptr, bsa_sizes, bsa_workspace_bytes, lib,
+               resolve_k)
+
+
+class BSAAttention:
+    def __init__(self, geom: Geometry, r: float, f: float, tau: float, B: int, Hh: int, d: int, device="cuda",
+                 scale=None, cache_partition: bool = True):
+        self.g, self.r, self.tau = geom, float(r), float(tau)
+        self.B, self.Hh, self.d = B, Hh, d
+        self.N, self.Lq, self.max_kept = bsa_sizes(geom, r)
+        self.k = resolve_k(f, self.N) if isinstance(f, float) else int(f)
+        self.scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        self.device = torch.device(device)
+        self.cache_partition = cache_partition
+        dev, N, Lq, L = self.device, self.N, self.Lq, geom.L
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.block_off = torch.empty(N + 1, **i32)
+        self.block_tok = torch.empty(L, **i32)
+        self.block_ext = torch.empty(N, 3, **i32)
+        self.kept_off = torch.empty(N + 1, **i32)
+        self.kept_tok = torch.empty(B, Hh, Lq, **i32)
+        self.donor = torch.empty(B, Hh, L, **i32)
+        self.q_pooled = torch.empty(B, Hh, N, d, dtype=torch.float64, device=dev)
+        self.q_packed = torch.empty(B, Hh, Lq, d, dtype=torch.bfloat16, device=dev)
+        self.q2k_num = torch.empty(B, Hh, N, **i32)
+        self.q2k_idx = torch.empty(B, Hh, N, N, **i32)
+        self.k2q_num = torch.empty(B, Hh, N, **i32)
+        self.k2q_idx = torch.empty(B, Hh, N, N, **i32)
+        self.O = torch.empty(B, Hh, L, d, dtype=torch.bfloat16, device=dev)
+        self.lse = torch.empty(B, Hh, Lq, dtype=torch.float32, device=dev)
+        self.dQ = torch.empty_like(self.O)
+        self.dK = torch.empty_like(self.O)
+        self.dV = torch.empty_like(self.O)
+        self.ws_kv_bytes = bsa_workspace_bytes(OP_SELECT_KV, geom, r, B, Hh, d)
+        self.ws_fwd_bytes = bsa_workspace_bytes(OP_ATTN_FWD, geom, r, B, Hh, d)
+        self.ws_bwd_bytes = bsa_workspace_bytes(OP_ATTN_BWD, geom, r, B, Hh, d)
+        self.ws = torch.empty(max(self.ws_kv_bytes, self.ws_fwd_bytes, self.ws_bwd_bytes, 256), dtype=torch.uint8,
+                              device=dev)
+        self._g = geom.c()
+        self._partitioned = False
+        self._saved = None
+
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def partition(self):
+        """a1; geometry-only, so cached after the first call when cache_partition."""
+        if self._partitioned and self.cache_partition:
+            return
+        _check(lib().bsa_block_partition(ctypes.byref(self._g), self.r, _ptr(self.block_off), _ptr(self.block_tok),
+                                         _ptr(self.block_ext), _ptr(self.kept_off), self._stream()),
+               "bsa_block_partition")
+        self._partitioned = True
+
+    def select(self, Q: torch.Tensor, K: torch.Tensor):
+        """a2..a6: query pruning (Eq.2) and KV-block admission (Eq.3, Eq.4) with its transpose."""
+        L, st = lib(), self._stream()
+        self.partition()
+        _check(L.bsa_select_queries(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q),
+                                    _ptr(self.kept_off), _ptr(self.kept_tok), _ptr(self.donor), _ptr(self.q_pooled),
+                                    _ptr(self.q_packed), st), "bsa_select_queries")
+        _check(L.bsa_select_kv_blocks(ctypes.byref(self._g), self.B, self.Hh, self.d, _ptr(Q), _ptr(self.q_pooled),
+                                      _ptr(K), self.k, self.tau, _ptr(self.q2k_num), _ptr(self.q2k_idx),
+                                      _ptr(self.k2q_num), _ptr(self.k2q_idx), None, _ptr(self.ws), self.ws.numel(),
+                                      st), "bsa_select_kv_blocks")
+
+    def attend(self, Q, K, V):
+        """a7 (Eq.5) + fill into self.O / self.lse."""
+        _check(lib().bsa_attn_fwd(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q), _ptr(K), _ptr(V),
+                                  _ptr(self.q_packed), _ptr(self.kept_off), _ptr(self.kept_tok), _ptr(self.donor),
+                                  _ptr(self.q2k_num), _ptr(self.q2k_idx), ctypes.c_float(self.scale), _ptr(self.O),
+                                  _ptr(self.lse), _ptr(self.ws), self.ws.numel(), self._stream()), "bsa_attn_fwd")
+        return self.O
+
+    def forward(self, Q, K, V):
+        for t in (Q, K, V):
+            if t.shape != (self.B, self.Hh, self.g.L, self.d) or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise BSAError("Q, K, V must be contiguous bf16 [B, Hh, L, d] matching the layer")
+        self.select(Q, K)
+        self._saved = (Q, K, V)
+        return self.attend(Q, K, V)
+
+    def backward(self, dO):
+        """a8: returns (dQ, dK, dV) for the last forward."""
+        if self._saved is None:
+            raise BSAError("backward() before forward()")
+        Q, K, V = self._saved
+        _check(lib().bsa_attn_bwd(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q), _ptr(K), _ptr(V),
+                                  _ptr(self.O), _ptr(dO), _ptr(self.q_packed), _ptr(self.kept_off),
+                                  _ptr(self.kept_tok), _ptr(self.donor), _ptr(self.k2q_num), _ptr(self.k2q_idx),
+                                  _ptr(self.lse), ctypes.c_float(self.scale), _ptr(self.dQ), _ptr(self.dK),
+                                  _ptr(self.dV), _ptr(self.ws), self.ws.numel(), self._stream()), "bsa_attn_bwd")
+        return self.dQ, self.dK, self.dV
+
+    # ---------------------------------------------------------------- accounting (host side, untimed)
+    def executed_pairs(self) -> int:
+        """P = sum over (b,h,i) of |kept_i| * sum_{j in S_i} |block_j| (actual tokens)."""
+        bsz = (self.block_off[1:] - self.block_off[:-1]).to(torch.int64)  # [N]
+        kept = (self.kept_off[1:] - self.kept_off[:-1]).to(torch.int64)   # [N]
+        N = self.N
+        mask = torch.arange(N, device=self.device)[None, None, None, :] < self.q2k_num[..., None]
+        idx = torch.where(mask, self.q2k_idx, torch.zeros_like(self.q2k_idx)).long()
+        kv_tokens = torch.where(mask, bsz[idx], torch.zeros_like(idx)).sum(-1)  # [B,Hh,N]
+        return int((kv_tokens * kept[None, None, :]).sum().item())
+
+    def flops(self) -> dict:
+        P = self.executed_pairs()
+        d = self.d
+        dense = self.B * self.Hh * self.g.L * self.g.L
+        return dict(pairs=P, fwd=4 * d * P, bwd=10 * d * P, total=14 * d * P, dense_total=14 * d * dense,
+                    density=P / dense)
