@@ -24,10 +24,19 @@ namespace bsa {
 __device__ unsigned long long* g_fwd_trace = nullptr;
 __device__ int g_fwd_trace_cta = 0;
 #ifdef BSA_TRACE
+__device__ __forceinline__ unsigned long long trace_clock() {
+#ifdef BSA_TRACE_GLOBALTIMER
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+#else
+  return clock64();
+#endif
+}
 #define FWD_TRACE(slot, u)                           \
   do {                                               \
     if (trace_buf != nullptr && (u) < 1024)          \
-      trace_buf[(slot) * 1024 + (u)] = clock64();    \
+      trace_buf[(slot) * 1024 + (u)] = trace_clock(); \
   } while (0)
 #else
 #define FWD_TRACE(slot, u) \
@@ -94,6 +103,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o, bar_o_final;
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
+  // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
+  // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
+  // per-column index arithmetic (which, unrolled, bloated the softmax loop past the instruction cache).
+  __shared__ uint64_t s_clsmask[8];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -101,8 +114,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   const int G = p.G, SR = p.SR;
   const int NW = (g.N + 31) >> 5;
 #ifdef BSA_TRACE
-  unsigned long long* trace_buf =
-      (static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == g_fwd_trace_cta) ? g_fwd_trace : nullptr;
+  // CTA g_fwd_trace_cta writes slots [0, 8K); with BSA_TRACE_GLOBALTIMER also CTA +1 into [8K, 16K)
+  const int my_cta = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
+  unsigned long long* trace_buf = (my_cta == g_fwd_trace_cta) ? g_fwd_trace : nullptr;
+#ifdef BSA_TRACE_GLOBALTIMER
+  if (my_cta == g_fwd_trace_cta + 1 && g_fwd_trace != nullptr) trace_buf = g_fwd_trace + 8 * 1024;
+#endif
 #endif
 
   if (tid == 0) {
@@ -130,6 +147,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     s_koff[tid] = qb < g.N ? p.kept_off[qb] : 0;
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
+  if (tid < 8) {
+    const int et = (tid & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
+    const int eh = (tid & 2) ? g.H - (g.Nh - 1) * g.ch : g.ch;
+    const int ew = (tid & 1) ? g.W - (g.Nw - 1) * g.cw : g.cw;
+    uint64_t m = 0;
+#pragma unroll 1
+    for (int c = 0; c < BT; ++c) {
+      const int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
+      if (lt < et && lh < eh && lw < ew) m |= 1ull << c;
+    }
+    s_clsmask[tid] = m;
+  }
   __syncthreads();
   // admission bitmap of each slot (q2k lists)
   for (int gi = 0; gi < G; ++gi) {
@@ -160,8 +189,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       int pos = cnt + incl - c;
       while (v) {
-        int bit = __ffs(v) - 1;
-        ulist[pos++] = static_cast<uint16_t>(w * 32 + bit);
+        const int bit = __ffs(v) - 1, j = w * 32 + bit;
+        // entry = j | extent class << 12 (N <= 4096)
+        const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+        const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
+                        (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
+        ulist[pos++] = static_cast<uint16_t>(j | (cls << 12));
         v &= v - 1;
       }
       cnt += __shfl_sync(0xffffffffu, incl, 31);
@@ -177,7 +210,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   // instead of all streaming block 0, 1, 2, ... from the same L2 slices at once (order does not change
   // the result beyond fp32 summation order).
   const int rot = U > 0 ? static_cast<int>((static_cast<unsigned>(tile) * 2654435761u + bh * 40503u) % U) : 0;
-  auto kv_at = [&](int u) { int x = u + rot; return static_cast<int>(ulist[x >= U ? x - U : x]); };
+  auto entry_at = [&](int u) { int x = u + rot; return static_cast<int>(ulist[x >= U ? x - U : x]); };
+  auto kv_at = [&](int u) { return entry_at(u) & 0xFFF; };
   constexpr uint32_t KV_BYTES = SM::KV_BYTES;
 
   if (warp == W_PROD) {
@@ -273,11 +307,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #ifdef BSA_TRACE
   } else if (warp == 4) {
     // debug observer (trace builds only): timestamps each K/V stage landing
-    if (lane == 0 && trace_buf != nullptr)
-      for (int u = 0; u < U; ++u) {
-        mbar_wait(&bar_kv_full[u % FWD_STAGES], (u / FWD_STAGES) & 1);
-        FWD_TRACE(6, u);
-      }
 #endif
   } else if (warp < 4) {
     // ============================ softmax + epilogue (thread == query row == TMEM lane)
@@ -290,10 +319,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     float m_run = -INFINITY, l_run = 0.f;
     for (int u = 0; u < U; ++u) {
       const int sb = u & 1, pb = u & 1;
-      const int j = kv_at(u);
+      const int ent = entry_at(u), j = ent & 0xFFF, cls = ent >> 12;
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
-      // key validity of block j (ragged edge blocks: only actual tokens, C23)
-      const Box xj = block_box(g, j);
       mbar_wait(&bar_s_full[sb], (u >> 1) & 1);
       if (row == 0) FWD_TRACE(4, u);
       tc_fence_after();
@@ -301,28 +328,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll
       for (int c = 0; c < BT; c += 16) tmem_ld16(trow + D + sb * BT + c, sv + c);
       tmem_wait_ld();
+      if (row == 0) FWD_TRACE(6, u);
       tc_fence_before();
       mbar_arrive(&bar_s_free[sb]);
       float alpha = 1.f;
       bool need_rescale = false;
       if (admit) {
-        float mx = -INFINITY;
-        const bool full = xj.e[0] == g.ct && xj.e[1] == g.ch && xj.e[2] == g.cw;
-        if (full) {
+        // key validity (ragged edge blocks: only actual tokens, C23); raw scores, scale folded into ex2
+        if (cls != 0) {
+          const uint64_t km = s_clsmask[cls];
+          const uint32_t k0 = static_cast<uint32_t>(km), k1 = static_cast<uint32_t>(km >> 32);
 #pragma unroll
-          for (int c = 0; c < BT; ++c) {
-            sv[c] *= p.scale_log2;
-            mx = fmaxf(mx, sv[c]);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < BT; ++c) {
-            int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
-            bool kv = lt < xj.e[0] && lh < xj.e[1] && lw < xj.e[2];
-            sv[c] = kv ? sv[c] * p.scale_log2 : -INFINITY;
-            mx = fmaxf(mx, sv[c]);
-          }
+          for (int c = 0; c < BT; ++c)
+            if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
         }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < BT; ++c) mx = fmaxf(mx, sv[c]);
+        mx *= p.scale_log2;
 #ifndef BSA_ABLATE_RESCALE
         if (mx > m_run + 8.f) {  // conditional rescale: keep the stale max unless it grew by > 2^8
 #else
@@ -334,7 +357,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         }
         float sum = 0.f;
 #pragma unroll
-        for (int c = 0; c < BT; ++c) { sv[c] = ex2(sv[c] - m_run); sum += sv[c]; }
+        for (int c = 0; c < BT; ++c) { sv[c] = ex2(fmaf(sv[c], p.scale_log2, -m_run)); sum += sv[c]; }
         l_run += sum;
       } else {
 #pragma unroll
@@ -343,6 +366,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       // P buffer pb is free once PV(u-2) completed. Waiting here first also bounds bar_o to at most
       // one phase behind PV(u-1), which makes the parity wait below unambiguous.
       if (u >= 2) mbar_wait(&bar_p_free[pb], ((u - 2) >> 1) & 1);
+      if (row == 0) FWD_TRACE(7, u);
       // O rescale in TMEM (needs PV(u-1) complete); warp-collective access
       if (__any_sync(0xffffffffu, need_rescale)) {
         mbar_wait(&bar_o, (u - 1) & 1);

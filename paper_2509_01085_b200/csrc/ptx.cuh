@@ -44,6 +44,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 // Blocking wait for the phase with the given parity. try_wait with an explicit suspend-time hint in an
 // asm-level retry loop: the hint-less form measured ~11k-cycle late wake-ups on B200.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef BSA_WAIT_POLL
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "BSA_WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra BSA_DONE_%=;\n\t"
+      "bra BSA_WAIT_%=;\n\t"
+      "BSA_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "BSA_WAIT_%=:\n\t"
