@@ -145,7 +145,7 @@ BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   w.qs = 0;
   w.img = w.qs + align256(BH * Lq * d * 2);
   w.dv = w.img + align256(BH * g.N * static_cast<size_t>(SR) * d * 4);
-  w.dq = w.dv + align256(BH * Lq * 4);
+  w.dq = w.dv + align256(BH * g.N * static_cast<size_t>(SR) * 8);
   w.total = w.dq + align256(BH * Lq * d * 4);
   return w;
 }
@@ -427,7 +427,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.dK = static_cast<bsa::bf16*>(dK);
   a.dV = static_cast<bsa::bf16*>(dV);
   a.qdo_img = base + w.img;
-  a.Dvec = reinterpret_cast<float*>(base + w.dv);
+  a.lsed = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_BWD, 1, st, [&] { return bsa::launch_bwd_main(a, st); });

@@ -25,7 +25,7 @@ namespace bsa {
 
 bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
 bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int BH);
-bool make_map_1d_f32(CUtensorMap* m, const void* base, size_t n, int box);
+bool make_map_rows_f32(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -38,13 +38,16 @@ __device__ __forceinline__ float ex2b(float x) {
 // SR/8 groups of 8 rows; group q holds [Q^s d-half 0][Q^s d-half 1][dO^s d-half 0][dO^s d-half 1], each
 // 8 rows x 128 B with the 128-byte swizzle. Consecutive groups (also across the blocks stacked in a
 // chunk) are 2*NCB KB apart, so every UMMA operand over the chunk's 128 rows has a uniform stride.
-// One warp per padded row (b,h, block, row < SR); rows beyond the block's kept count are zero.
+// Next to it, the block's row statistics lsed[(b,h,block)] = [LSE*log2(e) of its SR rows][D of its SR rows]
+// (one more bulk copy per block). One warp per padded row (b,h, block, row < SR); rows beyond the block's
+// kept count are zero with LSE = +inf, D = 0, so they contribute P = dS = 0.
 template <int D>
 __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR, const int* __restrict__ kept_off,
                                                   const int* __restrict__ kept_tok, const int* __restrict__ donor,
                                                   const bf16* __restrict__ Qs, const bf16* __restrict__ dO,
-                                                  const bf16* __restrict__ O, uint8_t* __restrict__ qdo_img,
-                                                  float* __restrict__ Dvec, float* __restrict__ dQacc) {
+                                                  const bf16* __restrict__ O, const float* __restrict__ lse,
+                                                  uint8_t* __restrict__ qdo_img, float* __restrict__ lsed,
+                                                  float* __restrict__ dQacc) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
   constexpr int NCB = D / 64;
   const size_t wid = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -60,7 +63,12 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
   const uint32_t inrow = sw128_off(lr & 7, (ch0 & 63) >> 3) + (ch0 & 7) * 2;
   uint8_t* qdst = gbase + (ch0 >> 6) * 1024 + inrow;
   uint8_t* ddst = gbase + (NCB + (ch0 >> 6)) * 1024 + inrow;
+  float* ld = lsed + bi * 2 * SR + lr;
   if (lr >= nk) {
+    if (lane == 0) {
+      ld[0] = INFINITY;
+      ld[SR] = 0.f;
+    }
     if (PER == 4) {
       *reinterpret_cast<uint2*>(qdst) = make_uint2(0, 0);
       *reinterpret_cast<uint2*>(ddst) = make_uint2(0, 0);
@@ -112,7 +120,10 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
   else *reinterpret_cast<uint32_t*>(ddst) = *reinterpret_cast<const uint32_t*>(hv);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-  if (lane == 0) Dvec[prow] = dsum;
+  if (lane == 0) {
+    ld[0] = lse[prow] * 1.4426950408889634f;
+    ld[SR] = dsum;
+  }
   float* dq = dQacc + prow * D + lane * PER;
 #pragma unroll
   for (int e = 0; e < PER; ++e) dq[e] = 0.f;
@@ -139,10 +150,10 @@ struct BwdParams {
   const uint8_t* qdo_img;  // per query block Q^s|dO^s images (k_bwd_prep), SR*d*4 bytes each
   CUtensorMap mK;    // 5D block map
   CUtensorMap mV;
+  CUtensorMap mDQ;     // dQacc [BH*Lq, d] fp32, box {16, dq_rows}, 64B swizzle (bulk reduce-add target)
   Geo g;
-  const float* lse;  // [BH*Lq] packed
-  const float* Dvec;
-  int Lq, SR, G;
+  const float* lsed;   // per query block [LSE*log2e x SR][D x SR] (k_bwd_prep)
+  int Lq, SR, G, dq_rows;
   const int* kept_off;
   const int* k2q_num;
   const int* k2q_idx;
@@ -162,14 +173,15 @@ struct BwdSmem {
   static constexpr int KV_BYTES = BT * D * 2;
   static constexpr int TILE_BYTES = 128 * D * 2;            // Q^s or dO^s rows of one chunk
   static constexpr int PG = 2 * NCB * 1024;                 // stride of 8-row groups in a QdO image
-  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 2048;  // QdO images of the chunk's blocks, lse[128], D[128]
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 1024;  // QdO images of the chunk's blocks + their lsed
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
   static constexpr int OFF_ST = OFF_V + KV_BYTES;           // 2 stages
   static constexpr int OFF_P = OFF_ST + 2 * STAGE_BYTES;    // [128][64] bf16
   static constexpr int OFF_DS = OFF_P + 16384;
   static constexpr int OFF_ZERO = OFF_DS + 16384;           // d=64 only: zero MN chunk for M=128 padding
-  static constexpr int TOTAL = OFF_ZERO + (D == 64 ? 16384 : 0) + 1024;
+  static constexpr int OFF_DQS = OFF_ZERO + (D == 64 ? 16384 : 0);  // dQ drain: 4 warps x 2 slots x [32][16] fp32
+  static constexpr int TOTAL = OFF_DQS + 4 * 2 * 2048 + 1024;
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
@@ -185,18 +197,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   uint8_t* sdS = sm + SM::OFF_DS;
   auto stage_q = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES; };  // Q^s d-half 0 of group 0
   auto stage_do = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES + NCB * 1024; };
-  auto stage_lse = [&](int s) {
+  auto stage_ld = [&](int s) {  // lsed of the chunk's blocks: block gi at [gi * 2 SR, (gi + 1) * 2 SR)
     return reinterpret_cast<float*>(sm + SM::OFF_ST + s * SM::STAGE_BYTES + 2 * SM::TILE_BYTES);
-  };
-  auto stage_d = [&](int s) {
-    return reinterpret_cast<float*>(sm + SM::OFF_ST + s * SM::STAGE_BYTES + 2 * SM::TILE_BYTES + 1024);
   };
 
   __shared__ __align__(8) uint64_t bar_kv, bar_c_full[2], bar_c_empty[2], bar_sd_full, bar_sd_free, bar_ps_full,
       bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc;
   __shared__ uint32_t s_tmem;
   __shared__ int s_row0[2][BWD_MAX_G], s_nk[2][BWD_MAX_G], s_qb[2][BWD_MAX_G];
-  __shared__ int s_dqrow[2][128];
+  // dQ destinations of the chunk in each TMEM dQ buffer (first packed row and kept count per block; row -1 =
+  // no block), copied by the softmax warps so the drain never races the producer refilling s_row0/s_nk
+  __shared__ int s_dqr0[2][BWD_MAX_G], s_dqnk[2][BWD_MAX_G];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -211,7 +222,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   if (tid == 0) {
     mbar_init(&bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar_c_full[s], 2);  // TMA transaction arrival + LSE/D arrival
+      mbar_init(&bar_c_full[s], 1);
       mbar_init(&bar_c_empty[s], 1);
       mbar_init(&bar_dq_full[s], 1);
       mbar_init(&bar_dq_free[s], 128);
@@ -274,28 +285,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         }
         __syncwarp();
         if (lane == 0) {
-          const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4);
-          mbar_expect_tx(&bar_c_full[s], nb * blk_bytes);
+          const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
+          mbar_expect_tx(&bar_c_full[s], nb * (blk_bytes + ld_bytes));
           BWD_TRACE(0, c);
-          for (int gi = 0; gi < nb; ++gi)  // one contiguous request per query block
-            bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + (static_cast<size_t>(bh) * g.N + s_qb[s][gi]) * blk_bytes,
-                      blk_bytes, &bar_c_full[s]);
-        }
-        // LSE and D of the chunk's rows (tiny, plain loads by all lanes); the second arrival on
-        // c_full publishes them together with the TMA bytes
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = lane + 32 * k, gi = r / SR, lr = r % SR;
-          float lv = 0.f, dv = 0.f;
-          if (gi < nb && lr < s_nk[s][gi]) {
-            lv = p.lse[s_row0[s][gi] + lr];
-            dv = p.Dvec[s_row0[s][gi] + lr];
+          for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
+#ifndef BSA_ABLATE_BWD_HOTSET
+            const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[s][gi];
+#else
+            const size_t qimg = static_cast<size_t>(bh) * g.N + gi;
+#endif
+            bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + qimg * blk_bytes, blk_bytes, &bar_c_full[s]);
+            bulk_load(stage_ld(s) + gi * 2 * SR, p.lsed + qimg * 2 * SR, ld_bytes, &bar_c_full[s]);
           }
-          stage_lse(s)[r] = lv;
-          stage_d(s)[r] = dv;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_c_full[s]);
       }
     }
   } else if (warp == W_MMA) {
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         const int s = c & 1, qbuf = c & 1;
         const uint32_t so = (s * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
         mbar_wait(&bar_c_full[s], (c >> 1) & 1);
+        BWD_TRACE(11, c);
         if (c >= 1) mbar_wait(&bar_sd_free, (c - 1) & 1);
         tc_fence_after();
         if (leader) {
@@ -384,13 +388,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     for (int c = 0; c < nchunks; ++c) {
       const int s = c & 1;
       mbar_wait(&bar_c_full[s], (c >> 1) & 1);
-      const int nk = s_nk[s][gi];
-      const bool valid = lr < nk;
-      const int prow = s_row0[s][gi] + lr;
-      const float lse2 = stage_lse(s)[row] * 1.4426950408889634f;
-      const float Dq = stage_d(s)[row];
-      if (c >= 2) mbar_wait(&bar_dq_free[s], ((c - 2) >> 1) & 1);  // dQ WG done with s_dqrow[s] of chunk c-2
-      s_dqrow[s][row] = valid ? prow : -1;
+      const bool valid = lr < s_nk[s][gi];  // (slots past the chunk's last block have nk = 0)
+      const float lse2 = stage_ld(s)[gi * 2 * SR + lr];
+      const float Dq = stage_ld(s)[gi * 2 * SR + SR + lr];
+      if (row < G) {
+        if (c >= 2) mbar_wait(&bar_dq_free[s], ((c - 2) >> 1) & 1);  // drain done with s_dq*[s] of chunk c-2
+        s_dqr0[s][row] = s_row0[s][row];
+        s_dqnk[s][row] = s_nk[s][row];
+      }
       mbar_wait(&bar_sd_full, c & 1);
       tc_fence_after();
       if (row == 0) BWD_TRACE(4, c);
@@ -470,38 +475,62 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       }
     }
   } else if (warp < 8) {
-    // ============================ dQ drain: TMEM dQ partial -> fp32 vector reductions
+    // ============================ dQ drain: TMEM dQ partial -> smem slices -> TMA bulk reduce-add
+    // Each warp owns TMEM lane quadrant q4 (chunk rows 32 q4 .. +32), split into 32/R sub-boxes of R =
+    // min(SR, 32) rows that each belong to one query block and map to R consecutive packed dQacc rows.
+    // Per 16-column slice: tcgen05.ld -> [32][16] fp32 slot (64B swizzle, the map's layout) -> one
+    // cp.reduce.async.bulk.tensor add per sub-box; the L2 does the fp32 adds (no per-thread atomics).
+    // Rows past a block's kept count hold exact zeros (P = dS = 0 there), so a sub-box may overlap the
+    // next block's rows harmlessly.
     const int q4 = warp - 4;
     const int row = q4 * 32 + lane;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
+    uint8_t* slots = sm + SM::OFF_DQS + q4 * 2 * 2048;
+    const int R = p.dq_rows, nsub = 32 / R;
+    int nslice = 0;
     for (int c = 0; c < nchunks; ++c) {
       const int qbuf = c & 1;
       mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
       tc_fence_after();
       if (row == 0) BWD_TRACE(6, c);
-      const int prow = s_dqrow[qbuf][row];
-      float* dst = p.dQacc + static_cast<size_t>(prow < 0 ? 0 : prow) * D;
-#pragma unroll 1
-      for (int cc = 0; cc < D; cc += 16) {
-        float v[16];
-        tmem_ld16(trow + 4 * BT + qbuf * D + cc, v);
-        tmem_wait_ld();
-#ifndef BSA_ABLATE_DQ_RED
-        if (prow >= 0) {
-#else
-        if (prow < -1) {
-#endif
+      int dst = -1;  // lane k < nsub: first dQacc row of sub-box k
+      if (lane < nsub) {
+        const int r0 = q4 * 32 + lane * R, gi = r0 / SR, lr0 = r0 % SR;
+        if (gi < G && s_dqr0[qbuf][gi] >= 0 && lr0 < s_dqnk[qbuf][gi]) dst = s_dqr0[qbuf][gi] + lr0;
+      }
+      int dk[4];
 #pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + cc + e), "f"(v[e]), "f"(v[e + 1]),
-                         "f"(v[e + 2]), "f"(v[e + 3])
-                         : "memory");
+      for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
+      if (__any_sync(0xffffffffu, dst >= 0)) {
+#pragma unroll 1
+        for (int cs = 0; cs < D; cs += 16, ++nslice) {
+          float v[16];
+          tmem_ld16(trow + 4 * BT + qbuf * D + cs, v);
+          uint8_t* slot = slots + (nslice & 1) * 2048;
+          if (lane == 0) bulk_wait_group_read<1>();  // the reduce issued from this slot 2 slices ago read it
+          __syncwarp();
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<float4*>(slot + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+#ifndef BSA_ABLATE_DQ_RED
+            for (int k = 0; k < nsub; ++k)
+              if (dk[k] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 64, cs, dk[k]);
+#endif
+            bulk_commit_group();
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&bar_dq_free[qbuf]);
       if (row == 0) BWD_TRACE(7, c);
     }
+    if (lane == 0) bulk_wait_group<0>();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -554,10 +583,10 @@ cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
   const unsigned prep_blocks = static_cast<unsigned>((rows * 32 + 255) / 256);
   if (a.d == 128)
     k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                 a.O, a.qdo_img, a.Dvec, a.dQacc);
+                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc);
   else
     k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                a.O, a.qdo_img, a.Dvec, a.dQacc);
+                                                a.O, a.lse, a.qdo_img, a.lsed, a.dQacc);
   return cudaGetLastError();
 }
 
@@ -579,8 +608,9 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.qdo_img = a.qdo_img;
   if (!make_map_5d(&p.mK, a.K, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
   if (!make_map_5d(&p.mV, a.V, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
-  p.lse = a.lse;
-  p.Dvec = a.Dvec;
+  p.lsed = a.lsed;
+  p.dq_rows = a.SR < 32 ? a.SR : 32;
+  if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
   if (a.d == 128 && a.g.BT == 64) return run_bwd<128, 64>(p, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_bwd<128, 32>(p, a.BH, st);
   if (a.d == 64 && a.g.BT == 64) return run_bwd<64, 64>(p, a.BH, st);

@@ -77,7 +77,7 @@ struct BwdArgs {
   bf16* dV;
   // workspace
   uint8_t* qdo_img;  // [BH, N] query-block images of Q^s|dO^s, SR*d*4 bytes each (k_bwd_prep)
-  float* Dvec;       // [BH, Lq]
+  float* lsed;       // [BH, N, 2, SR]: per query block LSE*log2(e) of its SR rows, then D of its SR rows
   float* dQacc;  // [BH, Lq, d]
 };
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st);
