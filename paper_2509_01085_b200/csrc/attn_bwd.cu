@@ -140,9 +140,20 @@ __device__ int g_bwd_trace_cta = 0;
     if (_t != nullptr && (int)(blockIdx.y * gridDim.x + blockIdx.x) == g_bwd_trace_cta && (u) < 1024) \
       _t[(slot) * 1024 + (u)] = clock64();                                                              \
   } while (0)
+#define CTA_STAMP(k)                                                                                   \
+  do {                                                                                                 \
+    if (g_bwd_trace != nullptr && g_bwd_trace_cta == -1) {                                             \
+      unsigned long long _g;                                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                                          \
+      g_bwd_trace[8 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x) + (k)] = _g;           \
+    }                                                                                                  \
+  } while (0)
 #else
 #define BWD_TRACE(slot, u) \
   do {                     \
+  } while (0)
+#define CTA_STAMP(k) \
+  do {               \
   } while (0)
 #endif
 
@@ -150,7 +161,9 @@ struct BwdParams {
   const uint8_t* qdo_img;  // per query block Q^s|dO^s images (k_bwd_prep), SR*d*4 bytes each
   CUtensorMap mK;    // 5D block map
   CUtensorMap mV;
-  CUtensorMap mDQ;     // dQacc [BH*Lq, d] fp32, box {16, dq_rows}, 64B swizzle (bulk reduce-add target)
+  CUtensorMap mDQ;     // dQacc [BH*Lq, d] fp32, box {32, dq_rows}, 128B swizzle (bulk reduce-add target)
+  CUtensorMap mdK;     // 5D block maps over the dK / dV outputs (TMA store of the finished block)
+  CUtensorMap mdV;
   Geo g;
   const float* lsed;   // per query block [LSE*log2e x SR][D x SR] (k_bwd_prep)
   int Lq, SR, G, dq_rows;
@@ -180,8 +193,9 @@ struct BwdSmem {
   static constexpr int OFF_P = OFF_ST + 2 * STAGE_BYTES;    // [128][64] bf16
   static constexpr int OFF_DS = OFF_P + 16384;
   static constexpr int OFF_ZERO = OFF_DS + 16384;           // d=64 only: zero MN chunk for M=128 padding
-  static constexpr int OFF_DQS = OFF_ZERO + (D == 64 ? 16384 : 0);  // dQ drain: 4 warps x 2 slots x [32][16] fp32
-  static constexpr int TOTAL = OFF_DQS + 4 * 2 * 2048 + 1024;
+  static constexpr int DQ_SLOTS = 3;                         // per drain warp, [32][16] fp32 each
+  static constexpr int OFF_DQS = OFF_ZERO + (D == 64 ? 16384 : 0);
+  static constexpr int TOTAL = OFF_DQS + 4 * DQ_SLOTS * 2048 + 1024;
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
@@ -204,10 +218,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   __shared__ __align__(8) uint64_t bar_kv, bar_c_full[2], bar_c_empty[2], bar_sd_full, bar_sd_free, bar_ps_full,
       bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc;
   __shared__ uint32_t s_tmem;
-  __shared__ int s_row0[2][BWD_MAX_G], s_nk[2][BWD_MAX_G], s_qb[2][BWD_MAX_G];
-  // dQ destinations of the chunk in each TMEM dQ buffer (first packed row and kept count per block; row -1 =
-  // no block), copied by the softmax warps so the drain never races the producer refilling s_row0/s_nk
-  __shared__ int s_dqr0[2][BWD_MAX_G], s_dqnk[2][BWD_MAX_G];
+  // Chunk metadata ring (first packed row, kept count, block id of each slot; row -1 = empty slot), written
+  // by the producer for chunk c into entry c & 3. Four deep: the producer rewrites an entry only after
+  // the MMAs of chunk c-2 completed, by which time the softmax and drain warps are done with chunk c-4.
+  __shared__ int s_row0[4][BWD_MAX_G], s_nk[4][BWD_MAX_G], s_qb[4][BWD_MAX_G];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -219,6 +233,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   const int nchunks = (nq + G - 1) / G;
   const int crot = nchunks > 0 ? static_cast<int>((static_cast<unsigned>(j) * 2654435761u + bh * 40503u) % nchunks) : 0;
 
+#ifdef BSA_TRACE
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   if (tid == 0) {
     mbar_init(&bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
@@ -251,8 +269,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = s_tmem;
+  // TMEM columns: S, dP, dV^T, dK^T, dQ of chunk parity 0, dQ of parity 1
   const uint32_t tS = tbase, tdP = tbase + BT, tdV = tbase + 2 * BT, tdK = tbase + 3 * BT, tdQ = tbase + 4 * BT;
-  const Box xj = block_box(g, j);
+  if (tid == 0) CTA_STAMP(4);
 
   if (warp == W_PROD) {
     // ============================ producer (lane 0 issues TMA; all lanes fetch metadata)
@@ -278,10 +297,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           row0 = bh * p.Lq + ko;
         }
         mbar_wait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
+        const int ring = c & 3;
         if (lane < G) {
-          s_row0[s][lane] = row0;
-          s_nk[s][lane] = nk;
-          s_qb[s][lane] = qbl;
+          s_row0[ring][lane] = row0;
+          s_nk[ring][lane] = nk;
+          s_qb[ring][lane] = qbl;
         }
         __syncwarp();
         if (lane == 0) {
@@ -290,7 +310,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           BWD_TRACE(0, c);
           for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
 #ifndef BSA_ABLATE_BWD_HOTSET
-            const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[s][gi];
+            const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[ring][gi];
 #else
             const size_t qimg = static_cast<size_t>(bh) * g.N + gi;
 #endif
@@ -322,26 +342,45 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
       const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
       mbar_wait(&bar_kv, 0);
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c & 1, qbuf = c & 1;
-        const uint32_t so = (s * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
-        mbar_wait(&bar_c_full[s], (c >> 1) & 1);
-        BWD_TRACE(11, c);
-        if (c >= 1) mbar_wait(&bar_sd_free, (c - 1) & 1);
+      // S/dP(v) = Q^s K^T, dO^s V^T of chunk v (single TMEM buffer, free once the softmax warps have
+      // loaded S/dP(v-1) into registers)
+      auto issue_sd = [&](int v) {
+        const int sv = v & 1;
+        const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
+        mbar_wait(&bar_c_full[sv], (v >> 1) & 1);
+        BWD_TRACE(11, v);
+        if (v >= 1) mbar_wait(&bar_sd_free, (v - 1) & 1);
         tc_fence_after();
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const int cb = kk >> 2, ko = (kk & 3) * 32;
-            umma_ss(tS, dQa + so + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
-            umma_ss(tdP, dDa + so + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+            umma_ss(tS, dQa + sov + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+            umma_ss(tdP, dDa + sov + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
           }
           umma_commit(&bar_sd_full);
         }
         __syncwarp();
-        BWD_TRACE(1, c);
-        mbar_wait(&bar_ps_full, c & 1);
-        if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);
+        BWD_TRACE(1, v);
+      };
+      auto sd_ready = [&](int v) {  // non-blocking: operands of S/dP(v) landed and its TMEM buffer is free
+        bool ok = mbar_try_wait(&bar_c_full[v & 1], (v >> 1) & 1) && mbar_try_wait(&bar_sd_free, (v - 1) & 1);
+        return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+      };
+      // Software pipeline: S/dP of chunk c+1 goes on the tensor pipe ahead of the gradient MMAs of chunk c
+      // when its operands are already there (the softmax warps then never wait for it); otherwise the
+      // gradient MMAs go first, so the stage they free starts reloading without waiting on a load.
+      issue_sd(0);
+      int next_sd = 1;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1, qbuf = c & 1;
+        const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
+        // wait for P/dS(c), issuing S/dP(c+1) meanwhile as soon as it can go
+        while (true) {
+          if (next_sd == c + 1 && next_sd < nchunks && sd_ready(next_sd)) issue_sd(next_sd++);
+          if (__shfl_sync(0xffffffffu, mbar_try_wait(&bar_ps_full, c & 1) ? 1 : 0, 0)) break;
+        }
+        if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
         tc_fence_after();
         BWD_TRACE(2, c);
         if (leader) {
@@ -360,181 +399,233 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
             umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
           }
+          umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
             umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
           umma_commit(&bar_dq_full[qbuf]);
-          umma_commit(&bar_c_empty[s]);
           umma_commit(&bar_ps_free);
         }
         __syncwarp();
         BWD_TRACE(3, c);
+        if (next_sd == c + 1 && next_sd < nchunks) issue_sd(next_sd++);
       }
       if (leader) umma_commit(&bar_acc);
       __syncwarp();
     }
+#ifdef BSA_TRACE
+  } else if (warp == 9) {
+    // debug observer (trace builds only): when each chunk's loads land
+    if (lane == 0)
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&bar_c_full[c & 1], (c >> 1) & 1);
+        BWD_TRACE(12, c);
+      }
+    __syncwarp();
+#endif
   } else if (warp < 4) {
     // ============================ gradient softmax (thread == query row == TMEM lane)
     const int q4 = warp;
     const int row = q4 * 32 + lane;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
     const int gi = row / SR, lr = row % SR;
-    // key validity of block j (ragged edges, C23)
-    uint64_t kmask = 0;
-    for (int c = 0; c < BT; ++c) {
-      int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
-      if (lt < xj.e[0] && lh < xj.e[1] && lw < xj.e[2]) kmask |= 1ull << c;
-    }
+    // Key columns of a ragged block past its extent need no mask here: their K/V rows arrive as zeros
+    // (TMA out-of-grid fill), so they add nothing to dQ = dS K, and their dK/dV columns are never stored.
+    const float sl2 = p.scale_log2;
+    const uint32_t sP_u = smem_u32(sP) + row * 128, sdS_u = smem_u32(sdS) + row * 128;
     for (int c = 0; c < nchunks; ++c) {
       const int s = c & 1;
       mbar_wait(&bar_c_full[s], (c >> 1) & 1);
-      const bool valid = lr < s_nk[s][gi];  // (slots past the chunk's last block have nk = 0)
-      const float lse2 = stage_ld(s)[gi * 2 * SR + lr];
-      const float Dq = stage_ld(s)[gi * 2 * SR + SR + lr];
-      if (row < G) {
-        if (c >= 2) mbar_wait(&bar_dq_free[s], ((c - 2) >> 1) & 1);  // drain done with s_dq*[s] of chunk c-2
-        s_dqr0[s][row] = s_row0[s][row];
-        s_dqnk[s][row] = s_nk[s][row];
-      }
+      const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
+      const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
+      const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
       mbar_wait(&bar_sd_full, c & 1);
       tc_fence_after();
       if (row == 0) BWD_TRACE(4, c);
-#pragma unroll 1
-      for (int h = 0; h < BT / 32; ++h) {
-        float sv[32], dp[32];
-        tmem_ld16(trow + h * 32, sv);
-        tmem_ld16(trow + h * 32 + 16, sv + 16);
-        tmem_ld16(trow + BT + h * 32, dp);
-        tmem_ld16(trow + BT + h * 32 + 16, dp + 16);
-        tmem_wait_ld();
-        if (row == 0 && h == 0) BWD_TRACE(8, c);
-        if (h == BT / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&bar_sd_free);
-        }
+      // the whole S/dP row goes to registers first, so the TMEM buffer is handed back to the MMA warp
+      // (S/dP of the next chunk) before any math
+      float sv[BT], dp[BT];
 #pragma unroll
-        for (int cc = 0; cc < 32; ++cc) {
-          bool ok = valid && ((kmask >> (h * 32 + cc)) & 1ull);
-          float pr = ok ? ex2b(fmaf(sv[cc], p.scale_log2, -lse2)) : 0.f;
-          sv[cc] = pr;
-          dp[cc] = pr * (dp[cc] - Dq);
-        }
-        if (row == 0 && h == 0) BWD_TRACE(9, c);
-        if (h == 0 && c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
-        if (row == 0 && h == 0) BWD_TRACE(10, c);
+      for (int c16 = 0; c16 < BT; c16 += 16) {
+        tmem_ld16(trow + c16, sv + c16);
+        tmem_ld16(trow + BT + c16, dp + c16);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bar_sd_free);
+      if (row == 0) BWD_TRACE(8, c);
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
-          uint32_t wp[4], wd[4];
+      for (int cc = 0; cc < BT; ++cc) {
+        const float pr = ex2b(fmaf(sv[cc], sl2, nl));
+        sv[cc] = pr;
+        dp[cc] = pr * (dp[cc] - Dq);
+      }
+      if (row == 0) BWD_TRACE(9, c);
+      if (c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+      if (row == 0) BWD_TRACE(10, c);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 hp = __floats2bfloat162_rn(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]);
-            __nv_bfloat162 hd = __floats2bfloat162_rn(dp[c8 * 8 + 2 * e], dp[c8 * 8 + 2 * e + 1]);
-            wp[e] = *reinterpret_cast<uint32_t*>(&hp);
-            wd[e] = *reinterpret_cast<uint32_t*>(&hd);
-          }
-          *reinterpret_cast<uint4*>(sP + sw128_off(row, h * 4 + c8)) = make_uint4(wp[0], wp[1], wp[2], wp[3]);
-          *reinterpret_cast<uint4*>(sdS + sw128_off(row, h * 4 + c8)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        }
+      for (int c8 = 0; c8 < BT / 8; ++c8) {
+        const uint32_t off = ((static_cast<uint32_t>(c8) ^ (row & 7)) << 4);
+        const float* a = sv + c8 * 8;
+        const float* b = dp + c8 * 8;
+        sts128(sP_u + off, pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+        sts128(sdS_u + off, pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]), pack_bf16(b[4], b[5]), pack_bf16(b[6], b[7]));
       }
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bar_ps_full);
       if (row == 0) BWD_TRACE(5, c);
     }
-    // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j
-    const size_t head = static_cast<size_t>(bh) * g.L;
+    if (row == 0) CTA_STAMP(5);
+    // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j. Transposed into
+    // the block's [key][64-channel] SW128 tiles in smem (stage 0 is idle now) and written with the same
+    // 5D block box the K/V tiles came in with, so keys past a ragged block's extent are clipped by TMA.
     const int ch_ = row;
+    const uint32_t tdk = smem_u32(stage_q(0)), tdv = tdk + NCB * BT * 128;
     if (nchunks > 0) {
       mbar_wait(&bar_acc, 0);
       tc_fence_after();
+    }
 #pragma unroll 1
-      for (int cc0 = 0; cc0 < BT; cc0 += 16) {
-        float kv[16], vv[16];
+    for (int cc0 = 0; cc0 < BT; cc0 += 16) {
+      float kv[16], vv[16];
+      if (nchunks > 0) {
         tmem_ld16(trow + 3 * BT + cc0, kv);
         tmem_ld16(trow + 2 * BT + cc0, vv);
         tmem_wait_ld();
-        if (ch_ < D) {
+      } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            int cc = cc0 + e;
-            if (!((kmask >> cc) & 1ull)) continue;
-            int lw = cc % g.cw, lh = (cc / g.cw) % g.ch, lt = cc / (g.cw * g.ch);
-            size_t tok = (static_cast<size_t>(xj.o[0] + lt) * g.H + (xj.o[1] + lh)) * g.W + (xj.o[2] + lw);
-            p.dK[(head + tok) * D + ch_] = __float2bfloat16_rn(kv[e] * p.scale);
-            p.dV[(head + tok) * D + ch_] = __float2bfloat16_rn(vv[e]);
-          }
+        for (int e = 0; e < 16; ++e) kv[e] = vv[e] = 0.f;
+      }
+      if (ch_ < D) {
+        const uint32_t cofs = (ch_ >> 6) * BT * 128 + (ch_ & 7) * 2;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t o = cofs + sw128_off(cc0 + e, (ch_ & 63) >> 3);
+          sts16(tdk + o, __bfloat16_as_ushort(__float2bfloat16_rn(kv[e] * p.scale)));
+          sts16(tdv + o, __bfloat16_as_ushort(__float2bfloat16_rn(vv[e])));
         }
       }
-    } else if (ch_ < D) {
-      for (int cc = 0; cc < BT; ++cc) {
-        if (!((kmask >> cc) & 1ull)) continue;
-        int lw = cc % g.cw, lh = (cc / g.cw) % g.ch, lt = cc / (g.cw * g.ch);
-        size_t tok = (static_cast<size_t>(xj.o[0] + lt) * g.H + (xj.o[1] + lh)) * g.W + (xj.o[2] + lw);
-        p.dK[(head + tok) * D + ch_] = __float2bfloat16_rn(0.f);
-        p.dV[(head + tok) * D + ch_] = __float2bfloat16_rn(0.f);
-      }
     }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (row == 0) {
+      const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+      for (int cb = 0; cb < NCB; ++cb) {
+        tma_store_5d(&p.mdK, stage_q(0) + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+        tma_store_5d(&p.mdV, stage_q(0) + NCB * BT * 128 + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct,
+                     bh);
+      }
+      tma_store_commit_and_wait();
+    }
+    if (row == 0) CTA_STAMP(6);
   } else if (warp < 8) {
     // ============================ dQ drain: TMEM dQ partial -> smem slices -> TMA bulk reduce-add
     // Each warp owns TMEM lane quadrant q4 (chunk rows 32 q4 .. +32), split into 32/R sub-boxes of R =
-    // min(SR, 32) rows that each belong to one query block and map to R consecutive packed dQacc rows.
-    // Per 16-column slice: tcgen05.ld -> [32][16] fp32 slot (64B swizzle, the map's layout) -> one
-    // cp.reduce.async.bulk.tensor add per sub-box; the L2 does the fp32 adds (no per-thread atomics).
-    // Rows past a block's kept count hold exact zeros (P = dS = 0 there), so a sub-box may overlap the
-    // next block's rows harmlessly.
+    // min(SR, 16) rows that each belong to one query block and map to R consecutive packed dQacc rows.
+    // Per 32-column slice: tcgen05.ld -> two 16-row x 128 B slots (128B swizzle, the map's layout) ->
+    // one cp.reduce.async.bulk.tensor add per sub-box; the L2 does the fp32 adds (no per-thread atomics;
+    // 128-byte row segments reach ~6 TB/s of reduce traffic on B200, dbg/red_rate.cu). Rows past a
+    // block's kept count hold exact zeros (P = dS = 0 there), so a sub-box may overlap the next block's
+    // rows harmlessly. Slots form a per-warp ring; each 16-row half is one bulk group.
     const int q4 = warp - 4;
     const int row = q4 * 32 + lane;
-    const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
-    uint8_t* slots = sm + SM::OFF_DQS + q4 * 2 * 2048;
-    const int R = p.dq_rows, nsub = 32 / R;
-    int nslice = 0;
+    uint8_t* slots = sm + SM::OFF_DQS + q4 * SM::DQ_SLOTS * 2048;
+    const int R = p.dq_rows, nsub = 32 / R, per_half = 16 / R;
+    int slot_i = 0;
     for (int c = 0; c < nchunks; ++c) {
       const int qbuf = c & 1;
       mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
       tc_fence_after();
       if (row == 0) BWD_TRACE(6, c);
+      const int ring = c & 3;
       int dst = -1;  // lane k < nsub: first dQacc row of sub-box k
       if (lane < nsub) {
         const int r0 = q4 * 32 + lane * R, gi = r0 / SR, lr0 = r0 % SR;
-        if (gi < G && s_dqr0[qbuf][gi] >= 0 && lr0 < s_dqnk[qbuf][gi]) dst = s_dqr0[qbuf][gi] + lr0;
+        if (gi < G && s_row0[ring][gi] >= 0 && lr0 < s_nk[ring][gi]) dst = s_row0[ring][gi] + lr0;
       }
       int dk[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
-      if (__any_sync(0xffffffffu, dst >= 0)) {
+      const bool any = __any_sync(0xffffffffu, dst >= 0);
 #pragma unroll 1
-        for (int cs = 0; cs < D; cs += 16, ++nslice) {
-          float v[16];
-          tmem_ld16(trow + 4 * BT + qbuf * D + cs, v);
-          uint8_t* slot = slots + (nslice & 1) * 2048;
-          if (lane == 0) bulk_wait_group_read<1>();  // the reduce issued from this slot 2 slices ago read it
-          __syncwarp();
-          tmem_wait_ld();
+      for (int cs = 0; cs < D; cs += 32) {
+        float v[32];
+        const uint32_t tq = tdQ + qbuf * D + (static_cast<uint32_t>(q4 * 32) << 16) + cs;
+        tmem_ld16(tq, v);
+        tmem_ld16(tq + 16, v + 16);
+        tmem_wait_ld();
+        if (cs + 32 == D) {  // the whole partial is out of TMEM: dQ buffer free for chunk c+2
+          tc_fence_before();
+          mbar_arrive(&bar_dq_free[qbuf]);
+        }
+#ifdef BSA_DQ_RED_SLICES
+        if (cs < BSA_DQ_RED_SLICES * 32) {
+          const int sb = lane / R;
+          const int drow = __shfl_sync(0xffffffffu, dst, sb);
+          if (drow >= 0) {
+            float* gp = p.dQacc + static_cast<size_t>(drow + lane % R) * D + cs;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<float4*>(slot + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
-                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            for (int e = 0; e < 32; e += 4)
+              asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gp + e), "f"(v[e]), "f"(v[e + 1]),
+                           "f"(v[e + 2]), "f"(v[e + 3])
+                           : "memory");
+          }
+          continue;
+        }
+#endif
+        if (any) {
+          const int s0 = slot_i, s1 = slot_i + 1 == SM::DQ_SLOTS ? 0 : slot_i + 1;
+          slot_i = s1 + 1 == SM::DQ_SLOTS ? 0 : s1 + 1;
+          // the two slots' previous reduces (issued >= 1 group ago) must have read them
+          if (lane == 0) bulk_wait_group_read<SM::DQ_SLOTS - 2>();
+          __syncwarp();
+          const int rr = lane & 15;
+          const uint32_t srow = smem_u32(slots + ((lane >> 4) ? s1 : s0) * 2048) + rr * 128;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts128(srow + ((k ^ (rr & 7)) << 4), __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                   __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
 #ifndef BSA_ABLATE_DQ_RED
-            for (int k = 0; k < nsub; ++k)
-              if (dk[k] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 64, cs, dk[k]);
+              uint8_t* slot = slots + (hf ? s1 : s0) * 2048;
+              for (int k = 0; k < per_half; ++k) {
+                const int sb = hf * per_half + k;
+                if (dk[sb] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 128, cs, dk[sb]);
+              }
 #endif
-            bulk_commit_group();
+              bulk_commit_group();
+            }
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&bar_dq_free[qbuf]);
       if (row == 0) BWD_TRACE(7, c);
     }
     if (lane == 0) bulk_wait_group<0>();
+    if (row == 0) CTA_STAMP(7);
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
+#ifdef BSA_TRACE
+  // trace mode cta == -1: per-CTA [start, end, smid, nchunks] (globaltimer ns)
+  if (g_bwd_trace != nullptr && g_bwd_trace_cta == -1 && tid == 0) {
+    unsigned long long* e = g_bwd_trace + 8 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x);
+    unsigned long long t1;
+    unsigned sm_id;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    e[0] = t_start;
+    e[1] = t1;
+    e[2] = sm_id;
+    e[3] = nchunks;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------ finalize
@@ -608,8 +699,10 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.qdo_img = a.qdo_img;
   if (!make_map_5d(&p.mK, a.K, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
   if (!make_map_5d(&p.mV, a.V, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
+  if (!make_map_5d(&p.mdK, a.dK, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
+  if (!make_map_5d(&p.mdV, a.dV, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
   p.lsed = a.lsed;
-  p.dq_rows = a.SR < 32 ? a.SR : 32;
+  p.dq_rows = a.SR < 16 ? a.SR : 16;
   if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
   if (a.d == 128 && a.g.BT == 64) return run_bwd<128, 64>(p, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_bwd<128, 32>(p, a.BH, st);

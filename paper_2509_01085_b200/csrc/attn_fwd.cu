@@ -466,16 +466,16 @@ bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_r
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 2D row map over a packed [rows, d] fp32 matrix, box {16, box_rows} (64-byte rows), 64B swizzle.
+// 2D row map over a packed [rows, d] fp32 matrix, box {32, box_rows} (128-byte rows), 128B swizzle.
 bool make_map_rows_f32(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
   cuuint64_t str[1] = {static_cast<cuuint64_t>(d) * 4};
-  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, str, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
