@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         // wait for P/dS(c), issuing S/dP(c+1) meanwhile as soon as it can go
         while (true) {
           if (next_sd == c + 1 && next_sd < nchunks && sd_ready(next_sd)) issue_sd(next_sd++);
-          if (__shfl_sync(0xffffffffu, mbar_try_wait(&bar_ps_full, c & 1) ? 1 : 0, 0)) break;
+          // suspend (bounded) instead of spinning: the MMA warp shares its sub-partition with a softmax warp
+          if (__shfl_sync(0xffffffffu, mbar_wait_for(&bar_ps_full, c & 1, 100) ? 1 : 0, 0)) break;
         }
         if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
         tc_fence_after();

@@ -4,16 +4,20 @@
 //
 // B200 design:
 //  * One CTA per query tile = G consecutive query blocks, each in its own slot of SR = 128/G rows of
-//    the packed Q^s (kept queries, block-major). Q^s slots arrive by 2D TMA (128B swizzle).
-//  * The CTA walks the ascending UNION of its blocks' KV lists. Every KV block j is one 5D TMA box
-//    (64 channels x cw x ch x ct) straight from the raster [B,Hh,L,d] tensor: no permuted copy of
-//    K/V; out-of-grid (ragged edge) rows arrive as zeros and are masked to -inf.
-//  * S = Q^s K_j^T (M=128, N=BT) and O += P V_j (M=128, N=d) are tcgen05.mma kind::f16 with fp32
-//    accumulators in TMEM, issued by one thread; S is double-buffered in TMEM so QK(j+1) overlaps the
-//    softmax of j. Rows whose block did not admit j write P = 0 (their MMA work is the union waste).
+//    the packed Q^s (kept queries, block-major). The softmax threads copy their Q^s row straight from
+//    global memory into TMEM (packed bf16 pairs): Q is the A operand of every S MMA and is never
+//    re-read from shared memory.
+//  * The CTA walks the UNION of its blocks' KV lists (rotated start). KV block j arrives as ONE bulk
+//    copy of its pre-swizzled K|V image (k_kv_image) into a 6-deep stage ring.
+//  * S = Q^s K_j^T (M=128, N=BT) and O += P V_j (M=128, N=d) are tcgen05.mma kind::f16 with the A
+//    operand in TMEM (Q, then P) and fp32 accumulators in TMEM; only K and V are read from shared
+//    memory (the SS form with N = 64 is shared-memory-bandwidth bound on B200: dbg/mma_rate.cu).
+//    S and P are double-buffered in TMEM so QK(j+1) overlaps the softmax of j. Rows whose block did
+//    not admit j write P = 0 (their MMA work is the union waste).
 //  * Softmax: 128 threads, thread == TMEM lane == query row; online softmax in fp32 (log2 domain),
 //    O rescaled in TMEM only when the running max grows by more than 2^8 (exact: same final ratio).
-//  * Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 softmax/epilogue.
+//  * Warp roles: w0-3 softmax/epilogue, w5 TMEM allocator, w6 bulk-copy producer, w7 MMA issuer
+//    (control roles on the highest warp ids: the warp arbiter favours them).
 #include <cmath>
 #include "kernels.h"
 #include "ptx.cuh"
@@ -45,7 +49,7 @@ __device__ __forceinline__ unsigned long long trace_clock() {
 #endif
 
 struct FwdParams {
-  CUtensorMap mQs;  // 2D {d, BH*Lq}, box {64, SR}
+  const bf16* Qs;         // packed kept queries [BH*Lq, d] (block-major)
   const uint8_t* kv_img;  // block-major K|V images (k_kv_image): one contiguous 2*BT*d*2-byte request per block
   Geo g;
   int Lq, SR, G;
@@ -59,25 +63,22 @@ struct FwdParams {
 };
 
 constexpr int FWD_THREADS = 256;
-constexpr int FWD_STAGES = 4;
+constexpr int FWD_STAGES = 6;
 constexpr int MAX_N = 4096;
 constexpr int MAX_G = 16;
 
 template <int D, int BT>
 struct FwdSmem {
-  static constexpr int NCB = D / 64;
-  static constexpr int Q_BYTES = 128 * D * 2;
   static constexpr int KV_BYTES = BT * D * 2;  // one K or V tile
-  static constexpr int P_BYTES = 128 * 128;    // [128][64] bf16, 128B rows
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;      // stage s: K tile at OFF_K + 2 s KV_BYTES, V right after
-  static constexpr int OFF_V = OFF_K + KV_BYTES;
-  static constexpr int OFF_P = OFF_K + FWD_STAGES * 2 * KV_BYTES;
-  static constexpr int OFF_BITS = OFF_P + 2 * P_BYTES;
+  static constexpr int OFF_K = 0;               // stage s: K tile at OFF_K + 2 s KV_BYTES, V right after
+  static constexpr int OFF_BITS = OFF_K + FWD_STAGES * 2 * KV_BYTES;
   static constexpr int BITS_BYTES = MAX_G * (MAX_N / 32) * 4;
   static constexpr int OFF_ULIST = OFF_BITS + BITS_BYTES + 32 * 4;  // + union words
   static constexpr int ULIST_BYTES = MAX_N * 2;
   static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
+  // TMEM columns: O [0, D), S double buffer, Q^s (packed bf16 pairs), P double buffer (packed)
+  static constexpr int T_O = 0, T_S = D, T_Q = D + 2 * BT, T_P = T_Q + D / 2;
+  static constexpr int TMEM_COLS = (T_P + BT) <= 256 ? 256 : 512;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -89,17 +90,13 @@ __device__ __forceinline__ float ex2(float x) {
 template <int D, int BT>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_constant__ FwdParams p) {
   using SM = FwdSmem<D, BT>;
-  constexpr int NCB = SM::NCB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm + SM::OFF_Q;
   uint8_t* sK = sm + SM::OFF_K;
-  uint8_t* sV = sm + SM::OFF_V;
-  uint8_t* sP = sm + SM::OFF_P;
   uint32_t* bits = reinterpret_cast<uint32_t*>(sm + SM::OFF_BITS);
   uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
 
-  __shared__ __align__(8) uint64_t bar_q, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
+  __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
       bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o, bar_o_final;
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
@@ -123,7 +120,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #endif
 
   if (tid == 0) {
-    mbar_init(&bar_q, 1);
+    mbar_init(&bar_qt, 128);
     for (int s = 0; s < FWD_STAGES; ++s) { mbar_init(&bar_kv_full[s], 1); mbar_init(&bar_kv_empty[s], 1); }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
@@ -135,11 +132,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     mbar_init(&bar_o_final, 1);
     fence_mbar_init();
   }
-  // Warp roles. The SM's warp arbiter favours higher warp ids, so the latency-critical single-thread
-  // roles (TMA producer, MMA issuer) get the highest ids and are never starved by the softmax warps
-  // that share their sub-partition; softmax warps 0-3 read TMEM lane quadrant (warp % 4).
   constexpr int W_ALLOC = 5, W_PROD = 6, W_MMA = 7;
-  if (warp == W_ALLOC) tmem_alloc(&s_tmem, 256);
+  if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
   if (tid < G) {
     int qb = tile * G + tid;
     s_qb[tid] = qb < g.N ? qb : -1;
@@ -215,17 +209,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   constexpr uint32_t KV_BYTES = SM::KV_BYTES;
 
   if (warp == W_PROD) {
-    // ============================ TMA producer
+    // ============================ bulk-copy producer
     if (lane == 0) {
-      tma_prefetch(&p.mQs);
-      int nvalid = 0;
-      for (int gi = 0; gi < G; ++gi) nvalid += (s_qb[gi] >= 0);
-      mbar_expect_tx(&bar_q, static_cast<uint32_t>(nvalid * NCB * SR * 128));
-      for (int gi = 0; gi < G; ++gi) {
-        if (s_qb[gi] < 0) continue;
-        int row0 = bh * p.Lq + s_koff[gi];
-        for (int cb = 0; cb < NCB; ++cb) tma_load_2d(sQ + cb * 16384 + gi * SR * 128, &p.mQs, &bar_q, cb * 64, row0);
-      }
       for (int u = 0; u < U; ++u) {
         int s = u % FWD_STAGES;
         mbar_wait(&bar_kv_empty[s], ((u / FWD_STAGES) & 1) ^ 1);
@@ -246,18 +231,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const bool leader = elect_one();
     constexpr uint32_t idesc_qk = umma_idesc_bf16(128, BT, 0, 0);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, D, 0, 1);
-    const uint32_t tO = tbase, tS = tbase + D;
+    const uint32_t tO = tbase + SM::T_O, tS = tbase + SM::T_S, tQ = tbase + SM::T_Q, tP = tbase + SM::T_P;
     // base descriptors; an operand at byte offset o from the base is base + (o >> 4)
-    const uint64_t dQ0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t dK0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
-    const uint64_t dV0 = umma_desc_sw128(smem_u32(sV), BT * 128, 1024);
-    const uint64_t dP0 = umma_desc_sw128(smem_u32(sP), 16, 1024);
-    mbar_wait(&bar_q, 0);
-    auto qk_inputs_ready = [&](int v) {
-      bool ok = mbar_try_wait(&bar_kv_full[v % FWD_STAGES], (v / FWD_STAGES) & 1);
-      if (ok && v >= 2) ok = mbar_try_wait(&bar_s_free[v & 1], ((v - 2) >> 1) & 1);
-      return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
-    };
+    const uint64_t dV0 = umma_desc_sw128(smem_u32(sK + KV_BYTES), BT * 128, 1024);
+    mbar_wait(&bar_qt, 0);  // Q^s is in TMEM
     auto issue_qk = [&](int v) {  // S(v) = Q^s K_v^T into S buffer v & 1
       const int s = v % FWD_STAGES, sb = v & 1;
       mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
@@ -269,7 +247,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         for (int kk = 0; kk < D / 16; ++kk) {
           const int cb = kk >> 2, ko = (kk & 3) * 32;
 #ifndef BSA_ABLATE_FWD_MMA
-          umma_ss(tS + sb * BT, dQ0 + ((cb * 16384 + ko) >> 4), kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
+          umma_ts(tS + sb * BT, tQ + kk * 8, kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
 #endif
         }
         umma_commit(&bar_s_full[sb]);
@@ -277,21 +255,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       __syncwarp();
       FWD_TRACE(1, v);
     };
-    int next_qk = 0;
-    issue_qk(next_qk++);
+    // Order on the tensor pipe: QK(u+1) ahead of PV(u), so S(u+1) is ready when the softmax warps
+    // finish P(u). Every wait here suspends (no spinning: the MMA warp shares its sub-partition with a
+    // softmax warp). The K|V ring runs FWD_STAGES steps ahead, so QK(u+1)'s operands are normally there.
+    issue_qk(0);
     for (int u = 0; u < U; ++u) {
-      // QK(u+1) goes ahead of PV(u) only if its operands already landed: PV(u) never waits for a load
-      if (next_qk == u + 1 && next_qk < U && qk_inputs_ready(next_qk)) issue_qk(next_qk++);
       const int pb = u & 1, s = u % FWD_STAGES;
+      if (u + 1 < U) issue_qk(u + 1);
       mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
       FWD_TRACE(2, u);
       tc_fence_after();
-      const uint64_t pst = dP0 + ((pb * SM::P_BYTES) >> 4), vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
+      const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
       if (leader) {
 #pragma unroll
         for (int kk = 0; kk < BT / 16; ++kk) {
 #ifndef BSA_ABLATE_FWD_MMA
-          umma_ss(tO, pst + ((kk * 32) >> 4), vst + ((kk * 2048) >> 4), idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+          umma_ts(tO, tP + pb * (BT / 2) + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
 #endif
         }
         umma_commit(&bar_kv_empty[s]);
@@ -300,14 +279,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       __syncwarp();
       FWD_TRACE(3, u);
-      if (next_qk == u + 1 && next_qk < U) issue_qk(next_qk++);
     }
     if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
     __syncwarp();
-#ifdef BSA_TRACE
-  } else if (warp == 4) {
-    // debug observer (trace builds only): timestamps each K/V stage landing
-#endif
   } else if (warp < 4) {
     // ============================ softmax + epilogue (thread == query row == TMEM lane)
     const int q4 = warp;
@@ -316,6 +290,28 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
     const uint32_t* mybits = bits + (gi < G ? gi : 0) * NW;
+    const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0;
+    {
+      // Q^s row -> TMEM (A operand of the S MMAs): bf16 pairs are already packed in memory order
+      const uint4* src = reinterpret_cast<const uint4*>(p.Qs + prow_idx * D);
+#pragma unroll
+      for (int c0 = 0; c0 < D / 2; c0 += 16) {
+        float w[16];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint4 v = valid ? src[c0 / 4 + e] : make_uint4(0, 0, 0, 0);
+          w[4 * e] = __uint_as_float(v.x);
+          w[4 * e + 1] = __uint_as_float(v.y);
+          w[4 * e + 2] = __uint_as_float(v.z);
+          w[4 * e + 3] = __uint_as_float(v.w);
+        }
+        tmem_st16(trow + SM::T_Q + c0, w);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bar_qt);
+    }
+    const float sl2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
     for (int u = 0; u < U; ++u) {
       const int sb = u & 1, pb = u & 1;
@@ -326,9 +322,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       tc_fence_after();
       float sv[BT];
 #pragma unroll
-      for (int c = 0; c < BT; c += 16) tmem_ld16(trow + D + sb * BT + c, sv + c);
+      for (int c = 0; c < BT; c += 16) tmem_ld16(trow + SM::T_S + sb * BT + c, sv + c);
       tmem_wait_ld();
       if (row == 0) FWD_TRACE(6, u);
+      if (lane == 0) FWD_TRACE(12 + q4, u);
       tc_fence_before();
       mbar_arrive(&bar_s_free[sb]);
       float alpha = 1.f;
@@ -342,10 +339,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           for (int c = 0; c < BT; ++c)
             if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
         }
-        float mx = -INFINITY;
+        // row max and row sum with independent partial accumulators: a single serial chain of BT dependent
+        // FMNMX/FADD would cost more than the MUFU work it waits on
+        float mp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < BT; ++c) mx = fmaxf(mx, sv[c]);
-        mx *= p.scale_log2;
+        for (int c = 0; c < BT; ++c) mp[c & 3] = fmaxf(mp[c & 3], sv[c]);
+        float mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])) * sl2;
 #ifndef BSA_ABLATE_RESCALE
         if (mx > m_run + 8.f) {  // conditional rescale: keep the stale max unless it grew by > 2^8
 #else
@@ -355,18 +354,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           l_run *= alpha;
           m_run = mx;
         }
-        float sum = 0.f;
+        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < BT; ++c) { sv[c] = ex2(fmaf(sv[c], p.scale_log2, -m_run)); sum += sv[c]; }
-        l_run += sum;
+        for (int c = 0; c < BT; ++c) { sv[c] = ex2(fmaf(sv[c], sl2, -m_run)); sp[c & 7] += sv[c]; }
+        l_run += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
       } else {
 #pragma unroll
         for (int c = 0; c < BT; ++c) sv[c] = 0.f;
       }
       // P buffer pb is free once PV(u-2) completed. Waiting here first also bounds bar_o to at most
       // one phase behind PV(u-1), which makes the parity wait below unambiguous.
+      if (lane == 0) FWD_TRACE(16 + q4, u);
       if (u >= 2) mbar_wait(&bar_p_free[pb], ((u - 2) >> 1) & 1);
       if (row == 0) FWD_TRACE(7, u);
+      if (lane == 0) FWD_TRACE(20 + q4, u);
       // O rescale in TMEM (needs PV(u-1) complete); warp-collective access
       if (__any_sync(0xffffffffu, need_rescale)) {
         mbar_wait(&bar_o, (u - 1) & 1);
@@ -374,42 +375,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
           float ov[16];
-          tmem_ld16(trow + c, ov);
+          tmem_ld16(trow + SM::T_O + c, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 16; ++e) ov[e] *= alpha;
-          tmem_st16(trow + c, ov);
+          tmem_st16(trow + SM::T_O + c, ov);
         }
-        tmem_wait_st();
       }
-      // P row -> smem (bf16, 128B-swizzled [128][64])
-      uint8_t* prow = sP + pb * SM::P_BYTES;
+      if (lane == 0) FWD_TRACE(24 + q4, u);
+      // P row -> TMEM (bf16 pairs, the A operand of PV)
 #pragma unroll
-      for (int c16 = 0; c16 < BT / 8; ++c16) {
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(sv[c16 * 8 + 0], sv[c16 * 8 + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(sv[c16 * 8 + 2], sv[c16 * 8 + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(sv[c16 * 8 + 4], sv[c16 * 8 + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(sv[c16 * 8 + 6], sv[c16 * 8 + 7]);
-        uint4 v;
-        v.x = *reinterpret_cast<uint32_t*>(&h0);
-        v.y = *reinterpret_cast<uint32_t*>(&h1);
-        v.z = *reinterpret_cast<uint32_t*>(&h2);
-        v.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(prow + sw128_off(row, c16)) = v;
+      for (int c0 = 0; c0 < BT / 2; c0 += 16) {
+        float w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(pack_bf16(sv[2 * (c0 + e)], sv[2 * (c0 + e) + 1]));
+        tmem_st16(trow + SM::T_P + pb * (BT / 2) + c0, w);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar_p_full[pb]);
       if (row == 0) FWD_TRACE(5, u);
+      if (lane == 0) FWD_TRACE(8 + q4, u);
     }
     // epilogue: O^s = O / l, scattered to the kept token's raster row; LSE in natural log
     mbar_wait(&bar_o_final, 0);
     tc_fence_after();
     const float inv = valid ? 1.f / l_run : 0.f;
-    size_t prow_idx = 0;
     bf16* orow = nullptr;
     if (valid) {
-      prow_idx = static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr;
       int tok = p.kept_tok[prow_idx];
       orow = p.O + (static_cast<size_t>(bh) * g.L + tok) * D;
       p.lse[prow_idx] = (m_run + log2f(l_run)) * 0.6931471805599453f;
@@ -417,15 +410,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll 1
     for (int c = 0; c < D; c += 16) {
       float ov[16];
-      tmem_ld16(trow + c, ov);
+      tmem_ld16(trow + SM::T_O + c, ov);
       tmem_wait_ld();
       if (valid) {
         uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(ov[2 * e] * inv, ov[2 * e + 1] * inv);
-          w[e] = *reinterpret_cast<uint32_t*>(&h);
-        }
+        for (int e = 0; e < 8; ++e) w[e] = pack_bf16(ov[2 * e] * inv, ov[2 * e + 1] * inv);
         *reinterpret_cast<uint4*>(orow + c) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
       }
@@ -433,7 +423,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == W_ALLOC) tmem_dealloc(tbase, 256);
+  if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------------------------ host
@@ -519,7 +509,7 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.O = a.O;
   p.lse = a.lse;
   p.kv_img = a.kv_img;
-  if (!make_map_2d(&p.mQs, a.Qs, a.d, static_cast<size_t>(a.BH) * a.Lq, a.SR)) return cudaErrorInvalidValue;
+  p.Qs = a.Qs;
   int ntiles = (a.g.N + p.G - 1) / p.G;
   if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_fwd<128, 32>(p, ntiles, a.BH, st);
