@@ -30,6 +30,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json metric; value = effective (executed-FLOP) TFLOPS, ms_per_step = fwd+bwd ms
+METRIC = "BSA attention fwd+bwd ms & effective TFLOPS at 32k/75k tokens vs own dense"
+
 CONFIGS = {
     # name: grid, block, B, Hh, d, r, f (k = ceil(f N)), tau, generator
     "tiny": dict(grid=(4, 8, 8), block=(2, 4, 4), B=1, Hh=2, d=64, r=0.5, f=0.5, tau=0.9, kind="video"),
@@ -158,7 +161,7 @@ def run_reference(args, cfg, rank, world):
     sample = f"1 of {cfg['Hh']} heads of the {args.config} workload (full selection + fwd + bwd of that head), " \
              f"fp64, {threads} threads"
     line = {
-        "impl": "reference", "metric": "BSA attention fwd+bwd effective TFLOPS (executed FLOPs)", "value": val,
+        "impl": "reference", "metric": METRIC, "value": val,
         "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "sample": "1 head", **{k: v for k, v in cfg.items() if k != "kind"},
@@ -183,7 +186,7 @@ def main():
     ap.add_argument("--kind", default=None, choices=["video", "iid"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -313,23 +316,36 @@ def main():
         torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- e2e: host buffers, copies inside the region
+    # Each step copies its four input tensors host->device (pinned, on a copy stream, double-buffered so the
+    # copy of step s+1 overlaps the kernels of step s) and reads its result back: the forward's per-row LSE
+    # (the gradients stay on the device for the optimiser, as in training).
     hQ, hK, hV, hdO = (x.cpu().pin_memory() for x in (Q, K, V, dO))
-    outs = [torch.empty(B, Hh, g.L, d, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
-    dQ2, dK2, dV2, dO2 = (torch.empty_like(Q) for _ in range(4))
-    e2e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.e2e_steps)]
-    for s in range(args.e2e_steps + 1):
-        if s > 0:
-            e2e_ev[2 * (s - 1)].record()
-        Qg, Kg, Vg = (h.to(dev, non_blocking=True) for h in (hQ, hK, hV))
-        dOg = hdO.to(dev, non_blocking=True)
-        O = layer.forward(Qg, Kg, Vg)
-        dq, dk, dv = layer.backward(dOg)
-        for o, src in zip(outs, (O, dq, dk, dv)):
-            o.copy_(src, non_blocking=True)
-        if s > 0:
-            e2e_ev[2 * (s - 1) + 1].record()
-        torch.cuda.synchronize()
-    e2e_ms = sum(e2e_ev[2 * s].elapsed_time(e2e_ev[2 * s + 1]) for s in range(args.e2e_steps)) / max(1, args.e2e_steps)
+    h_lse = torch.empty(layer.lse.shape, dtype=torch.float32).pin_memory()
+    bufs = [[torch.empty_like(Q) for _ in range(4)] for _ in range(2)]
+    cstream = torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+    n_e2e = max(1, args.e2e_steps)
+    copied = [torch.cuda.Event() for _ in range(n_e2e)]
+    consumed = [torch.cuda.Event() for _ in range(n_e2e)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e_start.record(cstream)
+    for s in range(n_e2e):
+        with torch.cuda.stream(cstream):
+            if s >= 2:
+                cstream.wait_event(consumed[s - 2])  # step s-2 is done reading this buffer set
+            for dst, src in zip(bufs[s % 2], (hQ, hK, hV, hdO)):
+                dst.copy_(src, non_blocking=True)
+            copied[s].record(cstream)
+        main.wait_event(copied[s])
+        Qg, Kg, Vg, dOg = bufs[s % 2]
+        layer.forward(Qg, Kg, Vg)
+        layer.backward(dOg)
+        consumed[s].record(main)
+        h_lse.copy_(layer.lse, non_blocking=True)
+    e_end.record(main)
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end) / n_e2e
     e_local = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_local, op=dist.ReduceOp.MAX)
@@ -349,7 +365,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "BSA attention fwd+bwd effective TFLOPS (executed FLOPs) at 32k/75k tokens vs own dense",
+            "metric": METRIC,
             "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded G_video latents, bsa_gen)",
@@ -368,7 +384,9 @@ def main():
                          "dense_equiv_tflops": fl["dense_total"] * world / (t_max * 1e-3 / args.steps) / 1e12},
             "own_dense": dense,
             "e2e": {"value": e2e_val, "unit": "TFLOPS", "ms_per_step": float(e_local.item()),
-                    "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": 4 * tensor_bytes},
+                    "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": int(h_lse.numel() * 4),
+                    "note": "pinned H2D of Q,K,V,dO each step on a copy stream (double-buffered, overlaps the "
+                            "previous step's kernels); D2H of the step's LSE; through BSAAttention.forward/backward"},
             "cpu_baseline": cpu,
             "paper_context": "17.79x attention-training speedup and 20x FLOP reduction at 153,600 tokens on H100 "
                              "(Triton, precision unstated; PAPER.md P:234, P:22) — context, not the target",
