@@ -9,14 +9,14 @@
 //               S  = Q^s K_j^T, dP = dO^s V_j^T            (M=128 queries, N=BT keys)
 //               P  = exp(scale S - LSE), dS = P (dP - D)    (thread == query row)
 //               dV_j^T += dO^s^T P, dK_j^T += Q^s^T dS      (M=d=128, N=BT, K=128 queries; TMEM-resident)
-//               dQ_part = dS K_j                            (M=128, N=d) -> fp32 vector reductions
+//               dQ_part = dS K_j                            (M=128, N=d) -> L2 bulk reduce-add
 //   finalize: dQ[kept] = scale * dQacc (bf16), dQ[pruned] = 0.
 //
-// Warp roles of the main kernel (384 threads): w0 TMA producer (all lanes fetch the chunk's block
-// metadata in parallel; Q^s/dO^s tiles by 2D TMA, LSE/D rows by 1D TMA), w1 MMA issuer, w2 TMEM
-// allocator, w4-w7 gradient-softmax warpgroup (thread == query row), w8-w11 dQ warpgroup that drains
-// the double-buffered dQ accumulator (TMEM) into the packed fp32 dQ with red.global.add.v4.f32 while
-// the next chunk is computed.
+// Warp roles of the main kernel (384 threads): w0-3 gradient softmax (thread == query
+// row == TMEM lane), w4-7 dQ drain (TMEM -> smem slices -> cp.reduce.async.bulk.tensor into the packed
+// fp32 dQacc), w8 TMEM allocator, w10 bulk-copy producer (per query block: its QdO image and its LSE/D
+// row statistics), w11 MMA issuer. The control roles sit on the highest warp ids (the warp arbiter
+// favours them) and suspend on mbarriers rather than spin.
 #include <cmath>
 #include "kernels.h"
 #include "ptx.cuh"
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     // min(SR, 16) rows that each belong to one query block and map to R consecutive packed dQacc rows.
     // Per 32-column slice: tcgen05.ld -> two 16-row x 128 B slots (128B swizzle, the map's layout) ->
     // one cp.reduce.async.bulk.tensor add per sub-box; the L2 does the fp32 adds (no per-thread atomics;
-    // 128-byte row segments reach ~6 TB/s of reduce traffic on B200, dbg/red_rate.cu). Rows past a
+    // 128-byte row segments reach ~6 TB/s of reduce traffic on B200, tools/microbench/red_rate.cu). Rows past a
     // block's kept count hold exact zeros (P = dS = 0 there), so a sub-box may overlap the next block's
     // rows harmlessly. Slots form a per-warp ring; each 16-row half is one bulk group.
     const int q4 = warp - 4;

@@ -11,7 +11,7 @@
 //    copy of its pre-swizzled K|V image (k_kv_image) into a 6-deep stage ring.
 //  * S = Q^s K_j^T (M=128, N=BT) and O += P V_j (M=128, N=d) are tcgen05.mma kind::f16 with the A
 //    operand in TMEM (Q, then P) and fp32 accumulators in TMEM; only K and V are read from shared
-//    memory (the SS form with N = 64 is shared-memory-bandwidth bound on B200: dbg/mma_rate.cu).
+//    memory (the SS form with N = 64 is shared-memory-bandwidth bound on B200: tools/microbench/mma_rate.cu).
 //    S and P are double-buffered in TMEM so QK(j+1) overlaps the softmax of j. Rows whose block did
 //    not admit j write P = 0 (their MMA work is the union waste).
 //  * Softmax: 128 threads, thread == TMEM lane == query row; online softmax in fp32 (log2 domain),

@@ -243,7 +243,7 @@ __device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64
       : "memory");
 }
 // D[tmem] (+)= A[tmem] * B[smem]^T: A is M lanes x K/2 columns of packed bf16 pairs (element 2c in the
-// low half of column c); one K=16 step spans 8 columns (validated on B200: scratch/ts_test.cu)
+// low half of column c); one K=16 step spans 8 columns (validated on B200: tools/microbench/ts_test.cu)
 __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
