@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="problem", choices=["problem", "heads"],
+                    help="N>1: problem = one independent problem per rank (weak); heads = split the heads")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     for key in ("r", "f", "tau", "kind"):
@@ -215,9 +217,19 @@ def main():
 
     g = bsa.Geometry(*cfg["grid"], *cfg["block"])
     B, Hh, d = cfg["B"], cfg["Hh"], cfg["d"]
-    seed = args.seed + 1000 * rank  # weak scaling: each rank owns an independent problem (batch element)
+    from paper_2509_01085_b200.shard import head_range, problem_seed, reduce_step_stats
+    if args.shard == "heads":
+        # strong scaling: the heads of ONE problem are split over the ranks (no collective on the path)
+        seed = args.seed
+        h0, h1 = head_range(Hh, world, rank)
+    else:
+        # weak scaling: each rank owns an independent problem (its own batch element / seed)
+        seed, h0, h1 = problem_seed(args.seed, rank), 0, Hh
     Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, B, Hh, cfg["grid"], d, device=dev)
     dO = bsa_gen.grad_output(seed, (B, Hh, g.L, d)).to(dev)
+    if (h0, h1) != (0, Hh):
+        Q, K, V, dO = (x[:, h0:h1].contiguous() for x in (Q, K, V, dO))
+    Hh = h1 - h0
     layer = BSAAttention(g, cfg["r"], cfg["f"], cfg["tau"], B, Hh, d, device=dev, cache_partition=False)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -257,13 +269,8 @@ def main():
     L.bsa_timing_read(kms, kcnt, nk)
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
-    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    f_local = torch.tensor([fl["total"] * args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        dist.all_reduce(f_local, op=dist.ReduceOp.SUM)
-    t_max = float(t_local.item())
-    value = float(f_local.item()) / (t_max * 1e-3) / 1e12
+    t_max, f_sum = reduce_step_stats(total_ms, fl["total"] * args.steps, device=dev)
+    value = f_sum / (t_max * 1e-3) / 1e12
     ms_per_step = t_max / args.steps
     kernel_ms = {KERNEL_NAMES[i]: kms[i] / max(1, args.steps) for i in range(nk) if kcnt[i]}
     phases = {
@@ -346,10 +353,8 @@ def main():
     e_end.record(main)
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end) / n_e2e
-    e_local = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_local, op=dist.ReduceOp.MAX)
-    e2e_val = fl["total"] * world / (float(e_local.item()) * 1e-3) / 1e12 if args.e2e_steps else None
+    e2e_max, e2e_flops = reduce_step_stats(e2e_ms, fl["total"], device=dev)
+    e2e_val = e2e_flops / (e2e_max * 1e-3) / 1e12 if args.e2e_steps else None
     tensor_bytes = B * Hh * g.L * d * 2
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
@@ -367,13 +372,16 @@ def main():
         line = {
             "metric": METRIC,
             "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.shard == "heads" else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded G_video latents, bsa_gen)",
             "config": {"workload": args.config, "grid": list(cfg["grid"]), "block": list(cfg["block"]), "B": B,
                        "heads": Hh, "d": d, "r": cfg["r"], "k": layer.k, "k_frac": cfg["f"], "tau": cfg["tau"],
                        "generator": cfg["kind"], "tokens": g.L, "N_blocks": N,
                        "l2": "inputs > L2 (4 x %.0f MB) and 256 MiB L2 flush between timed steps" % (tensor_bytes / 1e6),
-                       "parallelism": f"bh-shard x{world} (independent problems, no collective)"},
+                       "parallelism": (f"head-shard x{world} (heads of one problem split over ranks, no collective)"
+                                       if args.shard == "heads" else
+                                       f"bh-shard x{world} (independent problems, no collective)")},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "roofline": roofline,
@@ -383,7 +391,7 @@ def main():
             "executed": {"pairs": fl["pairs"], "density": fl["density"], "flops_per_step": fl["total"],
                          "dense_equiv_tflops": fl["dense_total"] * world / (t_max * 1e-3 / args.steps) / 1e12},
             "own_dense": dense,
-            "e2e": {"value": e2e_val, "unit": "TFLOPS", "ms_per_step": float(e_local.item()),
+            "e2e": {"value": e2e_val, "unit": "TFLOPS", "ms_per_step": e2e_max,
                     "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": int(h_lse.numel() * 4),
                     "note": "pinned H2D of Q,K,V,dO each step on a copy stream (double-buffered, overlaps the "
                             "previous step's kernels); D2H of the step's LSE; through BSAAttention.forward/backward"},
