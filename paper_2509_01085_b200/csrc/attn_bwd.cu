@@ -14,9 +14,10 @@
 //
 // Warp roles of the main kernel (384 threads): w0-3 gradient softmax (thread == query
 // row == TMEM lane), w4-7 dQ drain (TMEM -> smem slices -> cp.reduce.async.bulk.tensor into the packed
-// fp32 dQacc), w8 TMEM allocator, w10 bulk-copy producer (per query block: its QdO image and its LSE/D
-// row statistics), w11 MMA issuer. The control roles sit on the highest warp ids (the warp arbiter
-// favours them) and suspend on mbarriers rather than spin.
+// fp32 dQacc), w8 TMEM allocator, w9 gradient-MMA issuer (dV, dK, dQ), w10 bulk-copy producer (per query
+// block: its QdO image and its LSE/D row statistics), w11 S/dP-MMA issuer. The control roles sit on the
+// highest warp ids (the warp arbiter favours them) and suspend on mbarriers rather than spin; two MMA
+// issuers with plain blocking waits let S/dP(c+1) run ahead of the gradient MMAs of chunk c by itself.
 #include <cmath>
 #include "kernels.h"
 #include "ptx.cuh"
@@ -255,8 +256,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   // Warp roles (the warp arbiter favours higher ids, so the single-thread producer and MMA roles get the
   // highest ones and are not starved by the math warps sharing their sub-partition):
   // w0-3 gradient softmax (TMEM quadrant = warp), w4-7 dQ drain (quadrant = warp - 4), w8 TMEM allocator,
-  // w10 producer, w11 MMA issuer.
-  constexpr int W_ALLOC = 8, W_PROD = 10, W_MMA = 11;
+  // w9 gradient-MMA issuer, w10 producer, w11 S/dP-MMA issuer.
+  constexpr int W_ALLOC = 8, W_B = 9, W_PROD = 10, W_SD = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
   // zero both stages (rows of unused slots must be finite: they meet P = dS = 0 in the MMAs)
   for (int o = tid * 16; o < 2 * SM::STAGE_BYTES; o += BWD_THREADS * 16)
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         __syncwarp();
       }
     }
-  } else if (warp == W_MMA) {
+  } else if (warp == W_SD || warp == W_B) {
     // ============================ MMA issuer: whole warp walks the schedule (uniform registers), one
     // elected lane issues. Descriptors are precomputed bases advanced by (byte offset >> 4).
     if (nchunks > 0) {
@@ -342,80 +343,71 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
       const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
       mbar_wait(&bar_kv, 0);
-      // S/dP(v) = Q^s K^T, dO^s V^T of chunk v (single TMEM buffer, free once the softmax warps have
-      // loaded S/dP(v-1) into registers)
-      auto issue_sd = [&](int v) {
-        const int sv = v & 1;
-        const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
-        mbar_wait(&bar_c_full[sv], (v >> 1) & 1);
-        BWD_TRACE(11, v);
-        if (v >= 1) mbar_wait(&bar_sd_free, (v - 1) & 1);
-        tc_fence_after();
-        if (leader) {
+      if (warp == W_SD) {
+        // S/dP(v) = Q^s K^T, dO^s V^T of chunk v, issued as soon as its stage landed and the softmax
+        // warps hold S/dP(v-1) in registers (single TMEM buffer)
+        for (int v = 0; v < nchunks; ++v) {
+          const int sv = v & 1;
+          const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
+          mbar_wait(&bar_c_full[sv], (v >> 1) & 1);
+          BWD_TRACE(11, v);
+          if (v >= 1) mbar_wait(&bar_sd_free, (v - 1) & 1);
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const int cb = kk >> 2, ko = (kk & 3) * 32;
-            umma_ss(tS, dQa + sov + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
-            umma_ss(tdP, dDa + sov + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
-          }
-          umma_commit(&bar_sd_full);
-        }
-        __syncwarp();
-        BWD_TRACE(1, v);
-      };
-      auto sd_ready = [&](int v) {  // non-blocking: operands of S/dP(v) landed and its TMEM buffer is free
-        bool ok = mbar_try_wait(&bar_c_full[v & 1], (v >> 1) & 1) && mbar_try_wait(&bar_sd_free, (v - 1) & 1);
-        return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
-      };
-      // Software pipeline: S/dP of chunk c+1 goes on the tensor pipe ahead of the gradient MMAs of chunk c
-      // when its operands are already there (the softmax warps then never wait for it); otherwise the
-      // gradient MMAs go first, so the stage they free starts reloading without waiting on a load.
-      issue_sd(0);
-      int next_sd = 1;
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c & 1, qbuf = c & 1;
-        const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
-        // wait for P/dS(c), issuing S/dP(c+1) meanwhile as soon as it can go
-        while (true) {
-          if (next_sd == c + 1 && next_sd < nchunks && sd_ready(next_sd)) issue_sd(next_sd++);
-          // suspend (bounded) instead of spinning: the MMA warp shares its sub-partition with a softmax warp
-          if (__shfl_sync(0xffffffffu, mbar_wait_for(&bar_ps_full, c & 1, 100) ? 1 : 0, 0)) break;
-        }
-        if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
-        tc_fence_after();
-        BWD_TRACE(2, c);
-        if (leader) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
-            const uint32_t ko = (kk * 2 * SM::PG) >> 4;
-            uint64_t aq, ad;
-            if (D == 128) {
-              aq = dQt + so + ko;
-              ad = dDt + so + ko;
-            } else {  // d = 64: the missing second d-chunk reads the zero block
-              const uint32_t qk = smem_u32(stage_q(s)) + kk * 2 * SM::PG, dk = smem_u32(stage_do(s)) + kk * 2 * SM::PG;
-              aq = umma_desc_sw128(qk, zero - qk, SM::PG);
-              ad = umma_desc_sw128(dk, zero - dk, SM::PG);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const int cb = kk >> 2, ko = (kk & 3) * 32;
+              umma_ss(tS, dQa + sov + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+              umma_ss(tdP, dDa + sov + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
             }
-            umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
-            umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&bar_sd_full);
           }
-          umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
-#pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk)
-            umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
-          umma_commit(&bar_dq_full[qbuf]);
-          umma_commit(&bar_ps_free);
+          __syncwarp();
+          BWD_TRACE(1, v);
         }
+      } else {
+        // gradient MMAs of chunk c once P/dS(c) is in smem and the drain emptied dQ buffer c & 1. S/dP(c)
+        // (the other issuer) completed before P/dS(c) could exist, so the c_empty commit below covers
+        // every read of the stage.
+        for (int c = 0; c < nchunks; ++c) {
+          const int s = c & 1, qbuf = c & 1;
+          const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
+          mbar_wait(&bar_ps_full, c & 1);
+          if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
+          tc_fence_after();
+          BWD_TRACE(2, c);
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
+              const uint32_t ko = (kk * 2 * SM::PG) >> 4;
+              uint64_t aq, ad;
+              if (D == 128) {
+                aq = dQt + so + ko;
+                ad = dDt + so + ko;
+              } else {  // d = 64: the missing second d-chunk reads the zero block
+                const uint32_t qk = smem_u32(stage_q(s)) + kk * 2 * SM::PG, dk = smem_u32(stage_do(s)) + kk * 2 * SM::PG;
+                aq = umma_desc_sw128(qk, zero - qk, SM::PG);
+                ad = umma_desc_sw128(dk, zero - dk, SM::PG);
+              }
+              umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+              umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+            }
+            umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
+#pragma unroll
+            for (int kk = 0; kk < BT / 16; ++kk)
+              umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
+            umma_commit(&bar_dq_full[qbuf]);
+            umma_commit(&bar_ps_free);
+          }
+          __syncwarp();
+          BWD_TRACE(3, c);
+        }
+        if (leader) umma_commit(&bar_acc);  // after the last gradient MMA: every MMA of the CTA is done
         __syncwarp();
-        BWD_TRACE(3, c);
-        if (next_sd == c + 1 && next_sd < nchunks) issue_sd(next_sd++);
       }
-      if (leader) umma_commit(&bar_acc);
-      __syncwarp();
     }
 #ifdef BSA_TRACE
-  } else if (warp == 9) {
+  } else if (warp == W_ALLOC) {
     // debug observer (trace builds only): when each chunk's loads land
     if (lane == 0)
       for (int c = 0; c < nchunks; ++c) {

@@ -16,8 +16,8 @@
 //    not admit j write P = 0 (their MMA work is the union waste).
 //  * Softmax: 128 threads, thread == TMEM lane == query row; online softmax in fp32 (log2 domain),
 //    O rescaled in TMEM only when the running max grows by more than 2^8 (exact: same final ratio).
-//  * Warp roles: w0-3 softmax/epilogue, w5 TMEM allocator, w6 bulk-copy producer, w7 MMA issuer
-//    (control roles on the highest warp ids: the warp arbiter favours them).
+//  * Warp roles: w0-7 two softmax/epilogue groups, w8 TMEM allocator, w9 bulk-copy producer, w10 PV
+//    issuer, w11 QK issuer (control roles on the highest warp ids: the warp arbiter favours them).
 #include <cmath>
 #include "kernels.h"
 #include "ptx.cuh"
@@ -62,7 +62,7 @@ struct FwdParams {
   float* lse;
 };
 
-constexpr int FWD_THREADS = 256;
+constexpr int FWD_THREADS = 384;
 constexpr int FWD_STAGES = 6;
 constexpr int MAX_N = 4096;
 constexpr int MAX_G = 16;
@@ -76,8 +76,9 @@ struct FwdSmem {
   static constexpr int OFF_ULIST = OFF_BITS + BITS_BYTES + 32 * 4;  // + union words
   static constexpr int ULIST_BYTES = MAX_N * 2;
   static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
-  // TMEM columns: O [0, D), S double buffer, Q^s (packed bf16 pairs), P double buffer (packed)
-  static constexpr int T_O = 0, T_S = D, T_Q = D + 2 * BT, T_P = T_Q + D / 2;
+  // TMEM columns: O of the even / odd steps [0, 2D), S double buffer, Q^s (packed bf16 pairs), P double
+  // buffer (packed). Buffer b = step parity = softmax group.
+  static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 2 * BT, T_P = T_Q + D / 2;
   static constexpr int TMEM_COLS = (T_P + BT) <= 256 ? 256 : 512;
 };
 
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
 
   __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
-      bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o, bar_o_final;
+      bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o_final;
+  __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
@@ -128,11 +130,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       mbar_init(&bar_p_full[b], 128);
       mbar_init(&bar_p_free[b], 1);
     }
-    mbar_init(&bar_o, 1);
     mbar_init(&bar_o_final, 1);
     fence_mbar_init();
   }
-  constexpr int W_ALLOC = 5, W_PROD = 6, W_MMA = 7;
+  constexpr int W_ALLOC = 8, W_PROD = 9, W_PV = 10, W_QK = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
   if (tid < G) {
     int qb = tile * G + tid;
@@ -225,9 +226,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
                   2 * KV_BYTES, &bar_kv_full[s]);
       }
     }
-  } else if (warp == W_MMA) {
-    // ============================ MMA issuer: the whole warp walks the schedule (so descriptors and
-    // counters live in uniform registers) and one elected lane issues tcgen05.mma / commit.
+  } else if (warp == W_QK || warp == W_PV) {
+    // ============================ MMA issuers. One tensor pipe, two issuing warps with plain blocking
+    // (suspending) waits: W_QK issues S(v) = Q^s K_v^T as soon as its K tile landed and its S buffer is
+    // free (v & 1 = softmax group), W_PV issues O_b += P(u) V_u as soon as P(u) is written. QK therefore
+    // runs ahead of PV by itself, and neither queue waits behind the other's dependencies. (A single
+    // issuer polling both queues needs a short suspend hint, which wakes ~0.3 us late on B200.) Each
+    // warp walks its schedule whole (uniform registers); one elected lane issues.
     const bool leader = elect_one();
     constexpr uint32_t idesc_qk = umma_idesc_bf16(128, BT, 0, 0);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, D, 0, 1);
@@ -235,63 +240,66 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     // base descriptors; an operand at byte offset o from the base is base + (o >> 4)
     const uint64_t dK0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t dV0 = umma_desc_sw128(smem_u32(sK + KV_BYTES), BT * 128, 1024);
-    mbar_wait(&bar_qt, 0);  // Q^s is in TMEM
-    auto issue_qk = [&](int v) {  // S(v) = Q^s K_v^T into S buffer v & 1
-      const int s = v % FWD_STAGES, sb = v & 1;
-      mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
-      if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
-      tc_fence_after();
-      const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
-      if (leader) {
+    if (warp == W_QK) {
+      mbar_wait(&bar_qt, 0);  // Q^s is in TMEM
+      for (int v = 0; v < U; ++v) {
+        const int s = v % FWD_STAGES, sb = v & 1;
+        mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
+        if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const int cb = kk >> 2, ko = (kk & 3) * 32;
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const int cb = kk >> 2, ko = (kk & 3) * 32;
 #ifndef BSA_ABLATE_FWD_MMA
-          umma_ts(tS + sb * BT, tQ + kk * 8, kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
+            umma_ts(tS + sb * BT, tQ + kk * 8, kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
 #endif
+          }
+          umma_commit(&bar_s_full[sb]);
         }
-        umma_commit(&bar_s_full[sb]);
+        __syncwarp();
+        FWD_TRACE(1, v);
       }
-      __syncwarp();
-      FWD_TRACE(1, v);
-    };
-    // Order on the tensor pipe: QK(u+1) ahead of PV(u), so S(u+1) is ready when the softmax warps
-    // finish P(u). Every wait here suspends (no spinning: the MMA warp shares its sub-partition with a
-    // softmax warp). The K|V ring runs FWD_STAGES steps ahead, so QK(u+1)'s operands are normally there.
-    issue_qk(0);
-    for (int u = 0; u < U; ++u) {
-      const int pb = u & 1, s = u % FWD_STAGES;
-      if (u + 1 < U) issue_qk(u + 1);
-      mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
-      FWD_TRACE(2, u);
-      tc_fence_after();
-      const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
-      if (leader) {
+    } else {
+      for (int u = 0; u < U; ++u) {
+        const int pb = u & 1, s = u % FWD_STAGES;
+        mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
+        FWD_TRACE(2, u);
+        tc_fence_after();
+        const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk) {
+          for (int kk = 0; kk < BT / 16; ++kk) {
 #ifndef BSA_ABLATE_FWD_MMA
-          umma_ts(tO, tP + pb * (BT / 2) + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+            umma_ts(tO + pb * D, tP + pb * (BT / 2) + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv,
+                    (u > 1 || kk > 0) ? 1u : 0u);
 #endif
+          }
+          // QK(u) (the other issuer) completed before P(u) could exist, so this commit covers every
+          // read of the stage
+          umma_commit(&bar_kv_empty[s]);
+          umma_commit(&bar_p_free[pb]);
         }
-        umma_commit(&bar_kv_empty[s]);
-        umma_commit(&bar_p_free[pb]);
-        umma_commit(&bar_o);
+        __syncwarp();
+        FWD_TRACE(3, u);
       }
+      if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
       __syncwarp();
-      FWD_TRACE(3, u);
     }
-    if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
-    __syncwarp();
-  } else if (warp < 4) {
-    // ============================ softmax + epilogue (thread == query row == TMEM lane)
-    const int q4 = warp;
+  } else if (warp < 8) {
+    // ============================ softmax + epilogue: two groups of four warps. Group b = warp / 4 runs
+    // the steps u = b, b+2, ... with its own running max / sum and its own O accumulator (TMEM columns
+    // [b D, (b+1) D)), so the two groups on one sub-partition (warps w and w+4 share TMEM lane quadrant
+    // w % 4) fill each other's latency; the two partial results are merged in the epilogue (split-K).
+    const int group = warp >> 2, q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const int gi = row / SR, lr = row % SR;
     const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
     const uint32_t* mybits = bits + (gi < G ? gi : 0) * NW;
     const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0;
-    {
+    if (group == 0) {
       // Q^s row -> TMEM (A operand of the S MMAs): bf16 pairs are already packed in memory order
       const uint4* src = reinterpret_cast<const uint4*>(p.Qs + prow_idx * D);
 #pragma unroll
@@ -312,22 +320,23 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       mbar_arrive(&bar_qt);
     }
     const float sl2 = p.scale_log2;
+    const uint32_t tS = trow + SM::T_S + group * BT, tP = trow + SM::T_P + group * (BT / 2);
+    const uint32_t tO = trow + SM::T_O + group * D;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int u = 0; u < U; ++u) {
-      const int sb = u & 1, pb = u & 1;
+    for (int u = group; u < U; u += 2) {
+      const int ph = (u >> 1) & 1;  // phase of this group's buffers
       const int ent = entry_at(u), j = ent & 0xFFF, cls = ent >> 12;
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
-      mbar_wait(&bar_s_full[sb], (u >> 1) & 1);
-      if (row == 0) FWD_TRACE(4, u);
+      mbar_wait(&bar_s_full[group], ph);
+      if (row == 0) FWD_TRACE(4 + 8 * group, u);
       tc_fence_after();
       float sv[BT];
 #pragma unroll
-      for (int c = 0; c < BT; c += 16) tmem_ld16(trow + SM::T_S + sb * BT + c, sv + c);
+      for (int c = 0; c < BT; c += 16) tmem_ld16(tS + c, sv + c);
       tmem_wait_ld();
-      if (row == 0) FWD_TRACE(6, u);
-      if (lane == 0) FWD_TRACE(12 + q4, u);
+      if (row == 0) FWD_TRACE(6 + 8 * group, u);
       tc_fence_before();
-      mbar_arrive(&bar_s_free[sb]);
+      mbar_arrive(&bar_s_free[group]);
       float alpha = 1.f;
       bool need_rescale = false;
       if (admit) {
@@ -362,60 +371,69 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll
         for (int c = 0; c < BT; ++c) sv[c] = 0.f;
       }
-      // P buffer pb is free once PV(u-2) completed. Waiting here first also bounds bar_o to at most
-      // one phase behind PV(u-1), which makes the parity wait below unambiguous.
-      if (lane == 0) FWD_TRACE(16 + q4, u);
-      if (u >= 2) mbar_wait(&bar_p_free[pb], ((u - 2) >> 1) & 1);
-      if (row == 0) FWD_TRACE(7, u);
-      if (lane == 0) FWD_TRACE(20 + q4, u);
-      // O rescale in TMEM (needs PV(u-1) complete); warp-collective access
+      // P buffer and O accumulator of this group are free once PV(u-2) (its previous step) completed
+      if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
+      if (row == 0) FWD_TRACE(7 + 8 * group, u);
+      // O rescale in TMEM; warp-collective access
       if (__any_sync(0xffffffffu, need_rescale)) {
-        mbar_wait(&bar_o, (u - 1) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
           float ov[16];
-          tmem_ld16(trow + SM::T_O + c, ov);
+          tmem_ld16(tO + c, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 16; ++e) ov[e] *= alpha;
-          tmem_st16(trow + SM::T_O + c, ov);
+          tmem_st16(tO + c, ov);
         }
       }
-      if (lane == 0) FWD_TRACE(24 + q4, u);
       // P row -> TMEM (bf16 pairs, the A operand of PV)
 #pragma unroll
       for (int c0 = 0; c0 < BT / 2; c0 += 16) {
         float w[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(pack_bf16(sv[2 * (c0 + e)], sv[2 * (c0 + e) + 1]));
-        tmem_st16(trow + SM::T_P + pb * (BT / 2) + c0, w);
+        tmem_st16(tP + c0, w);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bar_p_full[pb]);
-      if (row == 0) FWD_TRACE(5, u);
-      if (lane == 0) FWD_TRACE(8 + q4, u);
+      mbar_arrive(&bar_p_full[group]);
+      if (row == 0) FWD_TRACE(5 + 8 * group, u);
     }
-    // epilogue: O^s = O / l, scattered to the kept token's raster row; LSE in natural log
+    // epilogue: merge the two groups' (m, l, O), O^s = O / l scattered to the kept token's raster row,
+    // LSE in natural log. Group b writes output columns [b D/2, (b+1) D/2).
+    s_ml[group][0][row] = m_run;
+    s_ml[group][1][row] = l_run;
     mbar_wait(&bar_o_final, 0);
     tc_fence_after();
-    const float inv = valid ? 1.f / l_run : 0.f;
+    named_bar_sync(1, 256);
+    const float m0 = s_ml[0][0][row], l0 = s_ml[0][1][row], m1 = s_ml[1][0][row], l1 = s_ml[1][1][row];
+    const bool has1 = U > 1;  // the odd group ran at least one step (its O columns were written)
+    const float m = has1 ? fmaxf(m0, m1) : m0;
+    const float a0 = valid ? ex2(m0 - m) : 0.f, a1 = (valid && has1) ? ex2(m1 - m) : 0.f;
+    const float l = l0 * a0 + l1 * a1;
+    const float inv = valid ? 1.f / l : 0.f;
     bf16* orow = nullptr;
     if (valid) {
       int tok = p.kept_tok[prow_idx];
       orow = p.O + (static_cast<size_t>(bh) * g.L + tok) * D;
-      p.lse[prow_idx] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+      if (group == 0) p.lse[prow_idx] = (m + log2f(l)) * 0.6931471805599453f;
     }
+    const float s0 = a0 * inv, s1 = a1 * inv;
 #pragma unroll 1
-    for (int c = 0; c < D; c += 16) {
-      float ov[16];
-      tmem_ld16(trow + SM::T_O + c, ov);
+    for (int c = group * (D / 2); c < (group + 1) * (D / 2); c += 16) {
+      float o0[16], o1[16];
+      tmem_ld16(trow + SM::T_O + c, o0);
+      if (has1) tmem_ld16(trow + SM::T_O + D + c, o1);
       tmem_wait_ld();
       if (valid) {
         uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) w[e] = pack_bf16(ov[2 * e] * inv, ov[2 * e + 1] * inv);
+        for (int e = 0; e < 8; ++e) {
+          const float x0 = has1 ? o0[2 * e] * s0 + o1[2 * e] * s1 : o0[2 * e] * s0;
+          const float x1 = has1 ? o0[2 * e + 1] * s0 + o1[2 * e + 1] * s1 : o0[2 * e + 1] * s0;
+          w[e] = pack_bf16(x0, x1);
+        }
         *reinterpret_cast<uint4*>(orow + c) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
       }

@@ -89,6 +89,10 @@ cudaError_t launch_partition(const Geo& g, double r, int* block_off, int* block_
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+#ifdef BSA_COUNT_RESCORE
+__device__ unsigned long long g_rescore_count = 0;
+#endif
+
 template <int D>
 __device__ __forceinline__ double dot_rows(const bf16* a, const bf16* b) {
   double s = 0.0;
@@ -128,8 +132,63 @@ __device__ __forceinline__ float dot_rows_f32(const bf16* a, const bf16* b) {
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
+// fp32 Gram of the block's rows, G[i][j] = sum_c q_i[c] q_j[c], on the tensor cores (mma.sync
+// m16n8k16 bf16 -> fp32: the bf16 products are exact, the fp32 accumulation error is bounded like an
+// FFMA chain's). Rows/columns are padded to BTp (multiple of 16, zero rows); warp w owns the 16-row
+// tiles w, w+4, ...; the result goes to smem [BTp][GS].
+template <int D>
+__device__ __forceinline__ void block_gram(const bf16* sq, int DS, int BTp, float* gram, int GS) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = BTp / 8;
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sq));
+  // ldmatrix x4 lane addressing: A = [rows +0..7 | +8..15] x [k 0..7 | 8..15]; B = 2 n-tiles x 2 k-halves
+  const int am = lane >> 3, ar = lane & 7;
+  const uint32_t b_off = ((((am >> 1) * 8) + ar) * DS + (am & 1) * 8) * 2;
+  for (int r0 = warp * 16; r0 < BTp; r0 += 64) {
+    float acc[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+    const uint32_t a_addr = base + ((r0 + (am & 1) * 8 + ar) * DS + (am >> 1) * 8) * 2;
+#pragma unroll 1
+    for (int kk = 0; kk < D; kk += 16) {
+      uint32_t a[4];
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                   : "r"(a_addr + kk * 2));
+#pragma unroll
+      for (int np = 0; np < 8; ++np) {
+        if (2 * np >= ntiles) break;
+        uint32_t b[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                     : "r"(base + (np * 16 * DS + kk) * 2 + b_off));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float* c = acc[2 * np + h];
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%0,%1,%2,%3};"
+              : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+              : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[2 * h]), "r"(b[2 * h + 1]));
+        }
+      }
+    }
+    const int row = r0 + (lane >> 2), col = (lane & 3) * 2;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      if (nt >= ntiles) break;
+      gram[row * GS + nt * 8 + col] = acc[nt][0];
+      gram[row * GS + nt * 8 + col + 1] = acc[nt][1];
+      gram[(row + 8) * GS + nt * 8 + col] = acc[nt][2];
+      gram[(row + 8) * GS + nt * 8 + col + 1] = acc[nt][3];
+    }
+  }
+}
+
 // One CTA (128 threads) per (bh, block). Shared layout: rows padded to D+8 bf16 so that
-// lane-strided 16-byte row reads are bank-conflict free.
+// lane-strided 16-byte row reads and ldmatrix are bank-conflict free.
 template <int D>
 __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq, const bf16* __restrict__ Q,
                                                         const int* __restrict__ kept_off, int* __restrict__ kept_tok,
@@ -139,8 +198,8 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
   extern __shared__ __align__(16) uint8_t smem[];
   const int b = blockIdx.x, bh = blockIdx.y;
   const int BTn = g.BT;
-  bf16* sq = reinterpret_cast<bf16*>(smem);                          // [BT][DS]
-  double* nrm = reinterpret_cast<double*>(sq + BTn * DS);            // [BT]
+  bf16* sq = reinterpret_cast<bf16*>(smem);                          // [BTp][DS] (rows >= n zero)
+  double* nrm = reinterpret_cast<double*>(sq + ((BTn + 15) & ~15) * DS);  // [BT]
   double* cs = nrm + BTn;                                            // [BT]
   int* tok = reinterpret_cast<int*>(cs + BTn);                       // [BT]
   int* unit = tok + BTn;                                             // [BT]
@@ -148,6 +207,9 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
   int* keep = cen + BTn;                                             // [BT] 1 if kept
   int* mcnt = keep + BTn;                                            // [BT] keep count of my unit
   int* plist = mcnt + BTn;                                           // [BT] pruned local indices
+  const int BTp = (BTn + 15) & ~15;                                  // rows padded for the MMA tiles
+  const int GS = BTp + 1;                                            // Gram row stride (floats)
+  float* gram = reinterpret_cast<float*>(plist + BTn);              // [BTp][GS] fp32 Gram of the rows
   __shared__ int s_np;
 
   const Box x = block_box(g, b);
@@ -157,11 +219,13 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
   __syncthreads();
   // rows -> smem (16-byte vectors)
   constexpr int VPR = D / 8;
-  for (int v = threadIdx.x; v < n * VPR; v += blockDim.x) {
+  for (int v = threadIdx.x; v < BTp * VPR; v += blockDim.x) {
     int i = v / VPR, c = (v % VPR) * 8;
-    *reinterpret_cast<uint4*>(sq + i * DS + c) = *reinterpret_cast<const uint4*>(Q + (head + tok[i]) * D + c);
+    *reinterpret_cast<uint4*>(sq + i * DS + c) =
+        i < n ? *reinterpret_cast<const uint4*>(Q + (head + tok[i]) * D + c) : make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
+  block_gram<D>(sq, DS, BTp, gram, GS);  // read by the donor search below (after later barriers)
   // a2: pooled mean, summed in ascending token order
   if (q_pooled) {
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
@@ -224,13 +288,14 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
   // donors (C9): warp per pruned token, lanes over kept candidates of the same unit;
   // argmax cos(q_p, q_j), ties -> lowest token
   //
-  // Certified fp32 screening: bf16 x bf16 products are exact in fp32, so an fp32 FFMA dot over D
-  // channels is within gamma_D * sum|a_c b_c| <= gamma_D |a||b| of the exact dot (gamma_128 = 7.6e-6);
-  // with the fp64 norms the fp32 cosine is within EPS = 2e-5 of the fp64 one. A kept j whose fp32
-  // cosine is more than 2 EPS below the fp32 best can therefore not be the fp64 argmax; if only one
-  // candidate survives it IS the fp64 argmax, otherwise the survivors are re-scored with the exact
-  // fp64 formula. The decision is identical to a pure fp64 evaluation.
-  constexpr float EPS = 2e-5f;
+  // Certified fp32 screening: bf16 x bf16 products are exact in fp32, so an fp32 dot accumulated over D
+  // channels (tensor-core Gram above) is within ~D 2^-23 sum|a_c b_c| <= 1.6e-5 |a||b| of the exact
+  // dot even with truncating accumulation; with the fp64 norms the fp32 cosine is within EPS = 6e-5 of
+  // the fp64 one (4x margin). A kept j whose fp32 cosine is more than 2 EPS below the fp32 best can
+  // therefore not be the fp64 argmax; if only one candidate survives it IS the fp64 argmax, otherwise
+  // the survivors are re-scored with the exact fp64 formula. The decision is identical to a pure fp64
+  // evaluation.
+  constexpr float EPS = 6e-5f;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int pi = warp; pi < s_np; pi += 4) {
     const int p = plist[pi];
@@ -242,7 +307,7 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
       cv[k] = -FLT_MAX;
       if (j < n && keep[j] && unit[j] == unit[p]) {
         if (nrm[p] == 0.0 || nrm[j] == 0.0) cv[k] = 0.f;
-        else cv[k] = dot_rows_f32<D>(sq + p * DS, sq + j * DS) / static_cast<float>(nrm[p] * nrm[j]);
+        else cv[k] = gram[p * GS + j] / static_cast<float>(nrm[p] * nrm[j]);
       }
       best32 = fmaxf(best32, cv[k]);
     }
@@ -257,7 +322,14 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
       ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
       arg = min(arg, __shfl_xor_sync(0xffffffffu, arg, o));
     }
+#ifdef BSA_COUNT_RESCORE
+    if (lane == 0 && ncand > 1) atomicAdd(&g_rescore_count, 1ull);
+#endif
+#ifndef BSA_ABLATE_RESCORE
     if (ncand > 1) {  // near tie in fp32: decide in fp64 exactly as the plain definition does
+#else
+    if (ncand > 1000) {
+#endif
       double best = -DBL_MAX;
       arg = INT_MAX;
 #pragma unroll
@@ -279,7 +351,8 @@ __global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq,
 }
 
 static size_t select_smem(int BT, int D) {
-  return static_cast<size_t>(BT) * (D + 8) * 2 + static_cast<size_t>(BT) * 16 + static_cast<size_t>(BT) * 6 * 4;
+  const size_t BTp = (BT + 15) & ~15;
+  return BTp * (D + 8) * 2 + static_cast<size_t>(BT) * 16 + static_cast<size_t>(BT) * 6 * 4 + BTp * (BTp + 1) * 4;
 }
 
 cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, const bf16* Q, const int* kept_off,
