@@ -40,8 +40,13 @@ __device__ __forceinline__ float ex2b(float x) {
 // 8 rows x 128 B with the 128-byte swizzle. Consecutive groups (also across the blocks stacked in a
 // chunk) are 2*NCB KB apart, so every UMMA operand over the chunk's 128 rows has a uniform stride.
 // Next to it, the block's row statistics lsed[(b,h,block)] = [LSE*log2(e) of its SR rows][D of its SR rows]
-// (one more bulk copy per block). One warp per padded row (b,h, block, row < SR); rows beyond the block's
-// kept count are zero with LSE = +inf, D = 0, so they contribute P = dS = 0.
+// (one more bulk copy per block). Rows beyond the block's kept count are zero with LSE = +inf, D = 0, so
+// they contribute P = dS = 0.
+//
+// One CTA per (b,h, block): the block's tokens, their donors and their dO rows are staged in shared
+// memory once (coalesced 16-byte loads), then one warp per kept row folds the dO of the pruned tokens
+// whose donor it is (the gradient of the fill), forms D = rowsum(dO^s O^s) and writes its image
+// row, row statistics and the zeroed dQ accumulator row.
 template <int D>
 __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR, const int* __restrict__ kept_off,
                                                   const int* __restrict__ kept_tok, const int* __restrict__ donor,
@@ -51,83 +56,94 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
                                                   float* __restrict__ dQacc) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
   constexpr int NCB = D / 64;
-  const size_t wid = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (wid >= static_cast<size_t>(BH) * g.N * SR) return;
-  const int lr = static_cast<int>(wid % SR);
-  const size_t bi = wid / SR;
-  const int blk = static_cast<int>(bi % g.N);
-  const size_t bh = bi / g.N;
-  const int ko = kept_off[blk], nk = kept_off[blk + 1] - ko;
-  const int ch0 = lane * PER;
-  uint8_t* gbase = qdo_img + bi * static_cast<size_t>(SR) * D * 4 + (lr >> 3) * (2 * NCB * 1024);
-  const uint32_t inrow = sw128_off(lr & 7, (ch0 & 63) >> 3) + (ch0 & 7) * 2;
-  uint8_t* qdst = gbase + (ch0 >> 6) * 1024 + inrow;
-  uint8_t* ddst = gbase + (NCB + (ch0 >> 6)) * 1024 + inrow;
-  float* ld = lsed + bi * 2 * SR + lr;
-  if (lr >= nk) {
-    if (lane == 0) {
-      ld[0] = INFINITY;
-      ld[SR] = 0.f;
-    }
-    if (PER == 4) {
-      *reinterpret_cast<uint2*>(qdst) = make_uint2(0, 0);
-      *reinterpret_cast<uint2*>(ddst) = make_uint2(0, 0);
-    } else {
-      *reinterpret_cast<uint32_t*>(qdst) = 0u;
-      *reinterpret_cast<uint32_t*>(ddst) = 0u;
-    }
-    return;
-  }
-  const size_t prow = bh * Lq + ko + lr;
-  const int tok = kept_tok[prow];
-  const size_t head = bh * g.L;
-  if (PER == 4) *reinterpret_cast<uint2*>(qdst) = *reinterpret_cast<const uint2*>(Qs + prow * D + ch0);
-  else *reinterpret_cast<uint32_t*>(qdst) = *reinterpret_cast<const uint32_t*>(Qs + prow * D + ch0);
-  float acc[PER];
-  {
-    const bf16* src = dO + (head + tok) * D + lane * PER;
-#pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] = __bfloat162float(src[e]);
-  }
-  // donees of tok live in tok's block
-  int t = tok / (g.H * g.W), h = (tok / g.W) % g.H, w = tok % g.W;
-  int b = ((t / g.ct) * g.Nh + h / g.ch) * g.Nw + w / g.cw;
-  const Box x = block_box(g, b);
+  constexpr int MAXT = 128;    // tokens per block (checked by the API)
+  __shared__ __align__(16) bf16 s_do[MAXT * D];
+  __shared__ int s_tok[MAXT], s_don[MAXT];
+  const int blk = blockIdx.x, bh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t bi = static_cast<size_t>(bh) * g.N + blk;
+  const size_t head = static_cast<size_t>(bh) * g.L;
+  const Box x = block_box(g, blk);
   const int n = box_size(x);
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    int i = i0 + lane;
-    int ti = i < n ? box_token(g, x, i) : -1;
-    bool match = i < n && ti != tok && donor[head + ti] == tok;
-    unsigned m = __ballot_sync(0xffffffffu, match);
-    while (m) {
-      int src_lane = __ffs(m) - 1;
-      m &= m - 1;
-      int tsrc = __shfl_sync(0xffffffffu, ti, src_lane);
-      const bf16* src = dO + (head + tsrc) * D + lane * PER;
-#pragma unroll
-      for (int e = 0; e < PER; ++e) acc[e] += __bfloat162float(src[e]);
+  const int ko = kept_off[blk], nk = kept_off[blk + 1] - ko;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int t = box_token(g, x, i);
+    s_tok[i] = t;
+    s_don[i] = donor[head + t];
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < n * (D / 8); v += blockDim.x) {
+    const int i = v / (D / 8), c = (v % (D / 8)) * 8;
+    *reinterpret_cast<uint4*>(s_do + i * D + c) = *reinterpret_cast<const uint4*>(dO + (head + s_tok[i]) * D + c);
+  }
+  __syncthreads();
+  const int ch0 = lane * PER;
+  for (int lr = warp; lr < SR; lr += 8) {
+    uint8_t* gbase = qdo_img + bi * static_cast<size_t>(SR) * D * 4 + (lr >> 3) * (2 * NCB * 1024);
+    const uint32_t inrow = sw128_off(lr & 7, (ch0 & 63) >> 3) + (ch0 & 7) * 2;
+    uint8_t* qdst = gbase + (ch0 >> 6) * 1024 + inrow;
+    uint8_t* ddst = gbase + (NCB + (ch0 >> 6)) * 1024 + inrow;
+    float* ld = lsed + bi * 2 * SR + lr;
+    if (lr >= nk) {
+      if (lane == 0) {
+        ld[0] = INFINITY;
+        ld[SR] = 0.f;
+      }
+      if (PER == 4) {
+        *reinterpret_cast<uint2*>(qdst) = make_uint2(0, 0);
+        *reinterpret_cast<uint2*>(ddst) = make_uint2(0, 0);
+      } else {
+        *reinterpret_cast<uint32_t*>(qdst) = 0u;
+        *reinterpret_cast<uint32_t*>(ddst) = 0u;
+      }
+      continue;
     }
-  }
-  float dsum = 0.f;
-  const bf16* orow = O + (head + tok) * D + lane * PER;
-  bf16 hv[PER];
+    const size_t prow = static_cast<size_t>(bh) * Lq + ko + lr;
+    const int tok = kept_tok[prow];
+    if (PER == 4) *reinterpret_cast<uint2*>(qdst) = *reinterpret_cast<const uint2*>(Qs + prow * D + ch0);
+    else *reinterpret_cast<uint32_t*>(qdst) = *reinterpret_cast<const uint32_t*>(Qs + prow * D + ch0);
+    // dO^s = dO[tok] + sum of dO over the block's pruned tokens whose donor is tok (ascending token order)
+    float acc[PER];
+    int self = -1;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool is_self = i < n && s_tok[i] == tok;
+      const unsigned ms = __ballot_sync(0xffffffffu, is_self);
+      if (ms) self = i0 + __ffs(ms) - 1;
+    }
 #pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    hv[e] = __float2bfloat16_rn(acc[e]);
-    dsum += __bfloat162float(hv[e]) * __bfloat162float(orow[e]);
-  }
-  if (PER == 4) *reinterpret_cast<uint2*>(ddst) = *reinterpret_cast<const uint2*>(hv);
-  else *reinterpret_cast<uint32_t*>(ddst) = *reinterpret_cast<const uint32_t*>(hv);
+    for (int e = 0; e < PER; ++e) acc[e] = __bfloat162float(s_do[self * D + ch0 + e]);
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool match = i < n && s_tok[i] != tok && s_don[i] == tok;
+      unsigned m = __ballot_sync(0xffffffffu, match);
+      while (m) {
+        const int src = i0 + __ffs(m) - 1;
+        m &= m - 1;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-  if (lane == 0) {
-    ld[0] = lse[prow] * 1.4426950408889634f;
-    ld[SR] = dsum;
-  }
-  float* dq = dQacc + prow * D + lane * PER;
+        for (int e = 0; e < PER; ++e) acc[e] += __bfloat162float(s_do[src * D + ch0 + e]);
+      }
+    }
+    float dsum = 0.f;
+    const bf16* orow = O + (head + tok) * D + ch0;
+    bf16 hv[PER];
 #pragma unroll
-  for (int e = 0; e < PER; ++e) dq[e] = 0.f;
+    for (int e = 0; e < PER; ++e) {
+      hv[e] = __float2bfloat16_rn(acc[e]);
+      dsum += __bfloat162float(hv[e]) * __bfloat162float(orow[e]);
+    }
+    if (PER == 4) *reinterpret_cast<uint2*>(ddst) = *reinterpret_cast<const uint2*>(hv);
+    else *reinterpret_cast<uint32_t*>(ddst) = *reinterpret_cast<const uint32_t*>(hv);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    if (lane == 0) {
+      ld[0] = lse[prow] * 1.4426950408889634f;
+      ld[SR] = dsum;
+    }
+    float* dq = dQacc + prow * D + ch0;
+    if (PER == 4) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else *reinterpret_cast<float2*>(dq) = make_float2(0.f, 0.f);
+  }
 }
 
 // ------------------------------------------------------------------------------------ main
@@ -663,8 +679,7 @@ static cudaError_t run_bwd(const BwdParams& p, int BH, cudaStream_t st) {
 }
 
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
-  const size_t rows = static_cast<size_t>(a.BH) * a.g.N * a.SR;  // padded rows of the QdO images
-  const unsigned prep_blocks = static_cast<unsigned>((rows * 32 + 255) / 256);
+  const dim3 prep_blocks(a.g.N, a.BH);  // one CTA per (b,h, query block)
   if (a.d == 128)
     k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
                                                  a.O, a.lse, a.qdo_img, a.lsed, a.dQacc);
