@@ -41,7 +41,7 @@ CONFIGS = {
     "long_147k": dict(grid=(41, 45, 80), block=(4, 4, 4), B=1, Hh=40, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
 }
 KERNEL_NAMES = ["partition", "select_queries", "pool", "scores", "admit", "k2q", "gather", "attn_fwd", "fill",
-                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image"]
+                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image", "sp_relayout"]
 SELECTION_IDS = range(0, 7)
 
 
@@ -188,8 +188,9 @@ def main():
     ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", default="problem", choices=["problem", "heads"],
-                    help="N>1: problem = one independent problem per rank (weak); heads = split the heads")
+    ap.add_argument("--shard", default="problem", choices=["problem", "heads", "ulysses"],
+                    help="N>1: problem = one independent problem per rank (weak); heads = split the heads; "
+                         "ulysses = token-sharded inputs regathered per head group by all-to-all (strong)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     for key in ("r", "f", "tau", "kind"):
@@ -225,17 +226,35 @@ def main():
     else:
         # weak scaling: each rank owns an independent problem (its own batch element / seed)
         seed, h0, h1 = problem_seed(args.seed, rank), 0, Hh
+    if args.shard == "ulysses":
+        seed, h0, h1 = args.seed, 0, Hh
     Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, B, Hh, cfg["grid"], d, device=dev)
     dO = bsa_gen.grad_output(seed, (B, Hh, g.L, d)).to(dev)
     if (h0, h1) != (0, Hh):
         Q, K, V, dO = (x[:, h0:h1].contiguous() for x in (Q, K, V, dO))
     Hh = h1 - h0
-    layer = BSAAttention(g, cfg["r"], cfg["f"], cfg["tau"], B, Hh, d, device=dev, cache_partition=False)
+    if args.shard == "ulysses":
+        # sequence-parallel layout: this rank's contiguous token chunk of all heads, [B, L/P, Hh, d]
+        from paper_2509_01085_b200.ulysses import UlyssesBSA
+        uly = UlyssesBSA(g, cfg["r"], cfg["f"], cfg["tau"], B, Hh, d, device=dev)
+        Ls = g.L // world
+        Q, K, V, dO = (x.permute(0, 2, 1, 3)[:, rank * Ls:(rank + 1) * Ls].contiguous() for x in (Q, K, V, dO))
+        layer = uly.layer
+        layer.cache_partition = False
+
+        def fwd_bwd(q, k, v, do):
+            uly.forward(q, k, v)
+            uly.backward(do)
+    else:
+        layer = BSAAttention(g, cfg["r"], cfg["f"], cfg["tau"], B, Hh, d, device=dev, cache_partition=False)
+
+        def fwd_bwd(q, k, v, do):
+            layer.forward(q, k, v)
+            layer.backward(do)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        layer.forward(Q, K, V)
-        layer.backward(dO)
+        fwd_bwd(Q, K, V, dO)
 
     for _ in range(args.warmup):
         step()
@@ -277,6 +296,7 @@ def main():
         "selection_ms": sum(kms[i] for i in SELECTION_IDS) / args.steps,
         "fwd_ms": (kms[7] + kms[8] + kms[12]) / args.steps,
         "bwd_ms": (kms[9] + kms[10] + kms[11]) / args.steps,
+        "sp_relayout_ms": kms[13] / args.steps,
     }
 
     # ---------------------------------------------------------------- roofline (dominant kernel)
@@ -296,7 +316,7 @@ def main():
                 "frac": achieved / peaks["bf16"], "traffic": traffic, "peak_source": f"{peaks['source']} bf16 burst",
                 "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_ms}
     # selection kernels against HBM (algorithmic bytes)
-    BH, Lq, N = B * Hh, layer.Lq, layer.N
+    BH, Lq, N = B * layer.Hh, layer.Lq, layer.N
     sel_bytes = BH * (4 * g.L * d + 4 * Lq + 4 * g.L + 2 * Lq * d + 8 * N * d + 4 * N * (1 + fl["pairs"] / max(1, BH * Lq)))
     sel_ms = phases["selection_ms"]
 
@@ -346,8 +366,7 @@ def main():
             copied[s].record(cstream)
         main.wait_event(copied[s])
         Qg, Kg, Vg, dOg = bufs[s % 2]
-        layer.forward(Qg, Kg, Vg)
-        layer.backward(dOg)
+        fwd_bwd(Qg, Kg, Vg, dOg)
         consumed[s].record(main)
         h_lse.copy_(layer.lse, non_blocking=True)
     e_end.record(main)
@@ -355,7 +374,7 @@ def main():
     e2e_ms = e_start.elapsed_time(e_end) / n_e2e
     e2e_max, e2e_flops = reduce_step_stats(e2e_ms, fl["total"], device=dev)
     e2e_val = e2e_flops / (e2e_max * 1e-3) / 1e12 if args.e2e_steps else None
-    tensor_bytes = B * Hh * g.L * d * 2
+    tensor_bytes = Q.numel() * 2
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
     cpu = None
@@ -373,7 +392,7 @@ def main():
             "metric": METRIC,
             "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.shard == "heads" else "weak", "vs_baseline": None,
+            "scaling": "strong" if args.shard in ("heads", "ulysses") else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded G_video latents, bsa_gen)",
             "config": {"workload": args.config, "grid": list(cfg["grid"]), "block": list(cfg["block"]), "B": B,
                        "heads": Hh, "d": d, "r": cfg["r"], "k": layer.k, "k_frac": cfg["f"], "tau": cfg["tau"],
@@ -381,6 +400,9 @@ def main():
                        "l2": "inputs > L2 (4 x %.0f MB) and 256 MiB L2 flush between timed steps" % (tensor_bytes / 1e6),
                        "parallelism": (f"head-shard x{world} (heads of one problem split over ranks, no collective)"
                                        if args.shard == "heads" else
+                                       f"ulysses x{world} (token-sharded [B, L/P, Hh, d] inputs; NCCL all-to-all "
+                                       f"to head groups and back, inside the timed step)"
+                                       if args.shard == "ulysses" else
                                        f"bh-shard x{world} (independent problems, no collective)")},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -136,11 +136,27 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
                  const float* lse, float scale, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
                  void* stream);
 
+/* ---------------------------------------------------------------- Ulysses sequence parallelism
+ * (SURVEY.md §8(e) mode 2). A sequence-parallel model gives each of P ranks a contiguous
+ * chunk of Ls = L/P raster tokens of all Hh heads, [B][Ls][Hh][d]. Selection needs every pooled block
+ * of a head, so around BSA the caller runs one all-to-all (NCCL; equal contiguous
+ * chunks of B*Hp*Ls*d elements, Hp = Hh/P) per tensor and this call reorders rows into and out of its
+ * buffers (no arithmetic; bf16 rows of d channels, d % 8 == 0; src and dst must not overlap):
+ *   BSA_SP_SEQ_TO_SEND    src [B][Ls][Hh][d]     -> dst [P][B][Hp][Ls][d]  (chunk p: head group p)
+ *   BSA_SP_RECV_TO_HEADS  src [P][B][Hp][Ls][d]  -> dst [B][Hp][P*Ls][d]   (BSA layout, whole sequence)
+ *   BSA_SP_HEADS_TO_SEND  src [B][Hp][P*Ls][d]   -> dst [P][B][Hp][Ls][d]  (chunk s: sequence chunk s)
+ *   BSA_SP_RECV_TO_SEQ    src [P][B][Hp][Ls][d]  -> dst [B][Ls][Hh][d]     (back to the model layout)
+ * Errors: BSA_ERR_INVALID_SHAPE for non-positive sizes, d % 8 != 0 or misaligned pointers;
+ * BSA_ERR_CONFIG for Hh % P != 0 or an unknown mode. */
+enum bsa_sp_mode { BSA_SP_SEQ_TO_SEND = 0, BSA_SP_RECV_TO_HEADS = 1, BSA_SP_HEADS_TO_SEND = 2, BSA_SP_RECV_TO_SEQ = 3 };
+int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int32_t P, const void* src, void* dst,
+                    void* stream);
+
 /* ---------------------------------------------------------------- instrumentation (off the hot path)
  * Kernel ids reported by bsa_timing_read / counted by bsa_launch_count. */
 enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
-  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_COUNT
+  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT, BSA_K_COUNT
 };
 /* Total kernels this thread has launched through libbsa (always counted; cheap). */
 int64_t bsa_launch_count(void);

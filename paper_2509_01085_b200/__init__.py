@@ -17,7 +17,7 @@ import torch
 
 __all__ = [
     "BSAError", "Geometry", "lib", "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
-    "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "Selection", "select", "resolve_k",
+    "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout", "Selection", "select", "resolve_k",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -84,13 +84,14 @@ def lib() -> ctypes.CDLL:
         L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _S, _P]
         L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P,
                                    _P, _P, _S, _P]
+        L.bsa_sp_relayout.argtypes = [_I, _I, _I, _I, _I, _I, _P, _P, _P]
         L.bsa_launch_count.restype = ctypes.c_int64
         L.bsa_launch_count.argtypes = []
         L.bsa_timing_enable.argtypes = [_I]
         L.bsa_timing_read.argtypes = [_P, _P, _I]
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
-                  "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd"):
+                  "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -224,6 +225,20 @@ def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, dono
                               _ptr(k2q_idx), _ptr(lse), float(scale), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(ws), nb,
                               _stream(dev)), "bsa_attn_bwd")
     return dQ, dK, dV
+
+
+SP_SEQ_TO_SEND, SP_RECV_TO_HEADS, SP_HEADS_TO_SEND, SP_RECV_TO_SEQ = 0, 1, 2, 3
+
+
+def bsa_sp_relayout(mode: int, src: torch.Tensor, dst: torch.Tensor, B: int, Ls: int, Hh: int, d: int, P: int):
+    """Row reorder around the Ulysses all-to-all (include/bsa.h, bsa_sp_relayout); writes dst."""
+    _need_cuda(src, dst)
+    if src.dtype != torch.bfloat16 or dst.dtype != torch.bfloat16 or not src.is_contiguous() or not dst.is_contiguous():
+        raise BSAError("bsa_sp_relayout: src and dst must be contiguous bf16")
+    if src.numel() != B * Ls * Hh * d or dst.numel() != src.numel():
+        raise BSAError("bsa_sp_relayout: src/dst must hold B*Ls*Hh*d elements")
+    _check(lib().bsa_sp_relayout(mode, B, Ls, Hh, d, P, _ptr(src), _ptr(dst), _stream(src.device)), "bsa_sp_relayout")
+    return dst
 
 
 def resolve_k(f: float, N: int) -> int:

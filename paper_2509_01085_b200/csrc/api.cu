@@ -438,6 +438,21 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
 
 int64_t bsa_launch_count(void) { return g_launches; }
 
+int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int32_t P, const void* src, void* dst,
+                    void* stream) {
+  if (B < 1 || Ls < 1 || Hh < 1 || P < 1) return fail(BSA_ERR_INVALID_SHAPE, "B, Ls, Hh, P must be >= 1");
+  if (d < 8 || d % 8) return fail(BSA_ERR_INVALID_SHAPE, "d must be a positive multiple of 8 (got %d)", d);
+  if (Hh % P) return fail(BSA_ERR_CONFIG, "Hh = %d heads do not split over P = %d ranks", Hh, P);
+  if (mode < BSA_SP_SEQ_TO_SEND || mode > BSA_SP_RECV_TO_SEQ) return fail(BSA_ERR_CONFIG, "unknown mode %d", mode);
+  if (!src || !dst || !aligned16(src) || !aligned16(dst))
+    return fail(BSA_ERR_INVALID_SHAPE, "src/dst must be non-NULL and 16-byte aligned");
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = timed(BSA_K_SP_RELAYOUT, 1, st, [&] { return bsa::launch_sp_relayout(mode, B, Ls, Hh, d, P, src, dst, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "sp_relayout");
+  return BSA_OK;
+}
+
 // Debug aid (not in bsa.h): per-step timeline of one forward CTA, see attn_fwd.cu FWD_TRACE.
 int bsa_debug_trace_fwd(void* dev_buf, int cta) {
   cudaError_t e = bsa::debug_trace_fwd(dev_buf, cta);

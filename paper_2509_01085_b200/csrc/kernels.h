@@ -55,6 +55,10 @@ cudaError_t debug_trace_fwd(void* dev_buf, int cta);
 cudaError_t debug_trace_bwd(void* dev_buf, int cta);
 cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st);
 
+// Ulysses sequence parallelism: row reorders around the all-to-all (sp.cu)
+cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, const void* src, void* dst,
+                               cudaStream_t st);
+
 // a8 backward
 struct BwdArgs {
   Geo g;

@@ -77,7 +77,7 @@ int main() {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   EncodeTiledFn enc = nullptr; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
-  for (int mode : {3, 4, 5, 6}) for (int ctas : {148}) {
+  for (int mode : {0, 1, 2, 3, 4, 5, 6}) for (int ctas : {148, 296}) {
     CUtensorMap map; int boxc = mode == 3 ? 16 : (mode == 4 || mode == 6) ? 32 : 128; int boxr = mode == 6 ? 16 : 32;
     {
       cuuint64_t dims[2] = {128, nrows}; cuuint64_t str[1] = {512}; cuuint32_t box[2] = {(cuuint32_t)boxc, (cuuint32_t)boxr}; cuuint32_t es[2] = {1, 1};

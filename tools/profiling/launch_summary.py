@@ -8,7 +8,7 @@ import csv
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 rnd, path = sys.argv[1], sys.argv[2]
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 lines = [l for l in open(path) if l.startswith('"')]
@@ -19,7 +19,7 @@ scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "m
 ours = []
 for r in rows[1:]:
     name = r[ki]
-    if "bsa::" not in name:
+    if "bsa::" not in name and not name.startswith("k_"):
         continue
     base = name.split("(")[0].replace("void ", "").replace("bsa::", "").split("<")[0].strip()
     ours.append((base, float(r[vi].replace(",", "")) * scale[r[ui]]))
@@ -39,7 +39,7 @@ for b, t in tail:
     a[0] += 1
     a[1] += t
 out = [f"# Launch list ({rnd}): bsa kernels of the last {steps} bench steps", "",
-       f"Source: `{os.path.basename(path)}` = `ncu --metrics gpu__time_duration.sum --clock-control none` over "
+       f"Source: `{os.path.basename(path)}` = `ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_` over "
        "`python bench.py --steps 2 --warmup 3 --dense-steps 0 --e2e-steps 0 --no-cpu-baseline` (wan1.3b_32k). "
        "ncu serialises launches and runs them cold: compare shares with bench.py's live kernel_ms, not absolutes.",
        "", "| kernel | launches | ms per step | share of step |", "|---|---|---|---|"]
