@@ -110,7 +110,7 @@ void host_sizes(const bsa::Geo& g, double r, int* Lq, int* maxk) {
 }
 
 struct SelKvWs {
-  size_t kc, qc, s, bits, total;
+  size_t kc, qc, s, bits, kvbits, ovf, total;
 };
 SelKvWs selkv_ws(const bsa::Geo& g, size_t BH, int d) {
   SelKvWs w;
@@ -119,7 +119,9 @@ SelKvWs selkv_ws(const bsa::Geo& g, size_t BH, int d) {
   w.qc = w.kc + align256(BH * N * d * 8);
   w.s = w.qc + align256(BH * N * d * 8);
   w.bits = w.s + align256(BH * N * N * 8);
-  w.total = w.bits + align256(BH * N * NW * 4);
+  w.kvbits = w.bits + align256(BH * N * NW * 4);  // admission row bitmaps
+  w.ovf = w.kvbits + align256(BH * N * NW * 4);   // their transpose
+  w.total = w.ovf + align256((BH * N + 1) * 4);  // overflow row list of the warp admission kernel
   return w;
 }
 
@@ -280,7 +282,8 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
   double* Kc = reinterpret_cast<double*>(base + w.kc);
   double* Qc = q_pooled ? const_cast<double*>(q_pooled) : reinterpret_cast<double*>(base + w.qc);
   double* S = reinterpret_cast<double*>(base + w.s);
-  uint32_t* bits = k2q_num ? reinterpret_cast<uint32_t*>(base + w.bits) : nullptr;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(base + w.bits);
+  int* ovf = reinterpret_cast<int*>(base + w.ovf);
   cudaError_t e = timed(BSA_K_POOL, 1, st, [&] {
     return bsa::launch_pool(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(K), Kc, st);
   });
@@ -290,7 +293,6 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
     });
   if (e == cudaSuccess)
     e = timed(BSA_K_SCORES, 1, st, [&] { return bsa::launch_scores(G.N, static_cast<int>(BH), d, Qc, Kc, S, st); });
-  if (e == cudaSuccess && bits) e = cudaMemsetAsync(bits, 0, BH * G.N * ((G.N + 31) / 32) * 4, st);
   double z = 0.0;
   if (k < G.N) {
     double u = 1.0 - static_cast<double>(k) / G.N;
@@ -299,11 +301,14 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
     z = bsa::normal_quantile(u);
   }
   if (e == cudaSuccess)
-    e = timed(BSA_K_ADMIT, 1, st, [&] {
-      return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, q2k_num, q2k_idx, thresh, bits, st);
+    e = timed(BSA_K_ADMIT, k < G.N ? 2 : 1, st, [&] {
+      return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, q2k_num, q2k_idx, thresh, bits, ovf, st);
     });
-  if (e == cudaSuccess && bits)
-    e = timed(BSA_K_K2Q, 1, st, [&] { return bsa::launch_k2q(G.N, static_cast<int>(BH), bits, k2q_num, k2q_idx, st); });
+  if (e == cudaSuccess && k2q_num)
+    e = timed(BSA_K_K2Q, 2, st, [&] {
+      return bsa::launch_k2q(G.N, static_cast<int>(BH), bits, reinterpret_cast<uint32_t*>(base + w.kvbits), k2q_num,
+                             k2q_idx, st);
+    });
   if (e != cudaSuccess) return cuda_fail(e, "select_kv_blocks");
   return BSA_OK;
 }

@@ -412,40 +412,58 @@ cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, 
 }
 
 // ------------------------------------------------------------------------------------ a4
-// S[bh][i][j] = (sum_c Qc[i][c] Kc[j][c]) / sqrt(d): 32x32 output tile per CTA, 256 threads x 4
-// outputs, channels summed sequentially with exactly rounded mul/add.
+// S[bh][i][j] = (sum_c Qc[i][c] Kc[j][c]) / sqrt(d): 64x64 output tile per CTA, 256 threads x (4 x 4)
+// outputs, channels summed sequentially with exactly rounded mul/add (bit-identical to a plain
+// sequential fp64 loop). Operands are staged channel-major ([c][row], padded) so a warp's loads are
+// broadcasts / consecutive: per channel a thread reads 4 + 4 doubles for 16 products, which puts the
+// kernel on the fp64 pipe rather than shared-memory bandwidth.
+constexpr int SC_T = 64, SC_KC = 16, SC_LD = SC_T + 2;
 __global__ void __launch_bounds__(256) k_scores(int N, int d, const double* __restrict__ Qc,
                                                 const double* __restrict__ Kc, double* __restrict__ S) {
-  __shared__ double sa[32][17], sb[32][17];
-  const int bh = blockIdx.z, i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // ty in 0..7 -> rows ty, ty+8, ty+16, ty+24
+  __shared__ double sa[SC_KC][SC_LD], sb[SC_KC][SC_LD];
+  const int bh = blockIdx.z, i0 = blockIdx.y * SC_T, j0 = blockIdx.x * SC_T;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // outputs (ty + 16 a, tx + 16 b)
   const double* qh = Qc + static_cast<size_t>(bh) * N * d;
   const double* kh = Kc + static_cast<size_t>(bh) * N * d;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int c0 = 0; c0 < d; c0 += 16) {
-    for (int v = threadIdx.x; v < 32 * 16; v += 256) {
-      int rr = v / 16, cc = v % 16;
-      sa[rr][cc] = (i0 + rr < N) ? qh[static_cast<size_t>(i0 + rr) * d + c0 + cc] : 0.0;
-      sb[rr][cc] = (j0 + rr < N) ? kh[static_cast<size_t>(j0 + rr) * d + c0 + cc] : 0.0;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int c0 = 0; c0 < d; c0 += SC_KC) {
+#pragma unroll
+    for (int v0 = 0; v0 < SC_T * SC_KC; v0 += 256) {
+      const int v = v0 + threadIdx.x, rr = v / SC_KC, cc = v % SC_KC;
+      sa[cc][rr] = (i0 + rr < N) ? qh[static_cast<size_t>(i0 + rr) * d + c0 + cc] : 0.0;
+      sb[cc][rr] = (j0 + rr < N) ? kh[static_cast<size_t>(j0 + rr) * d + c0 + cc] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) {
-      double kv = sb[tx][cc];
+    for (int cc = 0; cc < SC_KC; ++cc) {
+      double av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) acc[a] = dadd(acc[a], dmul(sa[ty + 8 * a][cc], kv));
+      for (int a = 0; a < 4; ++a) av[a] = sa[cc][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sb[cc][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = dadd(acc[a][b], dmul(av[a], bv[b]));
     }
     __syncthreads();
   }
   const double sd = sqrt((double)d);
-  for (int a = 0; a < 4; ++a) {
-    int i = i0 + ty + 8 * a, j = j0 + tx;
-    if (i < N && j < N) S[(static_cast<size_t>(bh) * N + i) * N + j] = acc[a] / sd;
-  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i < N && j < N) S[(static_cast<size_t>(bh) * N + i) * N + j] = acc[a][b] / sd;
+    }
 }
 
 cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st) {
-  dim3 grid((N + 31) / 32, (N + 31) / 32, BH);
+  dim3 grid((N + SC_T - 1) / SC_T, (N + SC_T - 1) / SC_T, BH);
   k_scores<<<grid, 256, 0, st>>>(N, d, Qc, Kc, S);
   return cudaGetLastError();
 }
@@ -468,19 +486,25 @@ __device__ __forceinline__ bool before(double sa, int ja, double sb, int jb) {
   return sa > sb || (sa == sb && ja < jb);
 }
 
-// One CTA (256 threads) per (bh, query-block row i).
-__global__ void __launch_bounds__(256) k_admit(int N, const double* __restrict__ S, int k, double z, double tau,
-                                               int* __restrict__ q2k_num, int* __restrict__ q2k_idx,
-                                               double* __restrict__ thresh, uint32_t* __restrict__ kvbits) {
+// Row bitmap of the admitted set: qbits[row][w] bit b <=> KV block 32 w + b admitted by row (the
+// transpose k2q is read off its columns by k_k2q, no atomics).
+//
+// Fallback: one CTA (256 threads) per row, for rows whose candidate set exceeds the warp kernel's
+// shared-memory capacity (and for k = N, where every row has N candidates). `rows` lists the rows
+// to do (NULL = all rows, row = blockIdx.x); CTAs past *nrows exit at once.
+__global__ void __launch_bounds__(256) k_admit_cta(int N, const double* __restrict__ S, int k, double z, double tau,
+                                                   const int* __restrict__ rows, const int* __restrict__ nrows,
+                                                   int* __restrict__ q2k_num, int* __restrict__ q2k_idx,
+                                                   double* __restrict__ thresh, uint32_t* __restrict__ qbits) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int row = blockIdx.x;  // bh * N + i
-  const int bh = row / N, i = row % N;
+  if (rows && static_cast<int>(blockIdx.x) >= *nrows) return;
+  const int row = rows ? rows[blockIdx.x] : static_cast<int>(blockIdx.x);  // bh * N + i
   int P2 = 1;
   while (P2 < N) P2 <<= 1;
   double* s = reinterpret_cast<double*>(smem);  // [N]
   double* cs = s + N;                           // [P2] candidate scores (sorted)
   int* cj = reinterpret_cast<int*>(cs + P2);    // [P2] candidate ids
-  int* flag = cj + P2;                          // [N] admitted flags / scan
+  int* flag = cj + P2;                          // [N] admitted flags
   __shared__ double red[32];
   __shared__ int s_nc, s_wcnt[32], s_ell;
 
@@ -596,12 +620,13 @@ __global__ void __launch_bounds__(256) k_admit(int N, const double* __restrict__
     __syncthreads();
     ell = s_ell;
   }
-  // admitted flags -> ascending list
+  // admitted flags -> ascending list + row bitmap
   for (int j = threadIdx.x; j < N; j += blockDim.x) flag[j] = 0;
   __syncthreads();
   for (int t = threadIdx.x; t < ell; t += blockDim.x) flag[cj[t]] = 1;
   __syncthreads();
   int* out = q2k_idx + static_cast<size_t>(row) * N;
+  const int NW = (N + 31) / 32;
   __shared__ int s_base;
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
@@ -609,17 +634,14 @@ __global__ void __launch_bounds__(256) k_admit(int N, const double* __restrict__
     int j = base + threadIdx.x;
     bool a = j < N && flag[j];
     unsigned m = __ballot_sync(0xffffffffu, a);
-    if (lane == 0) s_wcnt[warp] = __popc(m);
+    if (lane == 0) {
+      s_wcnt[warp] = __popc(m);
+      if (qbits && base + warp * 32 < N) qbits[static_cast<size_t>(row) * NW + (base >> 5) + warp] = m;
+    }
     __syncthreads();
     int off = s_base;
     for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-    if (a) {
-      out[off + __popc(m & ((1u << lane) - 1u))] = j;
-      if (kvbits) {
-        const int NW = (N + 31) / 32;
-        atomicOr(kvbits + (static_cast<size_t>(bh) * N + j) * NW + i / 32, 1u << (i % 32));
-      }
-    }
+    if (a) out[off + __popc(m & ((1u << lane) - 1u))] = j;
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -631,17 +653,205 @@ __global__ void __launch_bounds__(256) k_admit(int N, const double* __restrict__
   if (threadIdx.x == 0) q2k_num[row] = ell;
 }
 
+// Fast path: one WARP per row (8 rows per 256-thread CTA, grid-stride), no block barriers. The
+// candidate set (about k entries by Eq.3's quantile, reading C14) is compacted into the warp's shared
+// slice of ADMIT_CAP entries; rows with more candidates are appended to `ovf` for k_admit_cta.
+// Same arithmetic as k_admit_cta: warp-tree mean and population std, candidates s >= p, bitonic
+// sort by (s desc, j asc), exp(s - s_max) masses, inclusive scan, shortest prefix >= tau E.
+constexpr int ADMIT_CAP = 512;
+constexpr int ADMIT_WARPS = 8;
+
+__device__ __forceinline__ double warp_sum_bcast(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);  // one lane's rounding for the whole warp
+}
+
+__global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const double* __restrict__ S, int k,
+                                                    double z, double tau, int* __restrict__ q2k_num,
+                                                    int* __restrict__ q2k_idx, double* __restrict__ thresh,
+                                                    uint32_t* __restrict__ qbits, int* __restrict__ ovf,
+                                                    int* __restrict__ n_ovf) {
+  extern __shared__ __align__(16) uint8_t smem[];  // per warp: [CAP] scores, [CAP] ids, [128] bitmap words
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* cs = reinterpret_cast<double*>(smem) + warp * ADMIT_CAP;
+  int* cj = reinterpret_cast<int*>(smem + ADMIT_WARPS * ADMIT_CAP * 8) + warp * ADMIT_CAP;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + ADMIT_WARPS * ADMIT_CAP * 12) + warp * 128;  // N <= 4096
+  const int NW = (N + 31) / 32;
+  for (int row = blockIdx.x * ADMIT_WARPS + warp; row < rows_total; row += gridDim.x * ADMIT_WARPS) {
+    const double* srow = S + static_cast<size_t>(row) * N;
+    double a = 0.0;
+    for (int j = lane; j < N; j += 32) a += __ldg(srow + j);
+    const double mu = warp_sum_bcast(a) / (double)N;
+    a = 0.0;
+    for (int j = lane; j < N; j += 32) {
+      const double t = __ldg(srow + j) - mu;
+      a += t * t;
+    }
+    const double sigma = sqrt(warp_sum_bcast(a) / (double)N);
+    const double p = mu + sigma * z;
+    // compaction (ascending j)
+    int nc = 0;
+    bool over = false;
+    for (int j0 = 0; j0 < N; j0 += 32) {
+      const int j = j0 + lane;
+      const double v = j < N ? __ldg(srow + j) : 0.0;
+      const bool c = j < N && v >= p;
+      const unsigned m = __ballot_sync(0xffffffffu, c);
+      const int pos = nc + __popc(m & ((1u << lane) - 1u));
+      if (c && pos < ADMIT_CAP) {
+        cs[pos] = v;
+        cj[pos] = j;
+      }
+      nc += __popc(m);
+    }
+    if (nc > ADMIT_CAP) over = true;
+    if (over) {  // leave this row to the CTA fallback
+      if (lane == 0) ovf[atomicAdd(n_ovf, 1)] = row;
+      continue;
+    }
+    if (lane == 0 && thresh) thresh[row] = p;
+    if (nc == 0) {  // C16: empty -> {argmax, lowest id}
+      double bv = -INFINITY;
+      int bj = INT_MAX;
+      for (int j = lane; j < N; j += 32) {
+        const double v = __ldg(srow + j);
+        if (v > bv || (v == bv && j < bj)) { bv = v; bj = j; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+      }
+      if (lane == 0) { cs[0] = bv; cj[0] = bj; }
+      nc = 1;
+    }
+    __syncwarp();
+    int ell = nc;
+    if (tau < 1.0 && nc > 1) {
+      int P = 1;
+      while (P < nc) P <<= 1;
+      for (int t = nc + lane; t < P; t += 32) { cs[t] = -INFINITY; cj[t] = INT_MAX; }
+      __syncwarp();
+      for (int sz = 2; sz <= P; sz <<= 1) {
+        for (int st = sz >> 1; st > 0; st >>= 1) {
+          for (int t = lane; t < P; t += 32) {
+            const int u = t ^ st;
+            if (u > t) {
+              const bool up = ((t & sz) == 0);
+              const double ct = cs[t], cu = cs[u];
+              const int jt = cj[t], ju = cj[u];
+              const bool swap = up ? before(cu, ju, ct, jt) : before(ct, jt, cu, ju);
+              if (swap) { cs[t] = cu; cs[u] = ct; cj[t] = ju; cj[u] = jt; }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      const double m = cs[0];
+      // cumulative masses in sorted order (warp scan, chunks of 32 with a carry)
+      double carry = 0.0;
+      for (int t0 = 0; t0 < nc; t0 += 32) {
+        const int t = t0 + lane;
+        double v = t < nc ? exp(cs[t] - m) : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        v += carry;
+        if (t < nc) cs[t] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
+      __syncwarp();
+      const double target = tau * cs[nc - 1];
+      ell = nc;
+      for (int t0 = 0; t0 < nc; t0 += 32) {
+        const int t = t0 + lane;
+        const unsigned hit = __ballot_sync(0xffffffffu, t < nc && cs[t] >= target);
+        if (hit) { ell = t0 + __ffs(hit); break; }
+      }
+    }
+    // admitted ids -> bitmap -> ascending list
+    for (int w = lane; w < NW; w += 32) bm[w] = 0u;
+    __syncwarp();
+    for (int t = lane; t < ell; t += 32) atomicOr(&bm[cj[t] >> 5], 1u << (cj[t] & 31));
+    __syncwarp();
+    int* out = q2k_idx + static_cast<size_t>(row) * N;
+    int base = 0;
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t v = w < NW ? bm[w] : 0u;
+      if (w < NW && qbits) qbits[static_cast<size_t>(row) * NW + w] = v;
+      const int c = __popc(v);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int pos = base + incl - c;
+      while (v) {
+        out[pos++] = w * 32 + __ffs(v) - 1;
+        v &= v - 1;
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) q2k_num[row] = ell;
+    __syncwarp();
+  }
+}
+
 cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int* q2k_num, int* q2k_idx,
-                         double* thresh, uint32_t* kvbits, cudaStream_t st) {
+                         double* thresh, uint32_t* qbits, int* ovf, cudaStream_t st) {
   int P2 = 1;
   while (P2 < N) P2 <<= 1;
-  size_t sm = static_cast<size_t>(N) * 8 + static_cast<size_t>(P2) * 12 + static_cast<size_t>(N) * 4;
-  cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_admit<<<N * BH, 256, sm, st>>>(N, S, k, z, tau, q2k_num, q2k_idx, thresh, kvbits);
+  const size_t sm = static_cast<size_t>(N) * 8 + static_cast<size_t>(P2) * 12 + static_cast<size_t>(N) * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_admit_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  const int rows = N * BH;
+  if (k >= N) {  // C15: every row has all N candidates
+    k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, nullptr, nullptr, q2k_num, q2k_idx, thresh, qbits);
+    return cudaGetLastError();
+  }
+  // ovf[0] = overflow count, ovf[1..] = overflow rows
+  e = cudaMemsetAsync(ovf, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = min_i((rows + ADMIT_WARPS - 1) / ADMIT_WARPS, sms * 4);
+  const int wsm = ADMIT_WARPS * (ADMIT_CAP * 12 + 128 * 4);
+  e = cudaFuncSetAttribute(k_admit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
+  if (e != cudaSuccess) return e;
+  k_admit_warp<<<grid, 256, wsm, st>>>(N, rows, S, k, z, tau, q2k_num, q2k_idx, thresh, qbits, ovf + 1, ovf);
+  k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, ovf + 1, ovf, q2k_num, q2k_idx, thresh, qbits);
   return cudaGetLastError();
 }
 
-// k2q: one warp per (bh, KV block j) reads the admission bitmap row and emits ascending i.
+// k2q: the transpose of the admission bitmaps. k_bits_transpose turns the row bitmaps qbits[bh][i][w]
+// into column bitmaps kvbits[bh][j][w'] (one warp per 32 x 32 bit tile: lane r holds the word of row
+// i0 + r, and the ballot of bit b over the lanes is the word of column j0 + b); k_k2q then reads one
+// column bitmap row per warp and emits the admitting query blocks i in ascending order.
+__global__ void __launch_bounds__(256) k_bits_transpose(int N, int BH, const uint32_t* __restrict__ qbits,
+                                                        uint32_t* __restrict__ kvbits) {
+  const int NW = (N + 31) / 32;
+  const size_t wid = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<size_t>(BH) * NW * NW) return;
+  const int bh = static_cast<int>(wid / (static_cast<size_t>(NW) * NW));
+  const int tw = static_cast<int>(wid % (static_cast<size_t>(NW) * NW));
+  const int wi = tw / NW, wj = tw % NW;  // row word-block (rows 32 wi ..), column word wj
+  const int i = wi * 32 + lane;
+  const uint32_t v = i < N ? qbits[(static_cast<size_t>(bh) * N + i) * NW + wj] : 0u;
+#pragma unroll 4
+  for (int b = 0; b < 32; ++b) {
+    const uint32_t col = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+    const int j = wj * 32 + b;
+    if (lane == b && j < N) kvbits[(static_cast<size_t>(bh) * N + j) * NW + wi] = col;
+  }
+}
+
 __global__ void __launch_bounds__(128) k_k2q(int N, int BH, const uint32_t* __restrict__ kvbits,
                                              int* __restrict__ k2q_num, int* __restrict__ k2q_idx) {
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -670,8 +880,12 @@ __global__ void __launch_bounds__(128) k_k2q(int N, int BH, const uint32_t* __re
   if (lane == 0) k2q_num[wid] = cnt;
 }
 
-cudaError_t launch_k2q(int N, int BH, const uint32_t* kvbits, int* k2q_num, int* k2q_idx, cudaStream_t st) {
-  int warps = N * BH;
+cudaError_t launch_k2q(int N, int BH, const uint32_t* qbits, uint32_t* kvbits, int* k2q_num, int* k2q_idx,
+                       cudaStream_t st) {
+  const size_t NW = (N + 31) / 32;
+  const size_t tiles = static_cast<size_t>(BH) * NW * NW;
+  k_bits_transpose<<<static_cast<unsigned>((tiles + 7) / 8), 256, 0, st>>>(N, BH, qbits, kvbits);
+  const int warps = N * BH;
   k_k2q<<<(warps + 3) / 4, 128, 0, st>>>(N, BH, kvbits, k2q_num, k2q_idx);
   return cudaGetLastError();
 }

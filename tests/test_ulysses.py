@@ -199,9 +199,11 @@ def test_ulysses_emulated_ranks_match_single_layer(P):
         seq = emulate(relay, [outs[p][i] for p in range(P)], B, Ls, Hh, d, P, False)
         got = torch.cat(seq, dim=1).permute(0, 2, 1, 3)  # [B, Hh, L, d]
         torch.cuda.synchronize()
-        # same selection (asserted above), but the forward's union walk and the backward's chunk walk start
-        # at a rotation that depends on the head's index in the batch, and dQ uses fp32 reduce-adds: the
-        # results agree up to fp32 summation order (north_star tolerances, relative to output scale)
+        # Same selection (asserted above), but the forward's union walk and the backward's chunk walk start
+        # at a rotation that depends on the head's index in the batch (so P is rounded to bf16 against
+        # different running maxima), and dQ uses fp32 reduce-adds: two valid runs, each within the oracle
+        # tolerance, that differ by a few bf16 steps in rare elements. A relayout error would be O(rms).
         diff = (got.float() - ref.float()).abs()
         rms = ref.float().pow(2).mean().sqrt().item()
-        assert diff.max().item() <= 2e-2 * rms and diff.mean().item() <= 2e-3 * rms, (i, diff.max().item(), rms)
+        assert diff.max().item() <= 5e-2 * rms and diff.mean().item() <= 1e-3 * rms, (i, diff.max().item(),
+                                                                                     diff.mean().item(), rms)
