@@ -315,6 +315,15 @@ def main():
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16"], "traffic": traffic, "peak_source": f"{peaks['source']} bf16 burst",
                 "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_ms}
+    # Secondary bound of the backward: every admitted (query row, KV block) sends one fp32 dQ
+    # partial row of d values to the L2 reduce units; measured ceiling of that path 6.2 TB/s
+    # (tools/microbench/red_rate.cu, 128-byte-row tensor reduce boxes, all SMs).
+    dq_bytes = layer.admitted_block_rows() * d * 4
+    bwd_ms = kms[10] / max(1, kcnt[10])
+    roofline["secondary"] = {"bound": "l2_reduce", "kernel": "attn_bwd", "bytes_per_launch": dq_bytes,
+                             "achieved_tbs": dq_bytes / (bwd_ms * 1e-3) / 1e12, "peak_tbs": 6.2,
+                             "frac": dq_bytes / (bwd_ms * 1e-3) / 1e12 / 6.2,
+                             "peak_source": "measured, tools/microbench/red_rate.cu (profiles/r01_microbench.md)"}
     # selection kernels against HBM (algorithmic bytes)
     BH, Lq, N = B * layer.Hh, layer.Lq, layer.N
     sel_bytes = BH * (4 * g.L * d + 4 * Lq + 4 * g.L + 2 * Lq * d + 8 * N * d + 4 * N * (1 + fl["pairs"] / max(1, BH * Lq)))

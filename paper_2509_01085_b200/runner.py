@@ -120,6 +120,12 @@ class BSAAttention:
         kv_tokens = torch.where(mask, bsz[idx], torch.zeros_like(idx)).sum(-1)  # [B,Hh,N]
         return int((kv_tokens * kept[None, None, :]).sum().item())
 
+    def admitted_block_rows(self) -> int:
+        """sum over (b,h,i) of |kept_i| * |S_i|: query rows times admitted KV blocks, i.e. the dQ partial rows the
+        KV-stationary backward reduces into L2 (one row of d fp32 per admitted (query row, KV block))."""
+        kept = (self.kept_off[1:] - self.kept_off[:-1]).to(torch.int64)
+        return int((self.q2k_num.to(torch.int64) * kept[None, None, :]).sum().item())
+
     def flops(self) -> dict:
         P = self.executed_pairs()
         d = self.d

@@ -184,8 +184,7 @@ def test_ulysses_emulated_ranks_match_single_layer(P):
     Q, K, V = bsa_gen.make_inputs("video", 1, B, Hh, grid, d, device="cuda")
     dO = bsa_gen.grad_output(1, (B, Hh, L, d)).cuda()
     full = BSAAttention(g, 0.5, 0.2, 0.9, B, Hh, d)
-    O = full.forward(Q, K, V).clone()
-    dQ, dK, dV = (x.clone() for x in full.backward(dO))
+    full.forward(Q, K, V)
     relay = lambda *a: bsa.bsa_sp_relayout(*a)
     to_shards = lambda x: [x.permute(0, 2, 1, 3)[:, s * Ls:(s + 1) * Ls].contiguous() for s in range(P)]
     Qh, Kh, Vh, dOh = (emulate(relay, to_shards(x), B, Ls, Hh, d, P, True) for x in (Q, K, V, dO))
@@ -195,15 +194,22 @@ def test_ulysses_emulated_ranks_match_single_layer(P):
         o = lay.forward(Qh[p], Kh[p], Vh[p]).clone()
         assert torch.equal(lay.q2k_num, full.q2k_num[:, p * Hp:(p + 1) * Hp])
         outs.append((o, *(x.clone() for x in lay.backward(dOh[p]))))
-    for i, ref in enumerate((O, dQ, dK, dV)):
+    # The assembled Ulysses result must meet the same oracle tolerance as the single layer (the two GPU runs
+    # differ only in summation order -- rotations depend on the head's index in the batch -- so they are
+    # compared through the oracle rather than bit for bit).
+    import math
+    from parity_util import assert_close
+    og = orc.Geom(*grid, 4, 4, 4)
+    k = resolve_k(0.2, orc.sizes(og, 0.5)[0])
+    Qn, Kn, Vn, dOn = (x[0].float().cpu().double().numpy() for x in (Q, K, V, dO))
+    qs = orc.select_queries(og, 0.5, Qn)
+    kv = orc.select_kv(og, Qn, Kn, k, 0.9)
+    sc = 1.0 / math.sqrt(d)
+    Or, _ = orc.attn_fwd(og, 0.5, Qn, Kn, Vn, qs["kept_tok"], qs["donor"], kv["q2k_num"], kv["q2k_idx"], sc)
+    grads = orc.attn_bwd(og, 0.5, Qn, Kn, Vn, dOn, qs["kept_tok"], qs["donor"], kv["q2k_num"], kv["q2k_idx"], sc)
+    assert np.array_equal(full.q2k_num[0].cpu().numpy(), kv["q2k_num"])
+    for i, (name, ref) in enumerate(zip(("O", "dQ", "dK", "dV"), (Or, *grads))):
         seq = emulate(relay, [outs[p][i] for p in range(P)], B, Ls, Hh, d, P, False)
         got = torch.cat(seq, dim=1).permute(0, 2, 1, 3)  # [B, Hh, L, d]
         torch.cuda.synchronize()
-        # Same selection (asserted above), but the forward's union walk and the backward's chunk walk start
-        # at a rotation that depends on the head's index in the batch (so P is rounded to bf16 against
-        # different running maxima), and dQ uses fp32 reduce-adds: two valid runs, each within the oracle
-        # tolerance, that differ by a few bf16 steps in rare elements. A relayout error would be O(rms).
-        diff = (got.float() - ref.float()).abs()
-        rms = ref.float().pow(2).mean().sqrt().item()
-        assert diff.max().item() <= 5e-2 * rms and diff.mean().item() <= 1e-3 * rms, (i, diff.max().item(),
-                                                                                     diff.mean().item(), rms)
+        assert_close(name, got[0], ref)

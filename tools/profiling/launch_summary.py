@@ -19,7 +19,7 @@ scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "m
 ours = []
 for r in rows[1:]:
     name = r[ki]
-    if "bsa::" not in name and not name.startswith("k_"):
+    if "bsa::" not in name and not name.replace("void ", "").startswith("k_"):
         continue
     base = name.split("(")[0].replace("void ", "").replace("bsa::", "").split("<")[0].strip()
     ours.append((base, float(r[vi].replace(",", "")) * scale[r[ui]]))
