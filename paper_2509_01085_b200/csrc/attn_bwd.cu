@@ -275,9 +275,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   // w9 gradient-MMA issuer, w10 producer, w11 S/dP-MMA issuer.
   constexpr int W_ALLOC = 8, W_B = 9, W_PROD = 10, W_SD = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
-  // zero both stages (rows of unused slots must be finite: they meet P = dS = 0 in the MMAs)
-  for (int o = tid * 16; o < 2 * SM::STAGE_BYTES; o += BWD_THREADS * 16)
-    *reinterpret_cast<uint4*>(sm + SM::OFF_ST + o) = make_uint4(0, 0, 0, 0);
+  // Rows of unused slots must be finite (they meet P = dS = 0 in the MMAs). Every stage is fully written
+  // by its first chunk except when that chunk is the list's only partial chunk (the last one, cc =
+  // nchunks - 1) and lands at c < 2 in the rotated order: only then can uninitialised shared memory be
+  // read, so only then is that stage zeroed.
+  if (nq % G != 0) {
+    const int cpart = (nchunks - 1 - crot + nchunks) % nchunks;
+    if (cpart < 2)
+      for (int o = tid * 16; o < SM::STAGE_BYTES; o += BWD_THREADS * 16)
+        *reinterpret_cast<uint4*>(sm + SM::OFF_ST + cpart * SM::STAGE_BYTES + o) = make_uint4(0, 0, 0, 0);
+  }
   if (D == 64)
     for (int o = tid * 16; o < 16384; o += BWD_THREADS * 16)
       *reinterpret_cast<uint4*>(sm + SM::OFF_ZERO + o) = make_uint4(0, 0, 0, 0);

@@ -167,16 +167,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     s_clsmask[tid] = m;
   }
   __syncthreads();
-  // admission bitmap of each slot (q2k lists)
-  for (int gi = 0; gi < G; ++gi) {
-    int qb = s_qb[gi];
-    if (qb < 0) continue;
-    size_t row = static_cast<size_t>(bh) * g.N + qb;
-    int num = p.q2k_num[row];
-    const int* idx = p.q2k_idx + row * g.N;
-    for (int a = tid; a < num; a += FWD_THREADS) {
-      int j = idx[a];
-      atomicOr(&bits[gi * NW + (j >> 5)], 1u << (j & 31));
+  // admission bitmap of each slot (q2k lists). The G lists are read concurrently (thread group gi
+  // of FWD_THREADS / G threads per slot): one dependent global round trip instead of G.
+  {
+    const int per = FWD_THREADS / G, gi = tid / per, t = tid % per;
+    const int qb = gi < G ? s_qb[gi] : -1;
+    if (qb >= 0) {
+      const size_t row = static_cast<size_t>(bh) * g.N + qb;
+      const int num = p.q2k_num[row];
+      const int* idx = p.q2k_idx + row * g.N;
+      for (int a = t; a < num; a += per) {
+        const int j = idx[a];
+        atomicOr(&bits[gi * NW + (j >> 5)], 1u << (j & 31));
+      }
     }
   }
   __syncthreads();

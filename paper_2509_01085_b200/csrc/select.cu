@@ -189,8 +189,12 @@ __device__ __forceinline__ void block_gram(const bf16* sq, int DS, int BTp, floa
 
 // One CTA (128 threads) per (bh, block). Shared layout: rows padded to D+8 bf16 so that
 // lane-strided 16-byte row reads and ldmatrix are bank-conflict free.
+// 6 CTAs per SM (the shared-memory limit): caps registers at 80 (0.255 -> 0.231 ms at 32k)
+#ifndef BSA_SELQ_MIN_BLOCKS
+#define BSA_SELQ_MIN_BLOCKS 6
+#endif
 template <int D>
-__global__ void __launch_bounds__(128) k_select_queries(Geo g, double r, int Lq, const bf16* __restrict__ Q,
+__global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo g, double r, int Lq, const bf16* __restrict__ Q,
                                                         const int* __restrict__ kept_off, int* __restrict__ kept_tok,
                                                         int* __restrict__ donor, double* __restrict__ q_pooled,
                                                         bf16* __restrict__ q_packed) {
