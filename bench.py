@@ -109,7 +109,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ reference arm
-def oracle_sample(cfg, seed, heads, threads):
+def oracle_sample(cfg, seed, heads, threads, unit=(0, 0, 0)):
     """The fp64 oracle as it stands on `heads` heads of the workload: selection + fwd + bwd.
     Returns (seconds, executed fwd+bwd FLOPs of the sample)."""
     import ctypes
@@ -119,7 +119,7 @@ def oracle_sample(cfg, seed, heads, threads):
     import bsa_gen
     import oracle as orc
     orc.set_threads(threads)
-    g = orc.Geom(*cfg["grid"], *cfg["block"])
+    g = orc.Geom(*cfg["grid"], *cfg["block"], *unit)
     d, r, tau = cfg["d"], cfg["r"], cfg["tau"]
     N, Lq = orc.sizes(g, r)
     k = orc.resolve_k(cfg["f"], N)
@@ -184,6 +184,7 @@ def main():
     ap.add_argument("--f", type=float, default=None, help="Eq.3 key fraction: k = ceil(f N)")
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--kind", default=None, choices=["video", "iid"])
+    ap.add_argument("--unit", default=None, help="query-selection window ut,uh,uw (P:168; default = whole block)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=6)
@@ -216,7 +217,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     L = bsa.lib()
 
-    g = bsa.Geometry(*cfg["grid"], *cfg["block"])
+    unit = tuple(int(x) for x in args.unit.split(",")) if args.unit else (0, 0, 0)
+    g = bsa.Geometry(*cfg["grid"], *cfg["block"], *unit)
     B, Hh, d = cfg["B"], cfg["Hh"], cfg["d"]
     from paper_2509_01085_b200.shard import head_range, problem_seed, reduce_step_stats
     if args.shard == "heads":
@@ -391,7 +393,7 @@ def main():
         import oracle as orc
         orc.build()
         threads = os.cpu_count() or 1
-        dt, cfl = oracle_sample(cfg, args.seed, 1, threads)
+        dt, cfl = oracle_sample(cfg, args.seed, 1, threads, unit)
         cpu = {"value": cfl / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": "oracle",
                "sample": f"head 0 of {Hh} of the {args.config} workload: full selection + fwd + bwd, fp64, "
                          f"{dt:.1f} s"}
@@ -406,6 +408,7 @@ def main():
             "config": {"workload": args.config, "grid": list(cfg["grid"]), "block": list(cfg["block"]), "B": B,
                        "heads": Hh, "d": d, "r": cfg["r"], "k": layer.k, "k_frac": cfg["f"], "tau": cfg["tau"],
                        "generator": cfg["kind"], "tokens": g.L, "N_blocks": N,
+                       "unit": list(unit) if args.unit else "block",
                        "l2": "inputs > L2 (4 x %.0f MB) and 256 MiB L2 flush between timed steps" % (tensor_bytes / 1e6),
                        "parallelism": (f"head-shard x{world} (heads of one problem split over ranks, no collective)"
                                        if args.shard == "heads" else

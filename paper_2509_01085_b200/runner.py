@@ -56,6 +56,7 @@ class BSAAttention:
         self._g = geom.c()
         self._partitioned = False
         self._saved = None
+        self._O = self.O
 
     def _stream(self):
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -81,33 +82,42 @@ class BSAAttention:
                                       _ptr(self.k2q_num), _ptr(self.k2q_idx), None, _ptr(self.ws), self.ws.numel(),
                                       st), "bsa_select_kv_blocks")
 
-    def attend(self, Q, K, V):
-        """a7 (Eq.5) + fill into self.O / self.lse."""
+    def attend(self, Q, K, V, out=None):
+        """a7 (Eq.5) + fill into `out` (default: the layer's own O buffer) and self.lse."""
+        O = self.O if out is None else out
+        if O.shape != self.O.shape or O.dtype != torch.bfloat16 or not O.is_contiguous():
+            raise BSAError("out must be a contiguous bf16 [B, Hh, L, d] tensor")
         _check(lib().bsa_attn_fwd(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q), _ptr(K), _ptr(V),
                                   _ptr(self.q_packed), _ptr(self.kept_off), _ptr(self.kept_tok), _ptr(self.donor),
-                                  _ptr(self.q2k_num), _ptr(self.q2k_idx), ctypes.c_float(self.scale), _ptr(self.O),
+                                  _ptr(self.q2k_num), _ptr(self.q2k_idx), ctypes.c_float(self.scale), _ptr(O),
                                   _ptr(self.lse), _ptr(self.ws), self.ws.numel(), self._stream()), "bsa_attn_fwd")
-        return self.O
+        self._O = O
+        return O
 
-    def forward(self, Q, K, V):
+    def forward(self, Q, K, V, out=None):
         for t in (Q, K, V):
             if t.shape != (self.B, self.Hh, self.g.L, self.d) or t.dtype != torch.bfloat16 or not t.is_contiguous():
                 raise BSAError("Q, K, V must be contiguous bf16 [B, Hh, L, d] matching the layer")
         self.select(Q, K)
         self._saved = (Q, K, V)
-        return self.attend(Q, K, V)
+        return self.attend(Q, K, V, out)
 
-    def backward(self, dO):
-        """a8: returns (dQ, dK, dV) for the last forward."""
+    def backward(self, dO, out=None):
+        """a8: returns (dQ, dK, dV) for the last forward, into `out` = (dQ, dK, dV) if given (default: the
+        layer's own buffers)."""
         if self._saved is None:
             raise BSAError("backward() before forward()")
         Q, K, V = self._saved
+        dQ, dK, dV = (self.dQ, self.dK, self.dV) if out is None else out
+        for t in (dQ, dK, dV):
+            if t.shape != self.dQ.shape or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise BSAError("gradient outputs must be contiguous bf16 [B, Hh, L, d] tensors")
         _check(lib().bsa_attn_bwd(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q), _ptr(K), _ptr(V),
-                                  _ptr(self.O), _ptr(dO), _ptr(self.q_packed), _ptr(self.kept_off),
+                                  _ptr(self._O), _ptr(dO), _ptr(self.q_packed), _ptr(self.kept_off),
                                   _ptr(self.kept_tok), _ptr(self.donor), _ptr(self.k2q_num), _ptr(self.k2q_idx),
-                                  _ptr(self.lse), ctypes.c_float(self.scale), _ptr(self.dQ), _ptr(self.dK),
-                                  _ptr(self.dV), _ptr(self.ws), self.ws.numel(), self._stream()), "bsa_attn_bwd")
-        return self.dQ, self.dK, self.dV
+                                  _ptr(self.lse), ctypes.c_float(self.scale), _ptr(dQ), _ptr(dK), _ptr(dV),
+                                  _ptr(self.ws), self.ws.numel(), self._stream()), "bsa_attn_bwd")
+        return dQ, dK, dV
 
     # ---------------------------------------------------------------- accounting (host side, untimed)
     def executed_pairs(self) -> int:

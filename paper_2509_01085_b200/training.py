@@ -1,0 +1,126 @@
+"""Training integration of the BSA layer: an autograd function over the C-ABI
+forward/backward and the paper's annealed sparsity schedule (§4 Implementation Details).
+
+    sched = AnnealSchedule()
+    attn = BSASelfAttention(Geometry(21, 30, 52, 4, 4, 4, 2, 2, 2), B=1, Hh=12, d=128, schedule=sched)
+    for step in range(steps):
+        attn.set_step(step)                 # (r, k, tau) of this step
+        O = attn(Q, K, V)                   # [B, Hh, L, d] bf16, differentiable w.r.t. Q, K, V
+        loss(O).backward()
+
+Selection (Eq.2-Eq.4) is piecewise constant in Q and K and is held fixed in the backward (reading C10);
+the gradients are those of bsa_attn_bwd. Every step runs in libbsa's kernels; this module only keeps a
+BSAAttention per (r, k, tau) setting and allocates the tensors autograd hands out.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import BSAError, Geometry, bsa_sizes, resolve_k
+
+
+@dataclass(frozen=True)
+class AnnealSchedule:
+    """"training begins with full attention, and every 30 steps, the sparsity is increased by 0.03
+    until reaching a maximum of 0.9. In KV-sparse, the number of top-k tokens selected is gradually reduced
+    from the total number of blocks to 0.1x the total".
+
+    Readings (C27): the combined sparsity s(step) = min(cap, increment * floor(step / interval));
+    the query side takes it first, r = max(r_final, 1 - s) (the paper's r = 0.5 is reached at s = 0.5, SPEC
+    knobs_for_sparsity); Eq.3's key fraction f = k / N falls linearly from kv_start to kv_end over the same
+    horizon the sparsity anneal needs to reach its cap (cap / increment * interval = 900 steps), then stays.
+    tau (Eq.4's cumulative target) is fixed."""
+    interval: int = 30
+    increment: float = 0.03
+    cap: float = 0.9
+    r_final: float = 0.5
+    kv_start: float = 1.0
+    kv_end: float = 0.1
+    tau: float = 0.9
+
+    @property
+    def horizon(self) -> int:
+        return int(round(self.cap / self.increment)) * self.interval
+
+    def sparsity_at_step(self, step: int) -> float:
+        if step < 0:
+            raise ValueError("step must be >= 0")
+        return min(self.cap, self.increment * (step // self.interval))
+
+    def kv_fraction_at_step(self, step: int) -> float:
+        if step < 0:
+            raise ValueError("step must be >= 0")
+        t = min(1.0, step / self.horizon)
+        return max(self.kv_end, self.kv_start + (self.kv_end - self.kv_start) * t)
+
+    def knobs(self, step: int) -> tuple[float, float, float]:
+        """(r, f, tau) for this step; step 0 is full attention (r = 1, f = 1, tau = 1)."""
+        s = self.sparsity_at_step(step)
+        if s == 0.0:
+            return 1.0, 1.0, 1.0
+        r = max(self.r_final, 1.0 - s)
+        return r, self.kv_fraction_at_step(step), self.tau
+
+
+class _BSAFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, Q, K, V, layer):
+        O = torch.empty_like(Q)
+        layer.forward(Q, K, V, out=O)
+        layer._fwd_count = getattr(layer, "_fwd_count", 0) + 1
+        ctx.layer, ctx.count = layer, layer._fwd_count
+        return O
+
+    @staticmethod
+    def backward(ctx, dO):
+        layer = ctx.layer
+        if layer._fwd_count != ctx.count:
+            raise BSAError("BSA backward after another forward through the same layer: the layer holds the "
+                           "selection and statistics of its last forward only (use one layer per call site)")
+        grads = tuple(torch.empty_like(dO) for _ in range(3))
+        layer.backward(dO.contiguous(), out=grads)
+        return (*grads, None)
+
+
+def bsa_attention(Q, K, V, layer):
+    """Differentiable BSA attention through `layer` (a runner.BSAAttention sized for Q's shape)."""
+    return _BSAFunction.apply(Q, K, V, layer)
+
+
+class BSASelfAttention(torch.nn.Module):
+    """The attention op of a DiT block with BSA's sparsity: Q, K, V [B, Hh, L, d] bf16 -> O."""
+
+    def __init__(self, geom: Geometry, B: int, Hh: int, d: int, schedule: AnnealSchedule | None = None,
+                 r: float = 0.5, f: float = 0.1, tau: float = 0.9, device="cuda"):
+        super().__init__()
+        self.geom, self.B, self.Hh, self.d, self.device = geom, B, Hh, d, torch.device(device)
+        self.schedule = schedule
+        self.r, self.f, self.tau = r, f, tau
+        self._layers: dict = {}
+
+    def set_step(self, step: int):
+        if self.schedule is None:
+            raise BSAError("no schedule attached")
+        self.r, self.f, self.tau = self.schedule.knobs(step)
+
+    def _layer(self):
+        from .runner import BSAAttention
+        N = bsa_sizes(self.geom, self.r)[0]
+        key = (self.r, resolve_k(self.f, N), self.tau)
+        lay = self._layers.get(key)
+        if lay is None:
+            # one preallocated layer per (r, k, tau) setting; a schedule visits at most ~cap/increment of them,
+            # older ones are dropped to bound memory
+            if len(self._layers) >= 4:
+                self._layers.pop(next(iter(self._layers)))
+            lay = BSAAttention(self.geom, key[0], key[1], key[2], self.B, self.Hh, self.d, device=self.device,
+                               scale=1.0 / math.sqrt(self.d))
+            self._layers[key] = lay
+        return lay
+
+    def forward(self, Q, K, V):
+        return bsa_attention(Q, K, V, self._layer())

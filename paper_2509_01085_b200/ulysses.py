@@ -56,11 +56,13 @@ class UlyssesBSA:
         n = B * self.Ls * Hh * d
         mk = dict(dtype=dtype, device=self.device)
         # per exchanged tensor: send / receive buffers (flat [P][B][Hp][Ls][d]) and the head-layout result
-        self._send = [torch.empty(n, **mk) for _ in range(3)]
-        self._recv = [torch.empty(n, **mk) for _ in range(3)]
+        # (P = 1: the head layout is reached by one reorder, no exchange buffers)
+        nx = n if self.P > 1 else 0
+        self._send = [torch.empty(nx, **mk) for _ in range(3)]
+        self._recv = [torch.empty(nx, **mk) for _ in range(3)]
         self._heads = [torch.empty(B, self.Hp, geom.L, d, **mk) for _ in range(3)]
         # dO gets its own buffers: Q^h, K^h, V^h stay saved for the backward
-        self._dO_bufs = (torch.empty(n, **mk), torch.empty(n, **mk), torch.empty(B, self.Hp, geom.L, d, **mk))
+        self._dO_bufs = (torch.empty(nx, **mk), torch.empty(nx, **mk), torch.empty(B, self.Hp, geom.L, d, **mk))
 
     # ---------------------------------------------------------------- exchanges
     def _a2a(self, recv, send, async_op=False):
@@ -73,10 +75,15 @@ class UlyssesBSA:
         """[B, Ls, Hh, d] (this rank's tokens) -> async exchange into slot i; returns the work handle."""
         if x.shape != (self.B, self.Ls, self.Hh, self.d):
             raise BSAError(f"Ulysses: expected [B, Ls, Hh, d] = {(self.B, self.Ls, self.Hh, self.d)}, got {tuple(x.shape)}")
+        if self.P == 1:  # [1][B][Hh][L][d] is already the head layout: no exchange, no second reorder
+            self._relayout(SP_SEQ_TO_SEND, x.contiguous(), self._heads[i], self.B, self.Ls, self.Hh, self.d, 1)
+            return None
         self._relayout(SP_SEQ_TO_SEND, x.contiguous(), self._send[i], self.B, self.Ls, self.Hh, self.d, self.P)
         return self._a2a(self._recv[i], self._send[i], async_op=True)
 
     def _recv_heads(self, i, work):
+        if self.P == 1:
+            return self._heads[i]
         if work is not None:
             work.wait()
         self._relayout(SP_RECV_TO_HEADS, self._recv[i], self._heads[i], self.B, self.Ls, self.Hh, self.d, self.P)
@@ -84,9 +91,12 @@ class UlyssesBSA:
 
     def _to_seq(self, x, i=0):
         """[B, Hp, L, d] (this rank's heads) -> [B, Ls, Hh, d] (this rank's tokens, all heads)."""
+        out = torch.empty(self.B, self.Ls, self.Hh, self.d, dtype=x.dtype, device=x.device)
+        if self.P == 1:  # x is [1][B][Hh][L][d]: one reorder back to the model layout
+            self._relayout(SP_RECV_TO_SEQ, x.contiguous(), out, self.B, self.Ls, self.Hh, self.d, 1)
+            return out
         self._relayout(SP_HEADS_TO_SEND, x.contiguous(), self._send[i], self.B, self.Ls, self.Hh, self.d, self.P)
         self._a2a(self._recv[i], self._send[i])
-        out = torch.empty(self.B, self.Ls, self.Hh, self.d, dtype=x.dtype, device=x.device)
         self._relayout(SP_RECV_TO_SEQ, self._recv[i], out, self.B, self.Ls, self.Hh, self.d, self.P)
         return out
 
@@ -109,9 +119,12 @@ class UlyssesBSA:
         s, r, h = self._dO_bufs
         if dO.shape != (self.B, self.Ls, self.Hh, self.d):
             raise BSAError("Ulysses: dO must be [B, Ls, Hh, d]")
-        self._relayout(SP_SEQ_TO_SEND, dO.contiguous(), s, self.B, self.Ls, self.Hh, self.d, self.P)
-        self._a2a(r, s)
-        self._relayout(SP_RECV_TO_HEADS, r, h, self.B, self.Ls, self.Hh, self.d, self.P)
+        if self.P == 1:
+            self._relayout(SP_SEQ_TO_SEND, dO.contiguous(), h, self.B, self.Ls, self.Hh, self.d, 1)
+        else:
+            self._relayout(SP_SEQ_TO_SEND, dO.contiguous(), s, self.B, self.Ls, self.Hh, self.d, self.P)
+            self._a2a(r, s)
+            self._relayout(SP_RECV_TO_HEADS, r, h, self.B, self.Ls, self.Hh, self.d, self.P)
         dQ, dK, dV = self.layer.backward(h)
         # the send/recv slots of Q, K, V are free again (their head layouts live in self._heads)
         return self._to_seq(dQ, 0), self._to_seq(dK, 1), self._to_seq(dV, 2)
