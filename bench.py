@@ -109,7 +109,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ reference arm
-def oracle_sample(cfg, seed, heads, threads, unit=(0, 0, 0)):
+def oracle_sample(cfg, seed, heads, threads, unit=(0, 0, 0), inputs=None):
     """The fp64 oracle as it stands on `heads` heads of the workload: selection + fwd + bwd.
     Returns (seconds, executed fwd+bwd FLOPs of the sample)."""
     import ctypes
@@ -123,8 +123,11 @@ def oracle_sample(cfg, seed, heads, threads, unit=(0, 0, 0)):
     d, r, tau = cfg["d"], cfg["r"], cfg["tau"]
     N, Lq = orc.sizes(g, r)
     k = orc.resolve_k(cfg["f"], N)
-    Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, 1, heads, cfg["grid"], d)
-    dO = bsa_gen.grad_output(seed, (1, heads, g.L, d))
+    if inputs is None:
+        Q, K, V = bsa_gen.make_inputs(cfg["kind"], seed, 1, heads, cfg["grid"], d)
+        dO = bsa_gen.grad_output(seed, (1, heads, g.L, d))
+    else:  # the exact bf16 values the GPU run used (generated on the device)
+        Q, K, V, dO = (x[:1, :heads].cpu() for x in inputs)
     Qd, Kd, Vd, dOd = (x.double().numpy().reshape(heads, g.L, d) for x in (Q, K, V, dO))
     t0 = time.perf_counter()
     qs = orc.select_queries(g, r, Qd)
@@ -140,7 +143,22 @@ def oracle_sample(cfg, seed, heads, threads, unit=(0, 0, 0)):
     for h in range(heads):
         for i in range(N):
             P += int(kept[i]) * int(bsz[kv["q2k_idx"][h, i, :kv["q2k_num"][h, i]]].sum())
+    oracle_sample.last = (qs, kv)  # selection of the sample, for the GPU-vs-oracle spot check
     return dt, 14 * d * P
+
+
+def selection_spot_check(layer, qs, kv):
+    """Head 0's selection from the timed GPU run against the oracle's (bit-exact expected)."""
+    import numpy as np
+    kept = layer.kept_tok[0, 0].cpu().numpy()
+    donor = layer.donor[0, 0].cpu().numpy()
+    num = layer.q2k_num[0, 0].cpu().numpy()
+    idx = layer.q2k_idx[0, 0].cpu().numpy()
+    rows_eq = sum(int(num[i] == kv["q2k_num"][0, i] and np.array_equal(idx[i, :num[i]], kv["q2k_idx"][0, i, :num[i]]))
+                  for i in range(len(num)))
+    return {"head": 0, "kept_tok_equal": bool(np.array_equal(kept, qs["kept_tok"][0])),
+            "donor_equal": bool(np.array_equal(donor, qs["donor"][0])), "q2k_rows_equal": rows_eq,
+            "q2k_rows": int(len(num))}
 
 
 def run_reference(args, cfg, rank, world):
@@ -393,10 +411,13 @@ def main():
         import oracle as orc
         orc.build()
         threads = os.cpu_count() or 1
-        dt, cfl = oracle_sample(cfg, args.seed, 1, threads, unit)
+        same = args.shard != "ulysses"
+        dt, cfl = oracle_sample(cfg, args.seed, 1, threads, unit, inputs=(Q, K, V, dO) if same else None)
         cpu = {"value": cfl / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": "oracle",
                "sample": f"head 0 of {Hh} of the {args.config} workload: full selection + fwd + bwd, fp64, "
                          f"{dt:.1f} s"}
+        if same:
+            cpu["selection_check"] = selection_spot_check(layer, *oracle_sample.last)
 
     if rank == 0:
         line = {
