@@ -216,6 +216,16 @@ struct BwdSmem {
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
+// A CTA handles BWD_NB (= 2; 4 / 8 / 16 measured 1.72 / 1.82 / 1.97 ms vs 1.71 at 32k: tail imbalance)
+// consecutive KV blocks of one head, one after another, with every barrier phase
+// counted across them (chunk counter c runs over all of the CTA's chunks): the dQ drain of a block's last
+// chunks, its dK/dV epilogue and the next block's K/V load overlap the next block's first chunks, and the
+// CTA prologue (barrier init, TMEM allocation, stage zeroing) is paid once per BWD_NB blocks.
+#ifndef BSA_BWD_NB
+#define BSA_BWD_NB 2
+#endif
+constexpr int BWD_NB = BSA_BWD_NB;
+
 template <int D, int BT>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
   using SM = BwdSmem<D, BT>;
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   };
 
   __shared__ __align__(8) uint64_t bar_kv, bar_c_full[2], bar_c_empty[2], bar_sd_full, bar_sd_free, bar_ps_full,
-      bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc;
+      bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc, bar_acc_free;
   __shared__ uint32_t s_tmem;
   // Chunk metadata ring (first packed row, kept count, block id of each slot; row -1 = empty slot), written
   // by the producer for chunk c into entry c & 3. Four deep: the producer rewrites an entry only after
@@ -242,13 +252,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j = blockIdx.x, bh = blockIdx.y;
+  const int bh = blockIdx.y;
   const int G = p.G, SR = p.SR;
-  const size_t jrow = static_cast<size_t>(bh) * g.N + j;
-  const int nq = p.k2q_num[jrow];
-  const int* qlist = p.k2q_idx + jrow * g.N;
-  const int nchunks = (nq + G - 1) / G;
-  const int crot = nchunks > 0 ? static_cast<int>((static_cast<unsigned>(j) * 2654435761u + bh * 40503u) % nchunks) : 0;
+  const int j_first = blockIdx.x * BWD_NB, j_end = min_i(j_first + BWD_NB, g.N);
+  // per KV block of this CTA: admitting query blocks, chunks, rotation of the chunk order (concurrent CTAs
+  // start on different query blocks: no L2 hot spot)
+  auto nq_of = [&](int j) { return p.k2q_num[static_cast<size_t>(bh) * g.N + j]; };
+  auto rot_of = [&](int j, int nch) {
+    return nch > 0 ? static_cast<int>((static_cast<unsigned>(j) * 2654435761u + bh * 40503u) % nch) : 0;
+  };
 
 #ifdef BSA_TRACE
   unsigned long long t_start;
@@ -267,24 +279,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     mbar_init(&bar_ps_full, 128);
     mbar_init(&bar_ps_free, 1);
     mbar_init(&bar_acc, 1);
+    mbar_init(&bar_acc_free, 128);
     fence_mbar_init();
   }
   // Warp roles (the warp arbiter favours higher ids, so the single-thread producer and MMA roles get the
   // highest ones and are not starved by the math warps sharing their sub-partition):
-  // w0-3 gradient softmax (TMEM quadrant = warp), w4-7 dQ drain (quadrant = warp - 4), w8 TMEM allocator,
-  // w9 gradient-MMA issuer, w10 producer, w11 S/dP-MMA issuer.
+  // w0-3 gradient softmax + dK/dV epilogue (TMEM quadrant = warp), w4-7 dQ drain (quadrant = warp - 4),
+  // w8 TMEM allocator, w9 gradient-MMA issuer, w10 producer, w11 S/dP-MMA issuer.
   constexpr int W_ALLOC = 8, W_B = 9, W_PROD = 10, W_SD = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
-  // Rows of unused slots must be finite (they meet P = dS = 0 in the MMAs). Every stage is fully written
-  // by its first chunk except when that chunk is the list's only partial chunk (the last one, cc =
-  // nchunks - 1) and lands at c < 2 in the rotated order: only then can uninitialised shared memory be
-  // read, so only then is that stage zeroed.
-  if (nq % G != 0) {
-    const int cpart = (nchunks - 1 - crot + nchunks) % nchunks;
-    if (cpart < 2)
-      for (int o = tid * 16; o < SM::STAGE_BYTES; o += BWD_THREADS * 16)
-        *reinterpret_cast<uint4*>(sm + SM::OFF_ST + cpart * SM::STAGE_BYTES + o) = make_uint4(0, 0, 0, 0);
-  }
+  // zero both stages once (rows of unused slots must be finite: they meet P = dS = 0 in the MMAs; after a
+  // stage's first fill its stale rows stay finite)
+  for (int o = tid * 16; o < 2 * SM::STAGE_BYTES; o += BWD_THREADS * 16)
+    *reinterpret_cast<uint4*>(sm + SM::OFF_ST + o) = make_uint4(0, 0, 0, 0);
   if (D == 64)
     for (int o = tid * 16; o < 16384; o += BWD_THREADS * 16)
       *reinterpret_cast<uint4*>(sm + SM::OFF_ZERO + o) = make_uint4(0, 0, 0, 0);
@@ -299,8 +306,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 
   if (warp == W_PROD) {
     // ============================ producer (lane 0 issues TMA; all lanes fetch metadata)
-    if (nchunks > 0) {
+    int c = 0, nacc = 0;  // global chunk counter; blocks with MMAs so far (bar_kv / bar_acc phases)
+    for (int j = j_first; j < j_end; ++j) {
+      const int nq = nq_of(j), nchunks = (nq + G - 1) / G, crot = rot_of(j, nchunks);
+      if (nchunks == 0) continue;
+      const int* qlist = p.k2q_idx + (static_cast<size_t>(bh) * g.N + j) * g.N;
       if (lane == 0) {
+        // K/V of the previous block are read until its last MMA: bar_acc of that block
+        if (nacc > 0) mbar_wait(&bar_acc, (nacc - 1) & 1);
         int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
         mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
         for (int cb = 0; cb < NCB; ++cb) {
@@ -308,10 +321,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
         }
       }
-      for (int c = 0; c < nchunks; ++c) {
+      ++nacc;
+      for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
-        // rotated chunk order: concurrent CTAs start on different query blocks (no L2 hot spot)
-        const int cc = (c + crot) % nchunks;
+        const int cc = (cl + crot) % nchunks;
         const int nb = min_i(G, nq - cc * G);
         int row0 = -1, nk = 0, qbl = 0;
         if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
@@ -333,11 +346,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           mbar_expect_tx(&bar_c_full[s], nb * (blk_bytes + ld_bytes));
           BWD_TRACE(0, c);
           for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
-#ifndef BSA_ABLATE_BWD_HOTSET
             const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[ring][gi];
-#else
-            const size_t qimg = static_cast<size_t>(bh) * g.N + gi;
-#endif
             bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + qimg * blk_bytes, blk_bytes, &bar_c_full[s]);
             bulk_load(stage_ld(s) + gi * 2 * SR, p.lsed + qimg * 2 * SR, ld_bytes, &bar_c_full[s]);
           }
@@ -348,33 +357,36 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   } else if (warp == W_SD || warp == W_B) {
     // ============================ MMA issuer: whole warp walks the schedule (uniform registers), one
     // elected lane issues. Descriptors are precomputed bases advanced by (byte offset >> 4).
-    if (nchunks > 0) {
-      const bool leader = elect_one();
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, BT, 0, 0);  // Q K^T / dO V^T
-      constexpr uint32_t idesc_t = umma_idesc_bf16(128, BT, 1, 1);  // dO^T P / Q^T dS (M = d padded to 128)
-      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);   // dS K
-      const uint32_t zero = smem_u32(sm + SM::OFF_ZERO);
-      // K-major A over the chunk's 128 rows: 8-row groups SM::PG apart (QdO image layout)
-      const uint64_t dQa = umma_desc_sw128(smem_u32(stage_q(0)), 16, SM::PG);
-      const uint64_t dDa = umma_desc_sw128(smem_u32(stage_do(0)), 16, SM::PG);
-      // MN-major A over d (K = query rows, 16 per step = two 8-row groups, SBO = SM::PG); the second
-      // 64-channel chunk sits LBO = 1 KB after the first (d = 128)
-      const uint64_t dQt = umma_desc_sw128(smem_u32(stage_q(0)), 1024, SM::PG);
-      const uint64_t dDt = umma_desc_sw128(smem_u32(stage_do(0)), 1024, SM::PG);
-      const uint64_t dK = umma_desc_sw128(smem_u32(sK), 16, 1024), dV = umma_desc_sw128(smem_u32(sV), 16, 1024);
-      const uint64_t dKt = umma_desc_sw128(smem_u32(sK), BT * 128, 1024);
-      const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
-      const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
-      mbar_wait(&bar_kv, 0);
+    const bool leader = elect_one();
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, BT, 0, 0);  // Q K^T / dO V^T
+    constexpr uint32_t idesc_t = umma_idesc_bf16(128, BT, 1, 1);  // dO^T P / Q^T dS (M = d padded to 128)
+    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);   // dS K
+    const uint32_t zero = smem_u32(sm + SM::OFF_ZERO);
+    // K-major A over the chunk's 128 rows: 8-row groups SM::PG apart (QdO image layout)
+    const uint64_t dQa = umma_desc_sw128(smem_u32(stage_q(0)), 16, SM::PG);
+    const uint64_t dDa = umma_desc_sw128(smem_u32(stage_do(0)), 16, SM::PG);
+    // MN-major A over d (K = query rows, 16 per step = two 8-row groups, SBO = SM::PG); the second
+    // 64-channel chunk sits LBO = 1 KB after the first (d = 128)
+    const uint64_t dQt = umma_desc_sw128(smem_u32(stage_q(0)), 1024, SM::PG);
+    const uint64_t dDt = umma_desc_sw128(smem_u32(stage_do(0)), 1024, SM::PG);
+    const uint64_t dK = umma_desc_sw128(smem_u32(sK), 16, 1024), dV = umma_desc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t dKt = umma_desc_sw128(smem_u32(sK), BT * 128, 1024);
+    const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
+    const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
+    int c = 0, nacc = 0;
+    for (int j = j_first; j < j_end; ++j) {
+      const int nchunks = (nq_of(j) + G - 1) / G;
+      if (nchunks == 0) continue;
       if (warp == W_SD) {
+        mbar_wait(&bar_kv, nacc & 1);
         // S/dP(v) = Q^s K^T, dO^s V^T of chunk v, issued as soon as its stage landed and the softmax
         // warps hold S/dP(v-1) in registers (single TMEM buffer)
-        for (int v = 0; v < nchunks; ++v) {
-          const int sv = v & 1;
+        for (int cl = 0; cl < nchunks; ++cl, ++c) {
+          const int sv = c & 1;
           const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
-          mbar_wait(&bar_c_full[sv], (v >> 1) & 1);
-          BWD_TRACE(11, v);
-          if (v >= 1) mbar_wait(&bar_sd_free, (v - 1) & 1);
+          mbar_wait(&bar_c_full[sv], (c >> 1) & 1);
+          BWD_TRACE(11, c);
+          if (c >= 1) mbar_wait(&bar_sd_free, (c - 1) & 1);
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -386,13 +398,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             umma_commit(&bar_sd_full);
           }
           __syncwarp();
-          BWD_TRACE(1, v);
+          BWD_TRACE(1, c);
         }
       } else {
         // gradient MMAs of chunk c once P/dS(c) is in smem and the drain emptied dQ buffer c & 1. S/dP(c)
         // (the other issuer) completed before P/dS(c) could exist, so the c_empty commit below covers
-        // every read of the stage.
-        for (int c = 0; c < nchunks; ++c) {
+        // every read of the stage. The first chunk of a block overwrites dV/dK: the epilogue of the
+        // previous block must have read them (bar_acc_free).
+        if (nacc > 0) mbar_wait(&bar_acc_free, (nacc - 1) & 1);
+        for (int cl = 0; cl < nchunks; ++cl, ++c) {
           const int s = c & 1, qbuf = c & 1;
           const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
           mbar_wait(&bar_ps_full, c & 1);
@@ -412,8 +426,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
                 aq = umma_desc_sw128(qk, zero - qk, SM::PG);
                 ad = umma_desc_sw128(dk, zero - dk, SM::PG);
               }
-              umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
-              umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (c > 0 || kk > 0) ? 1u : 0u);
+              umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (cl > 0 || kk > 0) ? 1u : 0u);
+              umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (cl > 0 || kk > 0) ? 1u : 0u);
             }
             umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
 #pragma unroll
@@ -425,22 +439,26 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           __syncwarp();
           BWD_TRACE(3, c);
         }
-        if (leader) umma_commit(&bar_acc);  // after the last gradient MMA: every MMA of the CTA is done
+        if (leader) umma_commit(&bar_acc);  // after the block's last gradient MMA: all its MMAs are done
         __syncwarp();
       }
+      ++nacc;
     }
 #ifdef BSA_TRACE
   } else if (warp == W_ALLOC) {
     // debug observer (trace builds only): when each chunk's loads land
-    if (lane == 0)
-      for (int c = 0; c < nchunks; ++c) {
-        mbar_wait(&bar_c_full[c & 1], (c >> 1) & 1);
-        BWD_TRACE(12, c);
-      }
+    if (lane == 0) {
+      int c = 0;
+      for (int j = j_first; j < j_end; ++j)
+        for (int cl = 0; cl < (nq_of(j) + G - 1) / G; ++cl, ++c) {
+          mbar_wait(&bar_c_full[c & 1], (c >> 1) & 1);
+          BWD_TRACE(12, c);
+        }
+    }
     __syncwarp();
 #endif
   } else if (warp < 4) {
-    // ============================ gradient softmax (thread == query row == TMEM lane)
+    // ============================ gradient softmax (thread == query row == TMEM lane) + dK/dV epilogue
     const int q4 = warp;
     const int row = q4 * 32 + lane;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
@@ -449,92 +467,115 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     // (TMA out-of-grid fill), so they add nothing to dQ = dS K, and their dK/dV columns are never stored.
     const float sl2 = p.scale_log2;
     const uint32_t sP_u = smem_u32(sP) + row * 128, sdS_u = smem_u32(sdS) + row * 128;
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c & 1;
-      mbar_wait(&bar_c_full[s], (c >> 1) & 1);
-      const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
-      const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
-      const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
-      mbar_wait(&bar_sd_full, c & 1);
-      tc_fence_after();
-      if (row == 0) BWD_TRACE(4, c);
-      // the whole S/dP row goes to registers first, so the TMEM buffer is handed back to the MMA warp
-      // (S/dP of the next chunk) before any math
-      float sv[BT], dp[BT];
+    int c = 0, nacc = 0;
+    bool store_pending = false;  // a dK/dV TMA store still reading sP/sdS (issued by row 0)
+    for (int j = j_first; j < j_end; ++j) {
+      const int nchunks = (nq_of(j) + G - 1) / G;
+      for (int cl = 0; cl < nchunks; ++cl, ++c) {
+        const int s = c & 1;
+        mbar_wait(&bar_c_full[s], (c >> 1) & 1);
+        const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
+        const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
+        const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
+        mbar_wait(&bar_sd_full, c & 1);
+        tc_fence_after();
+        if (row == 0) BWD_TRACE(4, c);
+        // the whole S/dP row goes to registers first, so the TMEM buffer is handed back to the MMA warp
+        // (S/dP of the next chunk) before any math
+        float sv[BT], dp[BT];
 #pragma unroll
-      for (int c16 = 0; c16 < BT; c16 += 16) {
-        tmem_ld16(trow + c16, sv + c16);
-        tmem_ld16(trow + BT + c16, dp + c16);
-      }
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&bar_sd_free);
-      if (row == 0) BWD_TRACE(8, c);
-#pragma unroll
-      for (int cc = 0; cc < BT; ++cc) {
-        const float pr = ex2b(fmaf(sv[cc], sl2, nl));
-        sv[cc] = pr;
-        dp[cc] = pr * (dp[cc] - Dq);
-      }
-      if (row == 0) BWD_TRACE(9, c);
-      if (c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
-      if (row == 0) BWD_TRACE(10, c);
-#pragma unroll
-      for (int c8 = 0; c8 < BT / 8; ++c8) {
-        const uint32_t off = ((static_cast<uint32_t>(c8) ^ (row & 7)) << 4);
-        const float* a = sv + c8 * 8;
-        const float* b = dp + c8 * 8;
-        sts128(sP_u + off, pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
-        sts128(sdS_u + off, pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]), pack_bf16(b[4], b[5]), pack_bf16(b[6], b[7]));
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bar_ps_full);
-      if (row == 0) BWD_TRACE(5, c);
-    }
-    if (row == 0) CTA_STAMP(5);
-    // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j. Transposed into
-    // the block's [key][64-channel] SW128 tiles in smem (stage 0 is idle now) and written with the same
-    // 5D block box the K/V tiles came in with, so keys past a ragged block's extent are clipped by TMA.
-    const int ch_ = row;
-    const uint32_t tdk = smem_u32(stage_q(0)), tdv = tdk + NCB * BT * 128;
-    if (nchunks > 0) {
-      mbar_wait(&bar_acc, 0);
-      tc_fence_after();
-    }
-#pragma unroll 1
-    for (int cc0 = 0; cc0 < BT; cc0 += 16) {
-      float kv[16], vv[16];
-      if (nchunks > 0) {
-        tmem_ld16(trow + 3 * BT + cc0, kv);
-        tmem_ld16(trow + 2 * BT + cc0, vv);
+        for (int c16 = 0; c16 < BT; c16 += 16) {
+          tmem_ld16(trow + c16, sv + c16);
+          tmem_ld16(trow + BT + c16, dp + c16);
+        }
         tmem_wait_ld();
-      } else {
+        tc_fence_before();
+        mbar_arrive(&bar_sd_free);
+        if (row == 0) BWD_TRACE(8, c);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) kv[e] = vv[e] = 0.f;
+        for (int cc = 0; cc < BT; ++cc) {
+          const float pr = ex2b(fmaf(sv[cc], sl2, nl));
+          sv[cc] = pr;
+          dp[cc] = pr * (dp[cc] - Dq);
+        }
+        if (row == 0) BWD_TRACE(9, c);
+        if (c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+        if (store_pending) {  // the previous block's dK/dV store must have read sP/sdS
+          if (row == 0) bulk_wait_group_read<0>();
+          named_bar_sync(1, 128);
+          store_pending = false;
+        }
+        if (row == 0) BWD_TRACE(10, c);
+#pragma unroll
+        for (int c8 = 0; c8 < BT / 8; ++c8) {
+          const uint32_t off = ((static_cast<uint32_t>(c8) ^ (row & 7)) << 4);
+          const float* a = sv + c8 * 8;
+          const float* b = dp + c8 * 8;
+          sts128(sP_u + off, pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+          sts128(sdS_u + off, pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]), pack_bf16(b[4], b[5]), pack_bf16(b[6], b[7]));
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bar_ps_full);
+        if (row == 0) BWD_TRACE(5, c);
       }
-      if (ch_ < D) {
-        const uint32_t cofs = (ch_ >> 6) * BT * 128 + (ch_ & 7) * 2;
+      if (row == 0) CTA_STAMP(5);
+      // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j. Transposed into
+      // the block's [key][64-channel] SW128 tiles in sP (dK) and sdS (dV) -- free once the block's last
+      // gradient MMA completed -- and written with the same 5D block box the K/V tiles came in with, so
+      // keys past a ragged block's extent are clipped by TMA. bar_acc_free hands dV/dK back to the next
+      // block's first gradient MMAs as soon as they are in registers.
+      const int ch_ = row;
+      const uint32_t tdk = smem_u32(sP), tdv = smem_u32(sdS);
+      if (nchunks > 0) {
+        mbar_wait(&bar_acc, nacc & 1);
+        tc_fence_after();
+      }
+      if (store_pending) {  // (a block with no chunks right after another block's store)
+        if (row == 0) bulk_wait_group_read<0>();
+        named_bar_sync(1, 128);
+        store_pending = false;
+      }
+#pragma unroll 1
+      for (int cc0 = 0; cc0 < BT; cc0 += 16) {
+        float kv[16], vv[16];
+        if (nchunks > 0) {
+          tmem_ld16(trow + 3 * BT + cc0, kv);
+          tmem_ld16(trow + 2 * BT + cc0, vv);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t o = cofs + sw128_off(cc0 + e, (ch_ & 63) >> 3);
-          sts16(tdk + o, __bfloat16_as_ushort(__float2bfloat16_rn(kv[e] * p.scale)));
-          sts16(tdv + o, __bfloat16_as_ushort(__float2bfloat16_rn(vv[e])));
+          for (int e = 0; e < 16; ++e) kv[e] = vv[e] = 0.f;
+        }
+        if (ch_ < D) {
+          const uint32_t cofs = (ch_ >> 6) * BT * 128 + (ch_ & 7) * 2;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t o = cofs + sw128_off(cc0 + e, (ch_ & 63) >> 3);
+            sts16(tdk + o, __bfloat16_as_ushort(__float2bfloat16_rn(kv[e] * p.scale)));
+            sts16(tdv + o, __bfloat16_as_ushort(__float2bfloat16_rn(vv[e])));
+          }
         }
       }
-    }
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (row == 0) {
-      const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
-      for (int cb = 0; cb < NCB; ++cb) {
-        tma_store_5d(&p.mdK, stage_q(0) + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-        tma_store_5d(&p.mdV, stage_q(0) + NCB * BT * 128 + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct,
-                     bh);
+      if (nchunks > 0) {
+        tc_fence_before();
+        mbar_arrive(&bar_acc_free);
+        ++nacc;
       }
-      tma_store_commit_and_wait();
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (row == 0) {
+        const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+        for (int cb = 0; cb < NCB; ++cb) {
+          tma_store_5d(&p.mdK, sP + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+          tma_store_5d(&p.mdV, sdS + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      store_pending = true;
+      if (row == 0) CTA_STAMP(6);
     }
-    if (row == 0) CTA_STAMP(6);
+    if (row == 0) bulk_wait_group<0>();  // the last stores are complete before the CTA exits
   } else if (warp < 8) {
     // ============================ dQ drain: TMEM dQ partial -> smem slices -> TMA bulk reduce-add
     // Each warp owns TMEM lane quadrant q4 (chunk rows 32 q4 .. +32), split into 32/R sub-boxes of R =
@@ -549,77 +590,64 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     uint8_t* slots = sm + SM::OFF_DQS + q4 * SM::DQ_SLOTS * 2048;
     const int R = p.dq_rows, nsub = 32 / R, per_half = 16 / R;
     int slot_i = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int qbuf = c & 1;
-      mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
-      tc_fence_after();
-      if (row == 0) BWD_TRACE(6, c);
-      const int ring = c & 3;
-      int dst = -1;  // lane k < nsub: first dQacc row of sub-box k
-      if (lane < nsub) {
-        const int r0 = q4 * 32 + lane * R, gi = r0 / SR, lr0 = r0 % SR;
-        if (gi < G && s_row0[ring][gi] >= 0 && lr0 < s_nk[ring][gi]) dst = s_row0[ring][gi] + lr0;
-      }
-      int dk[4];
+    int c = 0;
+    for (int j = j_first; j < j_end; ++j) {
+      const int nchunks = (nq_of(j) + G - 1) / G;
+      for (int cl = 0; cl < nchunks; ++cl, ++c) {
+        const int qbuf = c & 1;
+        mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
+        tc_fence_after();
+        if (row == 0) BWD_TRACE(6, c);
+        const int ring = c & 3;
+        int dst = -1;  // lane k < nsub: first dQacc row of sub-box k
+        if (lane < nsub) {
+          const int r0 = q4 * 32 + lane * R, gi = r0 / SR, lr0 = r0 % SR;
+          if (gi < G && s_row0[ring][gi] >= 0 && lr0 < s_nk[ring][gi]) dst = s_row0[ring][gi] + lr0;
+        }
+        int dk[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
-      const bool any = __any_sync(0xffffffffu, dst >= 0);
+        for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
+        const bool any = __any_sync(0xffffffffu, dst >= 0);
 #pragma unroll 1
-      for (int cs = 0; cs < D; cs += 32) {
-        float v[32];
-        const uint32_t tq = tdQ + qbuf * D + (static_cast<uint32_t>(q4 * 32) << 16) + cs;
-        tmem_ld16(tq, v);
-        tmem_ld16(tq + 16, v + 16);
-        tmem_wait_ld();
-        if (cs + 32 == D) {  // the whole partial is out of TMEM: dQ buffer free for chunk c+2
-          tc_fence_before();
-          mbar_arrive(&bar_dq_free[qbuf]);
-        }
-#ifdef BSA_DQ_RED_SLICES
-        if (cs < BSA_DQ_RED_SLICES * 32) {
-          const int sb = lane / R;
-          const int drow = __shfl_sync(0xffffffffu, dst, sb);
-          if (drow >= 0) {
-            float* gp = p.dQacc + static_cast<size_t>(drow + lane % R) * D + cs;
-#pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gp + e), "f"(v[e]), "f"(v[e + 1]),
-                           "f"(v[e + 2]), "f"(v[e + 3])
-                           : "memory");
+        for (int cs = 0; cs < D; cs += 32) {
+          float v[32];
+          const uint32_t tq = tdQ + qbuf * D + (static_cast<uint32_t>(q4 * 32) << 16) + cs;
+          tmem_ld16(tq, v);
+          tmem_ld16(tq + 16, v + 16);
+          tmem_wait_ld();
+          if (cs + 32 == D) {  // the whole partial is out of TMEM: dQ buffer free for chunk c+2
+            tc_fence_before();
+            mbar_arrive(&bar_dq_free[qbuf]);
           }
-          continue;
-        }
-#endif
-        if (any) {
-          const int s0 = slot_i, s1 = slot_i + 1 == SM::DQ_SLOTS ? 0 : slot_i + 1;
-          slot_i = s1 + 1 == SM::DQ_SLOTS ? 0 : s1 + 1;
-          // the two slots' previous reduces (issued >= 1 group ago) must have read them
-          if (lane == 0) bulk_wait_group_read<SM::DQ_SLOTS - 2>();
-          __syncwarp();
-          const int rr = lane & 15;
-          const uint32_t srow = smem_u32(slots + ((lane >> 4) ? s1 : s0) * 2048) + rr * 128;
+          if (any) {
+            const int s0 = slot_i, s1 = slot_i + 1 == SM::DQ_SLOTS ? 0 : slot_i + 1;
+            slot_i = s1 + 1 == SM::DQ_SLOTS ? 0 : s1 + 1;
+            // the two slots' previous reduces (issued >= 1 group ago) must have read them
+            if (lane == 0) bulk_wait_group_read<SM::DQ_SLOTS - 2>();
+            __syncwarp();
+            const int rr = lane & 15;
+            const uint32_t srow = smem_u32(slots + ((lane >> 4) ? s1 : s0) * 2048) + rr * 128;
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            sts128(srow + ((k ^ (rr & 7)) << 4), __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
-                   __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
+            for (int k = 0; k < 8; ++k)
+              sts128(srow + ((k ^ (rr & 7)) << 4), __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                     __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-#ifndef BSA_ABLATE_DQ_RED
-              uint8_t* slot = slots + (hf ? s1 : s0) * 2048;
-              for (int k = 0; k < per_half; ++k) {
-                const int sb = hf * per_half + k;
-                if (dk[sb] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 128, cs, dk[sb]);
+              for (int hf = 0; hf < 2; ++hf) {
+                uint8_t* slot = slots + (hf ? s1 : s0) * 2048;
+                for (int k = 0; k < per_half; ++k) {
+                  const int sb = hf * per_half + k;
+                  if (dk[sb] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 128, cs, dk[sb]);
+                }
+                bulk_commit_group();
               }
-#endif
-              bulk_commit_group();
             }
           }
         }
+        if (row == 0) BWD_TRACE(7, c);
       }
-      if (row == 0) BWD_TRACE(7, c);
     }
     if (lane == 0) bulk_wait_group<0>();
     if (row == 0) CTA_STAMP(7);
@@ -636,10 +664,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     unsigned sm_id;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    int nch = 0;
+    for (int j = j_first; j < j_end; ++j) nch += (nq_of(j) + G - 1) / G;
     e[0] = t_start;
     e[1] = t1;
     e[2] = sm_id;
-    e[3] = nchunks;
+    e[3] = nch;
   }
 #endif
 }
@@ -681,7 +711,7 @@ static cudaError_t run_bwd(const BwdParams& p, int BH, cudaStream_t st) {
   constexpr int smem = BwdSmem<D, BT>::TOTAL;
   cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_attn_bwd<D, BT><<<dim3(p.g.N, BH), BWD_THREADS, smem, st>>>(p);
+  k_attn_bwd<D, BT><<<dim3((p.g.N + BWD_NB - 1) / BWD_NB, BH), BWD_THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
 
