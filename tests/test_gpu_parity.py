@@ -27,6 +27,9 @@ CASES = [
     ("multi_tile", (8, 16, 24), (4, 4, 4), (0, 0, 0), 3, 128, 0.5, 0.1, 0.9, "video"),
     ("d64_bt64", (8, 12, 16), (4, 4, 4), (0, 0, 0), 2, 64, 0.5, 0.2, 0.9, "iid"),
     ("d128_bt32", (6, 10, 12), (2, 4, 4), (0, 0, 0), 2, 128, 0.5, 0.3, 0.9, "video"),
+    # k = 1, tau = .5: about one KV block per row, so most KV blocks have no admitting query block and the
+    # backward's two-blocks-per-CTA walk meets empty blocks next to full ones
+    ("sparse_k1", (8, 12, 16), (4, 4, 4), (0, 0, 0), 3, 128, 0.5, 0.02, 0.5, "iid"),
 ]
 
 
