@@ -238,7 +238,7 @@ def main():
     unit = tuple(int(x) for x in args.unit.split(",")) if args.unit else (0, 0, 0)
     g = bsa.Geometry(*cfg["grid"], *cfg["block"], *unit)
     B, Hh, d = cfg["B"], cfg["Hh"], cfg["d"]
-    from paper_2509_01085_b200.shard import head_range, problem_seed, reduce_step_stats
+    from paper_2509_01085_b200.shard import head_range, problem_seed, rank_time_spread, reduce_step_stats
     if args.shard == "heads":
         # strong scaling: the heads of ONE problem are split over the ranks (no collective on the path)
         seed = args.seed
@@ -309,6 +309,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
     t_max, f_sum = reduce_step_stats(total_ms, fl["total"] * args.steps, device=dev)
+    t_hi, t_lo = rank_time_spread(total_ms, device=dev)
     value = f_sum / (t_max * 1e-3) / 1e12
     ms_per_step = t_max / args.steps
     kernel_ms = {KERNEL_NAMES[i]: kms[i] / max(1, args.steps) for i in range(nk) if kcnt[i]}
@@ -438,6 +439,7 @@ def main():
                                        if args.shard == "ulysses" else
                                        f"bh-shard x{world} (independent problems, no collective)")},
             "gpu_launches": int(launches),
+            "rank_imbalance": t_hi / t_lo if t_lo > 0 else None,
             "clocks": clk.summary(),
             "roofline": roofline,
             "selection_hbm": {"bytes": sel_bytes, "ms": sel_ms, "achieved_gbs": sel_bytes / (sel_ms * 1e-3) / 1e9,

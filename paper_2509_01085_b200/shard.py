@@ -44,3 +44,16 @@ def reduce_step_stats(time_ms: float, flops: float, device=None, group=None) -> 
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(f, op=dist.ReduceOp.SUM, group=group)
     return float(t.item()), float(f.item())
+
+
+def rank_time_spread(time_ms: float, device=None, group=None) -> tuple[float, float]:
+    """(max, min) over ranks of a rank's timed region: max/min is the load imbalance of the head or problem
+    partition (per-head sparsity differs). Identity with one rank."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(time_ms), float(time_ms)
+    hi = torch.tensor([float(time_ms)], dtype=torch.float64, device=device)
+    lo = hi.clone()
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    return float(hi.item()), float(lo.item())

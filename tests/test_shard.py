@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2509_01085_b200.shard import head_range, problem_seed, reduce_step_stats
+from paper_2509_01085_b200.shard import head_range, problem_seed, rank_time_spread, reduce_step_stats
 
 
 def test_head_range_partitions():
@@ -39,7 +39,7 @@ def _worker(rank, world, port, out):
     try:
         t, f = reduce_step_stats(10.0 + rank, 100.0 * (rank + 1))
         h = head_range(40, world, rank)
-        out[rank] = (t, f, h, problem_seed(7, rank))
+        out[rank] = (t, f, h, problem_seed(7, rank), rank_time_spread(10.0 + 3 * rank))
     finally:
         dist.destroy_process_group()
 
@@ -55,6 +55,7 @@ def test_gloo_two_ranks():
     assert res[0][1] == res[1][1] == 300.0  # FLOPs summed
     assert res[0][2] == (0, 20) and res[1][2] == (20, 40)
     assert res[0][3] != res[1][3]
+    assert res[0][4] == res[1][4] == (13.0, 10.0)  # (max, min) over ranks
 
 
 def test_single_process_identity():
