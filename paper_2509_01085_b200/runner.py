@@ -142,3 +142,30 @@ class BSAAttention:
         dense = self.B * self.Hh * self.g.L * self.g.L
         return dict(pairs=P, fwd=4 * d * P, bwd=10 * d * P, total=14 * d * P, dense_total=14 * d * dense,
                     density=P / dense)
+
+
+class BSAStepGraph:
+    """One training step of a layer (selection, forward, backward on fixed input buffers) captured into a
+    CUDA graph: replay() re-runs every libbsa kernel of the step with one launch. Inputs are read from the
+    captured tensors, so refill them in place (copy_) between replays; outputs land in the layer's
+    O / dQ / dK / dV buffers. Library event timing (bsa_timing_enable) must be off while capturing."""
+
+    def __init__(self, layer: BSAAttention, Q, K, V, dO, warmup: int = 2):
+        self.layer, self.inputs = layer, (Q, K, V, dO)
+        dev = layer.device
+        self.stream = torch.cuda.Stream(dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):  # partition cache, lazy attributes, allocator state
+                layer.forward(Q, K, V)
+                layer.backward(dO)
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            layer.forward(Q, K, V)
+            layer.backward(dO)
+        torch.cuda.current_stream(dev).wait_stream(self.stream)
+
+    def replay(self):
+        self.graph.replay()
+        return self.layer.O, self.layer.dQ, self.layer.dK, self.layer.dV
