@@ -38,5 +38,9 @@ for u in range(U // 2, min(U, U // 2 + 14)):
     print(f"{u:4d} {t[0, u] - base:6d} {t[1, u] - base:7d}  [{gr}: {t[4 + o, u] - base:6d} {t[6 + o, u] - base:6d} "
           f"{t[7 + o, u] - base:6d} {t[5 + o, u] - base:6d}]  {t[2, u] - base:6d} {t[3, u] - base:6d}")
 d = lambda a, b: np.median((t[a, U // 4:U - 1] - t[b, U // 4:U - 1]))
+done = t[16, U // 4:U - 1]
+seen = np.array([t[7 + 8 * (u & 1), u + 2] for u in range(U // 4, U - 3)])
+print("PV(u) issued -> done (observer):", np.median(done[:len(seen)] - t[3, U // 4:U // 4 + len(seen)]),
+      " PV(u) done -> P buffer free seen by group (step u+2):", np.median(seen - done[:len(seen)]))
 print("median over steady steps (cycles): S ready->regs", [d(6 + 8 * k, 4 + 8 * k) for k in (0, 1)][0],
       " regs->P written", d(5, 6), d(13, 14), " pfree wait->P written", d(5, 7), " P written->PV issued", d(3, 2))
