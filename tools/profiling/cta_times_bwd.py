@@ -8,7 +8,7 @@ dO = bsa_gen.grad_output(0, (1, 12, g.L, 128)).cuda()
 layer = BSAAttention(g, 0.5, 0.1, 0.9, 1, 12, 128)
 layer.forward(Q, K, V); layer.backward(dO); torch.cuda.synchronize()
 L = bsa.lib()
-ncta = layer.N * 12
+ncta = ((layer.N + 1) // 2) * 12  # BWD_NB = 2 KV blocks per CTA
 buf = torch.zeros(ncta * 8, dtype=torch.int64, device="cuda")
 L.bsa_debug_trace_bwd(ctypes.c_void_p(buf.data_ptr()), -1)
 layer.backward(dO); torch.cuda.synchronize()
