@@ -378,14 +378,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           l_run *= alpha;
           m_run = mx;
         }
-        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // paired fp32 arithmetic (FFMA2 / FADD2): two columns per instruction for the scale-and-shift and
+        // the row sum (1.003 -> 0.992 ms at 32k)
+        float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_run, -m_run);
 #pragma unroll
-        for (int c = 0; c < BT; ++c) {  // one column in four on the FMA pipe, the rest on the MUFU
-          const float x = fmaf(sv[c], sl2, -m_run);
-          sv[c] = (c & 3) == 3 ? ex2_poly(x) : ex2(x);
-          sp[c & 7] += sv[c];
+        for (int c = 0; c < BT; c += 2) {  // one column in four on the FMA pipe, the rest on the MUFU
+          const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+          sv[c] = ex2(x.x);
+          sv[c + 1] = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
+          sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(sv[c], sv[c + 1]));
         }
-        l_run += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+        l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
       } else {
 #pragma unroll
         for (int c = 0; c < BT; ++c) sv[c] = 0.f;
