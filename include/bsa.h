@@ -112,6 +112,23 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
                          const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
                          int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream);
 
+/* Variant of bsa_select_kv_blocks with the reading of Eq.3/Eq.4 as a parameter (the north_star's
+ * "selection variants" row; C17, C28):
+ *   BSA_KV_TWO_STAGE     the library's reading (identical to bsa_select_kv_blocks): Eq.3's p thresholds the
+ *                        raw scores into candidates, Eq.4 admits the shortest prefix of their softmax
+ *                        reaching tau.
+ *   BSA_KV_UNIFIED_PROB  SPEC's unified_prob: Eq.3 is taken over the softmax-normalised row,
+ *                        p = mu + sigma Phi^-1(clamp(1 - k/N, 1/(2N), 1 - 1/(2N))) clamped to (0, 1] (no
+ *                        k = N bypass), and Eq.4 admits the shortest prefix (s desc, j asc) of ALL blocks
+ *                        whose probability mass reaches p; tau is ignored. thresh[row] = p.
+ * The paper's "fixed threshold" KV variant (Table 2) is BSA_KV_TWO_STAGE with k = N. Other
+ * arguments, ownership and errors as bsa_select_kv_blocks; an unknown mode is BSA_ERR_CONFIG. */
+enum bsa_kv_mode { BSA_KV_TWO_STAGE = 0, BSA_KV_UNIFIED_PROB = 1 };
+int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q,
+                            const double* q_pooled, const void* K, int32_t k, double tau, int32_t mode,
+                            int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num, int32_t* k2q_idx, double* thresh,
+                            void* ws, size_t ws_bytes, void* stream);
+
 /* a7 — sparse attention forward (Eq.5) + fill:
  *   for each kept query q of block i: O^s[q] = softmax(scale * q K_S^T) V_S over the tokens of the
  *   KV blocks admitted by i; O[kept] = O^s, O[pruned t] = O^s[donor(t)]; lse[q] = natural-log

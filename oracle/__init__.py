@@ -169,6 +169,25 @@ def select_kv(g: Geom, Q, K, k: int, tau: float):
     return select_kv_from_pooled(pool(g, Q), pool(g, K), k, tau)
 
 
+def select_kv_unified_from_pooled(Qc: np.ndarray, Kc: np.ndarray, k: int):
+    """SPEC's unified_prob reading (C28): Eq.3 over the softmax-normalised row gives
+    a probability-mass target p, Eq.4 admits the shortest prefix reaching it."""
+    Qc = np.ascontiguousarray(Qc, np.float64)
+    Kc = np.ascontiguousarray(Kc, np.float64)
+    BH, N, d = Qc.shape
+    num = np.zeros((BH, N), np.int32)
+    idx = np.zeros((BH, N, N), np.int32)
+    th = np.zeros((BH, N), np.float64)
+    mm = np.zeros((BH, N), np.float64)
+    lib().or_select_kv_unified(_I(N), _I(BH), _I(d), _p(Qc, _D), _p(Kc, _D), _I(k), _p(num, _I), _p(idx, _I),
+                               _p(th, _D), _p(mm, _D))
+    return dict(q2k_num=num, q2k_idx=idx, thresh=th, mass_margin=mm)
+
+
+def select_kv_unified(g: Geom, Q, K, k: int):
+    return select_kv_unified_from_pooled(pool(g, Q), pool(g, K), k)
+
+
 def attn_fwd(g: Geom, r: float, Q, K, V, kept_tok, donor, q2k_num, q2k_idx, scale: float):
     Q, K, V = _f64(Q), _f64(K), _f64(V)
     BH, L, d = Q.shape

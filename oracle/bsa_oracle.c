@@ -354,6 +354,73 @@ void or_select_kv(int N, int BH, int d, const double* Qc, const double* Kc, int 
     }
 }
 
+/* KV selection, SPEC's unified_prob reading of Eq.3/Eq.4 (the variant the north_star's
+ * "selection variants" row compares against, C28) for every (bh, row i):
+ *   s_j = Qc[i].Kc[j] / sqrt(d); m = max s; e_j = exp(s_j - m); E = sum_j e_j (ascending j);
+ *   prob_j = e_j / E; mu = mean_j prob_j, sigma = sqrt(mean_j (prob_j - mu)^2)           (Eq.3 on the
+ *   softmax-normalised row); z = Phi^-1(clamp(1 - k/N, 1/(2N), 1 - 1/(2N))) (no k = N bypass here);
+ *   p = mu + sigma z clamped to (0, 1] (p_floor = the smallest positive double);
+ *   order all j by (s desc, j asc); p >= 1: S = all; else the shortest prefix with cumulative
+ *   e >= p E (Eq.4 with p as the mass target, at least one block).
+ * thresh[row] = p; mass_margin[row] as in or_select_kv. */
+void or_select_kv_unified(int N, int BH, int d, const double* Qc, const double* Kc, int k, int* q2k_num,
+                          int* q2k_idx, double* thresh, double* mass_margin) {
+  double u = 1.0 - (double)k / (double)N;
+  double lo = 1.0 / (2.0 * N), hi = 1.0 - 1.0 / (2.0 * N);
+  if (u < lo) u = lo;
+  if (u > hi) u = hi;
+  const double z = or_normal_quantile(u);
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int bh = 0; bh < BH; ++bh)
+    for (int i = 0; i < N; ++i) {
+      size_t row = (size_t)bh * N + i;
+      double* s = (double*)malloc(sizeof(double) * N);
+      sj* C = (sj*)malloc(sizeof(sj) * N);
+      const double* q = Qc + row * d;
+      for (int j = 0; j < N; ++j) s[j] = dotd(q, Kc + ((size_t)bh * N + j) * d, d) / sqrt((double)d);
+      double m = s[0];
+      for (int j = 1; j < N; ++j) if (s[j] > m) m = s[j];
+      double E = 0.0;
+      for (int j = 0; j < N; ++j) E += exp(s[j] - m);
+      double mu = 0.0;
+      for (int j = 0; j < N; ++j) mu += exp(s[j] - m) / E;
+      mu /= (double)N;
+      double var = 0.0;
+      for (int j = 0; j < N; ++j) {
+        double dp = exp(s[j] - m) / E - mu;
+        var += dp * dp;
+      }
+      double sigma = sqrt(var / (double)N);
+      double p = mu + sigma * z;
+      if (p > 1.0) p = 1.0;
+      if (p <= 0.0) p = DBL_MIN;
+      if (thresh) thresh[row] = p;
+      for (int j = 0; j < N; ++j) { C[j].s = s[j]; C[j].j = j; }
+      qsort(C, N, sizeof(sj), sj_cmp);
+      int ell = N;
+      double mm = DBL_MAX;
+      if (p < 1.0) {
+        double cum = 0.0;
+        for (int t = 0; t < N; ++t) {
+          double prev = cum;
+          cum += exp(C[t].s - m);
+          if (cum >= p * E) {
+            ell = t + 1;
+            mm = t == 0 ? fabs(cum - p * E) / E : fmin(fabs(cum - p * E), fabs(prev - p * E)) / E;
+            break;
+          }
+        }
+      }
+      if (mass_margin) mass_margin[row] = mm;
+      int* out = q2k_idx + row * N;
+      for (int t = 0; t < ell; ++t) out[t] = C[t].j;
+      qsort(out, ell, sizeof(int), int_cmp);
+      for (int t = ell; t < N; ++t) out[t] = -1;
+      q2k_num[row] = ell;
+      free(s); free(C);
+    }
+}
+
 /* Sparse attention forward (a7, Eq.5, C19, C20, C23) for every kept query q of block i:
  * keys = tokens of the blocks in S_i (ascending block id, ascending token), l = scale * q.k,
  * O^s[q] = softmax(l) V, LSE[q] = max l + log sum exp(l - max l); then the fill (C9):

@@ -85,13 +85,15 @@ def lib() -> ctypes.CDLL:
         L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P,
                                    _P, _P, _S, _P]
         L.bsa_sp_relayout.argtypes = [_I, _I, _I, _I, _I, _I, _P, _P, _P]
+        L.bsa_select_kv_blocks_ex.argtypes = [gp, _I, _I, _I, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _P, _S, _P]
         L.bsa_launch_count.restype = ctypes.c_int64
         L.bsa_launch_count.argtypes = []
         L.bsa_timing_enable.argtypes = [_I]
         L.bsa_timing_read.argtypes = [_P, _P, _I]
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
-                  "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout"):
+                  "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
+                  "bsa_select_kv_blocks_ex"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -170,10 +172,14 @@ def bsa_select_queries(g: Geometry, r: float, Q: torch.Tensor, kept_off: torch.T
     return kept, donor, qp, qs
 
 
+KV_TWO_STAGE, KV_UNIFIED_PROB = 0, 1
+
+
 def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, tau: float, q_pooled=None,
-                         with_k2q: bool = True, with_thresh: bool = False):
+                         with_k2q: bool = True, with_thresh: bool = False, mode: int = KV_TWO_STAGE):
     """a4-a6 (Eq.3, Eq.4): returns q2k_num [B,Hh,N], q2k_idx [B,Hh,N,N] (row i valid up to q2k_num),
-    k2q_num, k2q_idx (or None), thresh (or None)."""
+    k2q_num, k2q_idx (or None), thresh (or None). mode = KV_UNIFIED_PROB selects SPEC's unified_prob reading
+    (bsa_select_kv_blocks_ex; tau unused)."""
     _need_cuda(Q, K, q_pooled)
     B, Hh, L, d = K.shape
     N = bsa_sizes(g, 1.0)[0]
@@ -185,9 +191,9 @@ def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, 
     th = torch.empty(B, Hh, N, dtype=torch.float64, device=dev) if with_thresh else None
     nb = bsa_workspace_bytes(OP_SELECT_KV, g, 1.0, B, Hh, d)
     ws = _ws(nb, dev)
-    _check(lib().bsa_select_kv_blocks(ctypes.byref(g.c()), B, Hh, d, _ptr(Q), _ptr(q_pooled), _ptr(K), int(k),
-                                      float(tau), _ptr(num), _ptr(idx), _ptr(knum), _ptr(kidx), _ptr(th), _ptr(ws),
-                                      nb, _stream(dev)), "bsa_select_kv_blocks")
+    _check(lib().bsa_select_kv_blocks_ex(ctypes.byref(g.c()), B, Hh, d, _ptr(Q), _ptr(q_pooled), _ptr(K), int(k),
+                                         float(tau), int(mode), _ptr(num), _ptr(idx), _ptr(knum), _ptr(kidx), _ptr(th),
+                                         _ptr(ws), nb, _stream(dev)), "bsa_select_kv_blocks_ex")
     return num, idx, knum, kidx, th
 
 

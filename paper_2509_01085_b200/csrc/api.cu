@@ -263,6 +263,15 @@ int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32
 int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q, const double* q_pooled,
                          const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
                          int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream) {
+  return bsa_select_kv_blocks_ex(g, B, Hh, d, Q, q_pooled, K, k, tau, BSA_KV_TWO_STAGE, q2k_num, q2k_idx, k2q_num,
+                                 k2q_idx, thresh, ws, ws_bytes, stream);
+}
+
+int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q,
+                            const double* q_pooled, const void* K, int32_t k, double tau, int32_t mode,
+                            int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num, int32_t* k2q_idx, double* thresh,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (mode != BSA_KV_TWO_STAGE && mode != BSA_KV_UNIFIED_PROB) return fail(BSA_ERR_CONFIG, "unknown KV mode %d", mode);
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_dims(B, Hh, d));
@@ -294,15 +303,16 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
   if (e == cudaSuccess)
     e = timed(BSA_K_SCORES, 1, st, [&] { return bsa::launch_scores(G.N, static_cast<int>(BH), d, Qc, Kc, S, st); });
   double z = 0.0;
-  if (k < G.N) {
+  if (k < G.N || mode == BSA_KV_UNIFIED_PROB) {  // unified_prob has no k = N bypass (C28)
     double u = 1.0 - static_cast<double>(k) / G.N;
     double lo = 1.0 / (2.0 * G.N), hi = 1.0 - 1.0 / (2.0 * G.N);
     u = u < lo ? lo : (u > hi ? hi : u);
     z = bsa::normal_quantile(u);
   }
   if (e == cudaSuccess)
-    e = timed(BSA_K_ADMIT, k < G.N ? 2 : 1, st, [&] {
-      return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, q2k_num, q2k_idx, thresh, bits, ovf, st);
+    e = timed(BSA_K_ADMIT, (k < G.N && mode == BSA_KV_TWO_STAGE) ? 2 : 1, st, [&] {
+      return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, mode == BSA_KV_UNIFIED_PROB ? 1 : 0, q2k_num,
+                               q2k_idx, thresh, bits, ovf, st);
     });
   if (e == cudaSuccess && k2q_num)
     e = timed(BSA_K_K2Q, 2, st, [&] {

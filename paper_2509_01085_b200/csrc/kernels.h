@@ -21,8 +21,8 @@ cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, 
 // a4 pooled block scores S[bh][i][j] = Qc[i].Kc[j] / sqrt(d)
 cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st);
 // a5+a6 threshold + admission per row; sets bit i of kvbits[bh][j] for every admitted (i, j)
-cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int* q2k_num, int* q2k_idx,
-                         double* thresh, uint32_t* qbits, int* ovf, cudaStream_t st);
+cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int unified, int* q2k_num,
+                         int* q2k_idx, double* thresh, uint32_t* qbits, int* ovf, cudaStream_t st);
 // transpose of the admission: k2q lists (ascending query blocks per KV block)
 cudaError_t launch_k2q(int N, int BH, const uint32_t* qbits, uint32_t* kvbits, int* k2q_num, int* k2q_idx,
                        cudaStream_t st);

@@ -497,7 +497,8 @@ __device__ __forceinline__ bool before(double sa, int ja, double sb, int jb) {
 // shared-memory capacity (and for k = N, where every row has N candidates). `rows` lists the rows
 // to do (NULL = all rows, row = blockIdx.x); CTAs past *nrows exit at once.
 __global__ void __launch_bounds__(256) k_admit_cta(int N, const double* __restrict__ S, int k, double z, double tau,
-                                                   const int* __restrict__ rows, const int* __restrict__ nrows,
+                                                   int unified, const int* __restrict__ rows,
+                                                   const int* __restrict__ nrows,
                                                    int* __restrict__ q2k_num, int* __restrict__ q2k_idx,
                                                    double* __restrict__ thresh, uint32_t* __restrict__ qbits) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -522,10 +523,36 @@ __global__ void __launch_bounds__(256) k_admit_cta(int N, const double* __restri
   part = 0.0;
   for (int j = threadIdx.x; j < N; j += blockDim.x) part += (s[j] - mu) * (s[j] - mu);
   const double sigma = sqrt(block_sum(part, red) / (double)N);
-  const bool all = (k >= N);  // C15 bypass
-  const double p = mu + sigma * z;
+  const bool all = unified || (k >= N);  // C15 bypass; unified_prob ranks every block
+  double p = mu + sigma * z;
+  if (unified) {
+    // SPEC's unified_prob (C28): Eq.3 over the softmax-normalised row, p becomes Eq.4's mass target
+    double mloc = -INFINITY;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) mloc = fmax(mloc, s[j]);
+    for (int o = 16; o > 0; o >>= 1) mloc = fmax(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mloc;
+    __syncthreads();
+    double mrow = -INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mrow = fmax(mrow, red[w]);
+    part = 0.0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) part += exp(s[j] - mrow);
+    const double E = block_sum(part, red);
+    part = 0.0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) part += exp(s[j] - mrow) / E;
+    const double mup = block_sum(part, red) / (double)N;
+    part = 0.0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const double dp = exp(s[j] - mrow) / E - mup;
+      part += dp * dp;
+    }
+    const double sgp = sqrt(block_sum(part, red) / (double)N);
+    p = fmin(1.0, mup + sgp * z);
+    if (p <= 0.0) p = DBL_MIN;
+    tau = p;  // the prefix rule below with p as the mass target (p >= 1: every block)
+  }
   if (threadIdx.x == 0) {
-    if (thresh) thresh[row] = all ? -INFINITY : p;
+    if (thresh) thresh[row] = unified ? p : (all ? -INFINITY : p);
     s_nc = 0;
   }
   __syncthreads();
@@ -807,16 +834,16 @@ __global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const
   }
 }
 
-cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int* q2k_num, int* q2k_idx,
-                         double* thresh, uint32_t* qbits, int* ovf, cudaStream_t st) {
+cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double tau, int unified, int* q2k_num,
+                         int* q2k_idx, double* thresh, uint32_t* qbits, int* ovf, cudaStream_t st) {
   int P2 = 1;
   while (P2 < N) P2 <<= 1;
   const size_t sm = static_cast<size_t>(N) * 8 + static_cast<size_t>(P2) * 12 + static_cast<size_t>(N) * 4;
   cudaError_t e = cudaFuncSetAttribute(k_admit_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   const int rows = N * BH;
-  if (k >= N) {  // C15: every row has all N candidates
-    k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, nullptr, nullptr, q2k_num, q2k_idx, thresh, qbits);
+  if (k >= N || unified) {  // C15 / unified_prob: every row has all N candidates
+    k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, unified, nullptr, nullptr, q2k_num, q2k_idx, thresh, qbits);
     return cudaGetLastError();
   }
   // ovf[0] = overflow count, ovf[1..] = overflow rows
@@ -829,7 +856,7 @@ cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double
   e = cudaFuncSetAttribute(k_admit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
   if (e != cudaSuccess) return e;
   k_admit_warp<<<grid, 256, wsm, st>>>(N, rows, S, k, z, tau, q2k_num, q2k_idx, thresh, qbits, ovf + 1, ovf);
-  k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, ovf + 1, ovf, q2k_num, q2k_idx, thresh, qbits);
+  k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, 0, ovf + 1, ovf, q2k_num, q2k_idx, thresh, qbits);
   return cudaGetLastError();
 }
 

@@ -21,7 +21,7 @@ from . import (OP_ATTN_BWD, OP_ATTN_FWD, OP_SELECT_KV, BSAError, Geometry, _chec
 
 class BSAAttention:
     def __init__(self, geom: Geometry, r: float, f: float, tau: float, B: int, Hh: int, d: int, device="cuda",
-                 scale=None, cache_partition: bool = True):
+                 scale=None, cache_partition: bool = True, kv_mode: int = 0):
         self.g, self.r, self.tau = geom, float(r), float(tau)
         self.B, self.Hh, self.d = B, Hh, d
         self.N, self.Lq, self.max_kept = bsa_sizes(geom, r)
@@ -29,6 +29,7 @@ class BSAAttention:
         self.scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
         self.device = torch.device(device)
         self.cache_partition = cache_partition
+        self.kv_mode = int(kv_mode)  # 0 = two_stage (the library's reading), 1 = unified_prob (C28)
         dev, N, Lq, L = self.device, self.N, self.Lq, geom.L
         i32 = dict(dtype=torch.int32, device=dev)
         self.block_off = torch.empty(N + 1, **i32)
@@ -77,10 +78,11 @@ class BSAAttention:
         _check(L.bsa_select_queries(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, _ptr(Q),
                                     _ptr(self.kept_off), _ptr(self.kept_tok), _ptr(self.donor), _ptr(self.q_pooled),
                                     _ptr(self.q_packed), st), "bsa_select_queries")
-        _check(L.bsa_select_kv_blocks(ctypes.byref(self._g), self.B, self.Hh, self.d, _ptr(Q), _ptr(self.q_pooled),
-                                      _ptr(K), self.k, self.tau, _ptr(self.q2k_num), _ptr(self.q2k_idx),
-                                      _ptr(self.k2q_num), _ptr(self.k2q_idx), None, _ptr(self.ws), self.ws.numel(),
-                                      st), "bsa_select_kv_blocks")
+        _check(L.bsa_select_kv_blocks_ex(ctypes.byref(self._g), self.B, self.Hh, self.d, _ptr(Q),
+                                         _ptr(self.q_pooled), _ptr(K), self.k, self.tau, self.kv_mode,
+                                         _ptr(self.q2k_num), _ptr(self.q2k_idx), _ptr(self.k2q_num),
+                                         _ptr(self.k2q_idx), None, _ptr(self.ws), self.ws.numel(), st),
+               "bsa_select_kv_blocks_ex")
 
     def attend(self, Q, K, V, out=None):
         """a7 (Eq.5) + fill into `out` (default: the layer's own O buffer) and self.lse."""

@@ -139,3 +139,34 @@ def test_errors_fail_loudly():
     Q = torch.zeros(1, 1, 256, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(bsa.BSAError):
         bsa.bsa_select_kv_blocks(g, Q, Q, 0, 0.9)
+
+
+@pytest.mark.parametrize("kind,f", [("video", 0.1), ("iid", 0.5), ("video", 1.0)])
+def test_unified_prob_selection_parity(kind, f):
+    """bsa_select_kv_blocks_ex(BSA_KV_UNIFIED_PROB) vs the oracle's unified_prob (C28): bit-exact q2k except
+    rows whose admission cut is a near-tie of the mass rule (C24), and k2q is its transpose."""
+    grid, Hh, d = (6, 10, 14), 2, 128
+    og = orc.Geom(*grid, 4, 4, 4)
+    g = bsa.Geometry(*grid)
+    Qc, Kc, _ = bsa_gen.make_inputs(kind, 0, 1, Hh, grid, d)
+    N = orc.sizes(og, 0.5)[0]
+    k = bsa.resolve_k(f, N)
+    num, idx, knum, kidx, th = bsa.bsa_select_kv_blocks(g, Qc.cuda(), Kc.cuda(), k, 0.9, with_thresh=True,
+                                                        mode=bsa.KV_UNIFIED_PROB)
+    torch.cuda.synchronize()
+    ref = orc.select_kv_unified(og, Qc[0].double().numpy(), Kc[0].double().numpy(), k)
+    num, idx, th = num[0].cpu().numpy(), idx[0].cpu().numpy(), th[0].cpu().numpy()
+    assert np.allclose(th, ref["thresh"], rtol=1e-9, atol=0)
+    bad = []
+    for h in range(Hh):
+        for i in range(N):
+            a = idx[h, i, :num[h, i]]
+            b = ref["q2k_idx"][h, i, :ref["q2k_num"][h, i]]
+            if not (num[h, i] == ref["q2k_num"][h, i] and np.array_equal(a, b)) and ref["mass_margin"][h, i] >= 1e-6:
+                bad.append((h, i))
+    assert not bad, bad[:5]
+    kn, ki = knum[0].cpu().numpy(), kidx[0].cpu().numpy()
+    for h in range(Hh):
+        for j in range(N):
+            want = [i for i in range(N) if j in set(idx[h, i, :num[h, i]].tolist())]
+            assert ki[h, j, :kn[h, j]].tolist() == want

@@ -499,3 +499,53 @@ def test_sparsity_composition():
     """Table 2: 1 - (1-0.5)(1-0.86) = 0.93."""
     e = GOLD["sparsity_composition"]
     assert abs(1 - (1 - e["s_q"]) * (1 - e["s_kv"]) - e["combined"]) < 1e-12
+
+
+# ---------------------------------------------------------------- unified_prob variant (SPEC S:322, S:337; C28)
+def _unified_reference_row(s, k):
+    """Independent statement of the unified_prob rule on one row (numpy softmax, statistics.NormalDist)."""
+    import statistics
+    N = len(s)
+    e = np.exp(s - s.max())
+    prob = e / e.sum()
+    mu, sigma = prob.mean(), prob.std()
+    u = min(max(1 - k / N, 1 / (2 * N)), 1 - 1 / (2 * N))
+    p = min(1.0, mu + sigma * statistics.NormalDist().inv_cdf(u))
+    return prob, max(p, np.finfo(float).tiny)
+
+
+def test_unified_uniform_row_admits_one_block():
+    # all scores equal: prob = 1/N, sigma = 0, p = 1/N -> exactly one block, the lowest id (S:317, C7)
+    N, d = 6, 4
+    Qc = np.ones((1, N, d))
+    Kc = np.tile(np.arange(1.0, d + 1.0), (1, N, 1))
+    out = orc.select_kv_unified_from_pooled(Qc, Kc, k=2)
+    assert (out["q2k_num"][0] == 1).all() and (out["q2k_idx"][0, :, 0] == 0).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_unified_brute_force_and_monotone(seed):
+    rng = np.random.default_rng(seed)
+    N, d = 7, 4
+    Qc = rng.normal(size=(1, N, d)) * 2.0
+    Kc = rng.normal(size=(1, N, d)) * 2.0
+    prev = None
+    for k in range(1, N + 1):
+        out = orc.select_kv_unified_from_pooled(Qc, Kc, k)
+        for i in range(N):
+            s = Qc[0, i] @ Kc[0].T / np.sqrt(d)
+            prob, p = _unified_reference_row(s, k)
+            assert abs(out["thresh"][0, i] - p) <= 1e-12
+            got = set(out["q2k_idx"][0, i, :out["q2k_num"][0, i]].tolist())
+            # brute force: minimum cardinality reaching mass p; among those the largest mass, then lowest ids
+            best = None
+            for m in range(1, N + 1):
+                cands = [c for c in itertools.combinations(range(N), m) if prob[list(c)].sum() >= p * (1 - 1e-12)]
+                if cands:
+                    best = max(cands, key=lambda c: (prob[list(c)].sum(), [-x for x in c]))
+                    break
+            assert got == set(best), (k, i, got, best)
+        num = out["q2k_num"][0]
+        if prev is not None:  # larger k: smaller quantile, smaller p, never more blocks (C28)
+            assert (num <= prev).all()
+        prev = num

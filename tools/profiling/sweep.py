@@ -66,6 +66,14 @@ def main():
                             "speedup_vs_dense": None, "ideal_speedup": 1.0 / fl["density"]})
                 del layer
                 torch.cuda.empty_cache()
+    # selection variant (C28): SPEC's unified_prob at the paper's end point (r = .5, k = ceil(.1 N))
+    layer = BSAAttention(g, 0.5, 0.1, 1.0, 1, Hh, d, kv_mode=1)
+    ms = time_layer(layer, Q, K, V, dO, args.steps, flush)
+    fl = layer.flops()
+    pts.append({"r": 0.5, "k_frac": 0.1, "k": layer.k, "tau": None, "kv_mode": "unified_prob", "ms": ms,
+                "tflops_executed": fl["total"] / (ms * 1e-3) / 1e12, "density": fl["density"],
+                "speedup_vs_dense": None, "ideal_speedup": 1.0 / fl["density"],
+                "kv_blocks_per_row": float(layer.q2k_num.float().mean().item())})
     for p in pts:
         p["speedup_vs_dense"] = dense_ms / p["ms"]
     print(json.dumps({"workload": "wan1.3b_32k sweep", "grid": grid, "heads": Hh, "d": d, "generator": args.kind,
