@@ -98,6 +98,17 @@ def test_validation_errors_before_any_launch():
                         ctypes.c_void_p(256), ctypes.c_void_p(256), None, 0, None)
     assert rc == 1 and b"ct*ch*cw" in L.bsa_last_error()
     assert L.bsa_strerror(4) == b"unsupported device (needs sm_100a)"
+    # selection variant: unknown KV mode -> CONFIG
+    rc = L.bsa_select_kv_blocks_ex(ctypes.byref(g.c()), 1, 2, 64, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 3,
+                                   0.9, 7, ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None,
+                                   ctypes.c_void_p(16), 1 << 30, None)
+    assert rc == 2 and b"KV mode" in L.bsa_last_error()
+    # Ulysses reorders: heads not divisible by P -> CONFIG; d not a multiple of 8 / misaligned -> INVALID_SHAPE
+    assert L.bsa_sp_relayout(0, 1, 16, 6, 128, 4, ctypes.c_void_p(256), ctypes.c_void_p(512), None) == 2
+    assert b"split" in L.bsa_last_error()
+    assert L.bsa_sp_relayout(0, 1, 16, 8, 12, 4, ctypes.c_void_p(256), ctypes.c_void_p(512), None) == 1
+    assert L.bsa_sp_relayout(0, 1, 16, 8, 128, 4, ctypes.c_void_p(258), ctypes.c_void_p(512), None) == 1
+    assert L.bsa_sp_relayout(9, 1, 16, 8, 128, 4, ctypes.c_void_p(256), ctypes.c_void_p(512), None) == 2
 
 
 def test_workspace_sizes_monotone():
