@@ -60,6 +60,7 @@ struct FwdParams {
   float scale_log2;  // scale * log2(e)
   bf16* O;
   float* lse;
+  unsigned long long clsmask[8];  // key-validity mask of each block-extent class (host-computed, C23)
 };
 
 constexpr int FWD_THREADS = 384;
@@ -128,6 +129,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   // CTA g_fwd_trace_cta writes slots [0, 8K); with BSA_TRACE_GLOBALTIMER also CTA +1 into [8K, 16K)
   const int my_cta = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
   unsigned long long* trace_buf = (my_cta == g_fwd_trace_cta) ? g_fwd_trace : nullptr;
+  // trace mode cta == -1: per-CTA [start, first S ready, last PV issued, end, smid, U] (globaltimer ns)
+  unsigned long long t_cta0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cta0));
+  if (g_fwd_trace_cta == -1) trace_buf = nullptr;
 #ifdef BSA_TRACE_GLOBALTIMER
   if (my_cta == g_fwd_trace_cta + 1 && g_fwd_trace != nullptr) trace_buf = g_fwd_trace + 8 * 1024;
 #endif
@@ -154,19 +159,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     s_koff[tid] = qb < g.N ? p.kept_off[qb] : 0;
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
-  if (tid < 8) {
-    const int et = (tid & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
-    const int eh = (tid & 2) ? g.H - (g.Nh - 1) * g.ch : g.ch;
-    const int ew = (tid & 1) ? g.W - (g.Nw - 1) * g.cw : g.cw;
-    uint64_t m = 0;
-#pragma unroll 1
-    for (int c = 0; c < BT; ++c) {
-      const int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
-      if (lt < et && lh < eh && lw < ew) m |= 1ull << c;
-    }
-    s_clsmask[tid] = m;
-  }
+  if (tid < 8) s_clsmask[tid] = p.clsmask[tid];
   __syncthreads();
+  // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the union build;
+  // written to TMEM after it (A operand of every S MMA)
+  uint4 qrow[D / 8];
+  if (warp < 4) {
+    const int row = tid, gi = row / SR, lr = row % SR;
+    const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
+    const uint4* src = reinterpret_cast<const uint4*>(p.Qs + (valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0) * D);
+#pragma unroll
+    for (int e = 0; e < D / 8; ++e) qrow[e] = valid ? src[e] : make_uint4(0, 0, 0, 0);
+  }
   // admission bitmap of each slot (q2k lists). The G lists are read concurrently (thread group gi
   // of FWD_THREADS / G threads per slot): one dependent global round trip instead of G.
   {
@@ -198,12 +202,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         if (lane >= o) incl += a;
       }
       int pos = cnt + incl - c;
+      // block coordinates of the word's first id once, then advanced by the bit gaps (no per-entry divisions)
+      int j = w * 32, bw = j % g.Nw, bhh = (j / g.Nw) % g.Nh, bt = j / (g.Nh * g.Nw);
+      const bool rt = g.T % g.ct, rh = g.H % g.ch, rw = g.W % g.cw;
       while (v) {
-        const int bit = __ffs(v) - 1, j = w * 32 + bit;
+        const int nj = w * 32 + __ffs(v) - 1;
+        bw += nj - j;
+        j = nj;
+        while (bw >= g.Nw) {
+          bw -= g.Nw;
+          if (++bhh == g.Nh) { bhh = 0; ++bt; }
+        }
         // entry = j | extent class << 12 (N <= 4096)
-        const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
-        const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
-                        (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
+        const int cls = (bt == g.Nt - 1 && rt ? 4 : 0) | (bhh == g.Nh - 1 && rh ? 2 : 0) | (bw == g.Nw - 1 && rw ? 1 : 0);
         ulist[pos++] = static_cast<uint16_t>(j | (cls << 12));
         v &= v - 1;
       }
@@ -216,6 +227,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   tc_fence_after();
   const uint32_t tbase = s_tmem;
   const int U = s_U;
+#ifdef BSA_TRACE
+  if (tid == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fwd_trace[8 * static_cast<size_t>(my_cta) + 6] = t;  // union list built
+  }
+#endif
   // Every role walks the union in the same rotated order: concurrent CTAs start at different KV blocks
   // instead of all streaming block 0, 1, 2, ... from the same L2 slices at once (order does not change
   // the result beyond fp32 summation order).
@@ -257,6 +275,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const uint64_t dV0 = umma_desc_sw128(smem_u32(sK + KV_BYTES), BT * 128, 1024);
     if (warp == W_QK) {
       mbar_wait(&bar_qt, 0);  // Q^s is in TMEM
+#ifdef BSA_TRACE
+      if (lane == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 7] = t;  // Q^s in TMEM
+      }
+#endif
       for (int v = 0; v < U; ++v) {
         const int s = v % FWD_STAGES, sb = v & 1;
         mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
@@ -299,6 +324,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         __syncwarp();
         FWD_TRACE(3, u);
       }
+#ifdef BSA_TRACE
+      if (leader && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 2] = t;
+      }
+#endif
       if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
       __syncwarp();
     }
@@ -315,14 +347,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const uint32_t* mybits = bits + (gi < G ? gi : 0) * NW;
     const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0;
     if (group == 0) {
-      // Q^s row -> TMEM (A operand of the S MMAs): bf16 pairs are already packed in memory order
-      const uint4* src = reinterpret_cast<const uint4*>(p.Qs + prow_idx * D);
+      // Q^s row (loaded in the prologue) -> TMEM (A operand of the S MMAs): bf16 pairs in memory order
 #pragma unroll
       for (int c0 = 0; c0 < D / 2; c0 += 16) {
         float w[16];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint4 v = valid ? src[c0 / 4 + e] : make_uint4(0, 0, 0, 0);
+          const uint4 v = qrow[c0 / 4 + e];
           w[4 * e] = __uint_as_float(v.x);
           w[4 * e + 1] = __uint_as_float(v.y);
           w[4 * e + 2] = __uint_as_float(v.z);
@@ -344,6 +375,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
       mbar_wait(&bar_s_full[group], ph);
       if (row == 0) FWD_TRACE(4 + 8 * group, u);
+#ifdef BSA_TRACE
+      if (u == 0 && row == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 1] = t;
+      }
+#endif
       tc_fence_after();
       float sv[BT];
 #pragma unroll
@@ -465,6 +503,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   tc_fence_before();
   __syncthreads();
   if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
+#ifdef BSA_TRACE
+  if (g_fwd_trace != nullptr && g_fwd_trace_cta == -1 && tid == 0) {
+    unsigned long long* e = g_fwd_trace + 8 * static_cast<size_t>(my_cta);
+    unsigned long long t1;
+    unsigned sm_id;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    e[0] = t_cta0;
+    e[3] = t1;
+    e[4] = sm_id;
+    e[5] = U;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------ host
@@ -551,6 +602,18 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.lse = a.lse;
   p.kv_img = a.kv_img;
   p.Qs = a.Qs;
+  for (int cls = 0; cls < 8; ++cls) {  // key-validity mask per block-extent class (ragged last block per axis)
+    const Geo& g = a.g;
+    const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
+    const int eh = (cls & 2) ? g.H - (g.Nh - 1) * g.ch : g.ch;
+    const int ew = (cls & 1) ? g.W - (g.Nw - 1) * g.cw : g.cw;
+    unsigned long long m = 0;
+    for (int c = 0; c < g.BT; ++c) {
+      const int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
+      if (lt < et && lh < eh && lw < ew) m |= 1ull << c;
+    }
+    p.clsmask[cls] = m;
+  }
   int ntiles = (a.g.N + p.G - 1) / p.G;
   if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_fwd<128, 32>(p, ntiles, a.BH, st);
