@@ -160,6 +160,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
   if (tid < 8) s_clsmask[tid] = p.clsmask[tid];
+  // The slots' q2k lists are read now, concurrently with kept_off: thread group gi (FWD_THREADS / G
+  // threads) holds list entries t, t + per, ... of slot gi in registers (the row has N allocated entries,
+  // so reading past q2k_num is safe; only the first q2k_num are used below).
+  constexpr int QPF = 2;  // list entries prefetched per thread
+  const int per = FWD_THREADS / G, pgi = tid / per, pt = tid % per;
+  const int pqb = tile * G + pgi;
+  const size_t prow = static_cast<size_t>(bh) * g.N + (pqb < g.N ? pqb : 0);
+  const int pnum = pqb < g.N ? p.q2k_num[prow] : 0;
+  int pj[QPF];
+#pragma unroll
+  for (int e = 0; e < QPF; ++e) pj[e] = (pt + e * per < g.N) ? p.q2k_idx[prow * g.N + pt + e * per] : 0;
   __syncthreads();
   // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the union build;
   // written to TMEM after it (A operand of every S MMA)
@@ -173,17 +184,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   // admission bitmap of each slot (q2k lists). The G lists are read concurrently (thread group gi
   // of FWD_THREADS / G threads per slot): one dependent global round trip instead of G.
-  {
-    const int per = FWD_THREADS / G, gi = tid / per, t = tid % per;
-    const int qb = gi < G ? s_qb[gi] : -1;
-    if (qb >= 0) {
-      const size_t row = static_cast<size_t>(bh) * g.N + qb;
-      const int num = p.q2k_num[row];
-      const int* idx = p.q2k_idx + row * g.N;
-      for (int a = t; a < num; a += per) {
-        const int j = idx[a];
-        atomicOr(&bits[gi * NW + (j >> 5)], 1u << (j & 31));
-      }
+  if (pqb < g.N) {
+#pragma unroll
+    for (int e = 0; e < QPF; ++e)
+      if (pt + e * per < pnum) atomicOr(&bits[pgi * NW + (pj[e] >> 5)], 1u << (pj[e] & 31));
+    const int* idx = p.q2k_idx + prow * g.N;
+    for (int a = pt + QPF * per; a < pnum; a += per) {  // long lists (more than QPF per thread)
+      const int j = idx[a];
+      atomicOr(&bits[pgi * NW + (j >> 5)], 1u << (j & 31));
     }
   }
   __syncthreads();
