@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
+  __shared__ uint32_t s_uword[MAX_N / 32];  // union bitmap words and their exclusive popcount prefix
+  __shared__ int s_upre[MAX_N / 32];
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
   // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
   // per-column index arithmetic (which, unrolled, bloated the softmax loop past the instruction cache).
@@ -160,6 +162,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
   if (tid < 8) s_clsmask[tid] = p.clsmask[tid];
+#ifdef BSA_TRACE
+#define FWD_CSTAMP(k)                                                                   \
+  do {                                                                                  \
+    if (tid == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {                  \
+      unsigned long long _t;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
+      g_fwd_trace[16 * static_cast<size_t>(my_cta) + (k)] = _t;                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define FWD_CSTAMP(k) \
+  do {                \
+  } while (0)
+#endif
+  FWD_CSTAMP(8);
   // The slots' q2k lists are read now, concurrently with kept_off: thread group gi (FWD_THREADS / G
   // threads) holds list entries t, t + per, ... of slot gi in registers (the row has N allocated entries,
   // so reading past q2k_num is safe; only the first q2k_num are used below).
@@ -172,6 +189,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll
   for (int e = 0; e < QPF; ++e) pj[e] = (pt + e * per < g.N) ? p.q2k_idx[prow * g.N + pt + e * per] : 0;
   __syncthreads();
+  FWD_CSTAMP(9);
   // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the union build;
   // written to TMEM after it (A operand of every S MMA)
   uint4 qrow[D / 8];
@@ -195,40 +213,42 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     }
   }
   __syncthreads();
-  // ascending union list (one warp)
+  FWD_CSTAMP(10);
+  // ascending union list in two parallel passes: warp 0 ORs the slots' bitmaps word by word (lane-parallel)
+  // and prefix-sums the word popcounts; then every warp emits whole words, lane b writing bit b's entry
+  // (entry = j | extent class << 12, N <= 4096; class bit 2/1/0 = ragged last block along t/h/w, C23)
   if (warp == 0) {
-    int cnt = 0;
+    int carry = 0;
     for (int w0 = 0; w0 < NW; w0 += 32) {
-      int w = w0 + lane;
+      const int w = w0 + lane;
       uint32_t v = 0u;
       if (w < NW)
         for (int gi = 0; gi < G; ++gi) v |= bits[gi * NW + w];
-      int c = __popc(v), incl = c;
+      const int c = __popc(v);
+      int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, incl, o);
+        const int a = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += a;
       }
-      int pos = cnt + incl - c;
-      // block coordinates of the word's first id once, then advanced by the bit gaps (no per-entry divisions)
-      int j = w * 32, bw = j % g.Nw, bhh = (j / g.Nw) % g.Nh, bt = j / (g.Nh * g.Nw);
-      const bool rt = g.T % g.ct, rh = g.H % g.ch, rw = g.W % g.cw;
-      while (v) {
-        const int nj = w * 32 + __ffs(v) - 1;
-        bw += nj - j;
-        j = nj;
-        while (bw >= g.Nw) {
-          bw -= g.Nw;
-          if (++bhh == g.Nh) { bhh = 0; ++bt; }
-        }
-        // entry = j | extent class << 12 (N <= 4096)
-        const int cls = (bt == g.Nt - 1 && rt ? 4 : 0) | (bhh == g.Nh - 1 && rh ? 2 : 0) | (bw == g.Nw - 1 && rw ? 1 : 0);
-        ulist[pos++] = static_cast<uint16_t>(j | (cls << 12));
-        v &= v - 1;
+      if (w < NW) {
+        s_uword[w] = v;
+        s_upre[w] = carry + incl - c;
       }
-      cnt += __shfl_sync(0xffffffffu, incl, 31);
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) s_U = cnt;
+    if (lane == 0) s_U = carry;
+  }
+  __syncthreads();
+  for (int w = warp; w < NW; w += FWD_THREADS / 32) {
+    const uint32_t v = s_uword[w];
+    if ((v >> lane) & 1u) {
+      const int jj = w * 32 + lane;
+      const int bt = jj / (g.Nh * g.Nw), bhh = (jj / g.Nw) % g.Nh, bw = jj % g.Nw;
+      const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
+                      (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
+      ulist[s_upre[w] + __popc(v & ((1u << lane) - 1u))] = static_cast<uint16_t>(jj | (cls << 12));
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -239,7 +259,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   if (tid == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_fwd_trace[8 * static_cast<size_t>(my_cta) + 6] = t;  // union list built
+    g_fwd_trace[16 * static_cast<size_t>(my_cta) + 6] = t;  // union list built
   }
 #endif
   // Every role walks the union in the same rotated order: concurrent CTAs start at different KV blocks
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       if (lane == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 7] = t;  // Q^s in TMEM
+        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 7] = t;  // Q^s in TMEM
       }
 #endif
       for (int v = 0; v < U; ++v) {
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       if (leader && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 2] = t;
+        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 2] = t;
       }
 #endif
       if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
@@ -387,7 +407,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       if (u == 0 && row == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[8 * static_cast<size_t>(my_cta) + 1] = t;
+        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 1] = t;
       }
 #endif
       tc_fence_after();
@@ -513,7 +533,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
 #ifdef BSA_TRACE
   if (g_fwd_trace != nullptr && g_fwd_trace_cta == -1 && tid == 0) {
-    unsigned long long* e = g_fwd_trace + 8 * static_cast<size_t>(my_cta);
+    unsigned long long* e = g_fwd_trace + 16 * static_cast<size_t>(my_cta);
     unsigned long long t1;
     unsigned sm_id;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));

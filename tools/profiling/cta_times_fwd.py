@@ -20,12 +20,12 @@ layer.forward(Q, K, V)
 torch.cuda.synchronize()
 L = bsa.lib()
 ncta = ((layer.N + 3) // 4) * 12
-buf = torch.zeros(ncta * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
 L.bsa_debug_trace_fwd(ctypes.c_void_p(buf.data_ptr()), -1)
 layer.attend(Q, K, V)
 torch.cuda.synchronize()
 L.bsa_debug_trace_fwd(None, 0)
-t = buf.view(ncta, 8).cpu().numpy().astype(np.int64)
+t = buf.view(ncta, 16).cpu().numpy().astype(np.int64)
 dur = (t[:, 3] - t[:, 0]) / 1e3
 U = t[:, 5]
 pro = (t[:, 1] - t[:, 0]) / 1e3
@@ -38,6 +38,8 @@ print(f"fit: dur = {coef[0]:.2f} us + {coef[1] * 1e3:.1f} ns * U   (mean U {U.me
 print(f"prologue (start -> first S ready) mean {pro.mean():.2f} us; epilogue (last PV issued -> end) mean {epi.mean():.2f} us")
 un = (t[:, 6] - t[:, 0]) / 1e3
 ql = (t[:, 7] - t[:, 0]) / 1e3
+st = lambda k: ((t[:, k] - t[:, 0]) / 1e3).mean()
+print(f"  start -> masks/zero issued {st(8):.2f} us; -> first barrier (kept_off, q2k loads) {st(9):.2f} us; -> bitmaps {st(10):.2f} us")
 print(f"  start -> union list built {un.mean():.2f} us; -> Q^s in TMEM {ql.mean():.2f} us; -> first S ready {pro.mean():.2f} us")
 ends = np.sort(t[:, 3] - t[:, 0].min()) / 1e3
 print(f"tail: last 148 CTAs end within {ends[-1] - ends[-148]:.1f} us")
