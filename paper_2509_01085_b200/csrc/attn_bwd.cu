@@ -162,7 +162,7 @@ __device__ int g_bwd_trace_cta = 0;
     if (g_bwd_trace != nullptr && g_bwd_trace_cta == -1) {                                             \
       unsigned long long _g;                                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                                          \
-      g_bwd_trace[8 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x) + (k)] = _g;           \
+      g_bwd_trace[16 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x) + (k)] = _g;           \
     }                                                                                                  \
   } while (0)
 #else
@@ -266,6 +266,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
+  // Producer: metadata of the CTA's first chunk (k2q_num -> k2q_idx -> kept_off, three dependent loads)
+  // fetched before the prologue barrier, so its latency overlaps the barrier init, TMEM allocation and
+  // stage zeroing.
+  int pf_j = -1, pf_qbl = 0, pf_nk = 0, pf_row0 = -1;
+  if (warp == 10) {  // W_PROD
+    for (int j = j_first; j < j_end; ++j) {
+      const int nq = nq_of(j), nch = (nq + G - 1) / G;
+      if (nch == 0) continue;
+      const int cc = rot_of(j, nch);
+      if (lane < min_i(G, nq - cc * G)) {
+        pf_qbl = p.k2q_idx[(static_cast<size_t>(bh) * g.N + j) * g.N + cc * G + lane];
+        const int ko = p.kept_off[pf_qbl];
+        pf_nk = p.kept_off[pf_qbl + 1] - ko;
+        pf_row0 = bh * p.Lq + ko;
+      }
+      pf_j = j;
+      break;
+    }
+  }
   if (tid == 0) {
     mbar_init(&bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
@@ -327,7 +346,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         const int cc = (cl + crot) % nchunks;
         const int nb = min_i(G, nq - cc * G);
         int row0 = -1, nk = 0, qbl = 0;
-        if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
+        if (c == 0 && j == pf_j) {  // prefetched before the prologue barrier
+          row0 = pf_row0;
+          nk = pf_nk;
+          qbl = pf_qbl;
+        } else if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
           qbl = qlist[cc * G + lane];
           int ko = p.kept_off[qbl];
           nk = p.kept_off[qbl + 1] - ko;
@@ -345,6 +368,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
           mbar_expect_tx(&bar_c_full[s], nb * (blk_bytes + ld_bytes));
           BWD_TRACE(0, c);
+          if (c == 0) CTA_STAMP(11);
           for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
             const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[ring][gi];
             bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + qimg * blk_bytes, blk_bytes, &bar_c_full[s]);
@@ -474,12 +498,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
         mbar_wait(&bar_c_full[s], (c >> 1) & 1);
+        if (row == 0 && c == 0) CTA_STAMP(8);
         const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
         const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
         const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
         mbar_wait(&bar_sd_full, c & 1);
         tc_fence_after();
         if (row == 0) BWD_TRACE(4, c);
+        if (row == 0 && c == 0) CTA_STAMP(9);
         // the whole S/dP row goes to registers first, so the TMEM buffer is handed back to the MMA warp
         // (S/dP of the next chunk) before any math
         float sv[BT], dp[BT];
@@ -659,7 +685,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 #ifdef BSA_TRACE
   // trace mode cta == -1: per-CTA [start, end, smid, nchunks] (globaltimer ns)
   if (g_bwd_trace != nullptr && g_bwd_trace_cta == -1 && tid == 0) {
-    unsigned long long* e = g_bwd_trace + 8 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x);
+    unsigned long long* e = g_bwd_trace + 16 * static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x);
     unsigned long long t1;
     unsigned sm_id;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));

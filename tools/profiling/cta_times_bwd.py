@@ -9,11 +9,11 @@ layer = BSAAttention(g, 0.5, 0.1, 0.9, 1, 12, 128)
 layer.forward(Q, K, V); layer.backward(dO); torch.cuda.synchronize()
 L = bsa.lib()
 ncta = ((layer.N + 1) // 2) * 12  # BWD_NB = 2 KV blocks per CTA
-buf = torch.zeros(ncta * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
 L.bsa_debug_trace_bwd(ctypes.c_void_p(buf.data_ptr()), -1)
 layer.backward(dO); torch.cuda.synchronize()
 L.bsa_debug_trace_bwd(None, 0)
-t = buf.view(ncta, 8).cpu().numpy().astype(np.int64)
+t = buf.view(ncta, 16).cpu().numpy().astype(np.int64)
 t0 = t[:, 0].min(); span = t[:, 1].max() - t0
 dur = t[:, 1] - t[:, 0]
 nch = t[:, 3]
@@ -35,8 +35,8 @@ print(f"inter-CTA gap per SM: median {np.median(gaps)/1e3:.2f} us, mean {gaps.me
 ends = np.sort(t[:, 1] - t0)
 print(f"tail: last 148 CTAs end within {(ends[-1]-ends[-148])/1e3:.1f} us")
 
-names = {4: "prologue done", 5: "softmax loop done", 6: "dK/dV stored", 7: "drain done", 1: "end"}
-for k in (4, 5, 6, 7, 1):
+names = {11: "first stage issued", 8: "first chunk landed", 9: "first S/dP ready", 4: "prologue done", 5: "softmax loop done", 6: "dK/dV stored", 7: "drain done", 1: "end"}
+for k in (4, 11, 8, 9, 5, 6, 7, 1):
     d = (t[:, k] - t[:, 0]) / 1e3
     m = nch == 12
     print(f"  t[{names[k]:18s}] - start: mean {d.mean():7.2f} us   (nchunks=12: {d[m].mean():7.2f})")
