@@ -330,17 +330,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int nq = nq_of(j), nchunks = (nq + G - 1) / G, crot = rot_of(j, nchunks);
       if (nchunks == 0) continue;
       const int* qlist = p.k2q_idx + (static_cast<size_t>(bh) * g.N + j) * g.N;
-      if (lane == 0) {
-        // K/V of the previous block are read until its last MMA: bar_acc of that block
-        if (nacc > 0) mbar_wait(&bar_acc, (nacc - 1) & 1);
-        int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
-        mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
-        for (int cb = 0; cb < NCB; ++cb) {
-          tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-          tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-        }
-      }
-      ++nacc;
+      ++nacc;  // (the block's K/V tiles are loaded by the S/dP issuer, their first consumer)
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
         const int cc = (cl + crot) % nchunks;
@@ -402,6 +392,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int nchunks = (nq_of(j) + G - 1) / G;
       if (nchunks == 0) continue;
       if (warp == W_SD) {
+        // K/V tiles of the block: the previous block's are read until its last MMA (bar_acc)
+        if (leader) {
+          if (nacc > 0) mbar_wait(&bar_acc, (nacc - 1) & 1);
+          const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+          mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
+          for (int cb = 0; cb < NCB; ++cb) {
+            tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+            tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+          }
+        }
+        __syncwarp();
         mbar_wait(&bar_kv, nacc & 1);
         // S/dP(v) = Q^s K^T, dO^s V^T of chunk v, issued as soon as its stage landed and the softmax
         // warps hold S/dP(v-1) in registers (single TMEM buffer)
