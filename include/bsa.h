@@ -11,9 +11,15 @@
  *   bsa_attn_bwd          its gradient (semantics in DESIGN.md reading C10)
  *
  * Conventions (all calls):
- *  - Tensors Q, K, V, O, dO, dQ, dK, dV are bf16, contiguous [B, Hh, L, d] (d fastest), tokens in
- *    raster order n = t*H*W + h*W + w. d must be 64 or 128. Device pointers must be 16-byte
- *    aligned. Index arrays are int32, device memory.
+ *  - Tensors Q, K, V, O, dO, dQ, dK, dV are bf16 [B, Hh, L, d] passed as a bsa_tensor: a device pointer and
+ *    element strides (sb, sh, sl) of the batch, head and token dimensions; the d channels of a row are
+ *    contiguous. The problem statement is per head, Q, K, V in R^{L x d}, so any layout whose
+ *    rows of one head are evenly spaced works: contiguous [B, Hh, L, d] (sb = Hh L d, sh = L d, sl = d), a
+ *    model's [B, L, Hh, d] (sb = L Hh d, sh = d, sl = Hh d), or Q/K/V views of a fused [B, L, 3, Hh, d]
+ *    projection (sl = 3 Hh d). Tokens are in raster order n = t*H*W + h*W + w. d must be 64 or 128;
+ *    pointers must be 16-byte aligned and strides positive multiples of 8 elements with sl >= d
+ *    (BSA_ERR_INVALID_SHAPE otherwise). Output tensors must not overlap any input or each other.
+ *    Index arrays are int32, device memory; q_pooled / q_packed / lse and all selection arrays are packed.
  *  - Ownership: the caller allocates every buffer (device unless stated) and passes a CUDA stream
  *    (cudaStream_t, passed as void*; NULL = legacy default stream). The library never allocates,
  *    frees or synchronises; every call only enqueues work on `stream` and returns. Calls are
@@ -23,8 +29,9 @@
  *  - Geometry: grid (T,H,W), block (ct,ch,cw), query-selection unit (ut,uh,uw) (the paper's window
  *    (w_t,w_h,w_w)); ut=uh=uw=0 means unit = block (block-centre selection, the north_star
  *    default). Grids need not be divisible by the block: edge blocks are truncated (reading C1).
- *    Block ids are row-major over (ceil(T/ct), ceil(H/ch), ceil(W/cw)). The attention kernels
- *    require ct*ch*cw in {32, 64} and N = number of blocks <= 4096.
+ *    Block ids are row-major over (ceil(T/ct), ceil(H/ch), ceil(W/cw)). KV selection and the attention
+ *    kernels require N = number of blocks <= 4096 (BSA_ERR_INVALID_SHAPE otherwise); the attention kernels
+ *    also require ct*ch*cw in {32, 64}.
  *  - r in (0,1] is the query keep ratio (Eq.2's retention ratio); a unit of n tokens keeps
  *    clamp(ceil(r*n - 1e-9), 1, n) queries (reading C6). k in [1,N] is Eq.3's key count (k = N turns
  *    the threshold off, reading C15); tau in (0,1] is Eq.4's cumulative-mass target (reading C17).
@@ -48,6 +55,12 @@ enum bsa_status {
   BSA_ERR_CUDA = 5                 /* a CUDA launch failed; message carries cudaGetErrorString */
 };
 
+/* A bf16 [B, Hh, L, d] tensor: element (b, h, n, c) at ((bf16*)ptr)[b*sb + h*sh + n*sl + c]. */
+typedef struct bsa_tensor {
+  void* ptr;
+  int64_t sb, sh, sl;
+} bsa_tensor;
+
 typedef struct bsa_geom {
   int32_t T, H, W;    /* latent token grid */
   int32_t ct, ch, cw; /* cuboid block (C_t, C_h, C_w) */
@@ -61,6 +74,16 @@ int bsa_version(void);
 const char* bsa_strerror(int status);
 /* Message of the last error raised on the calling thread ("" if none). */
 const char* bsa_last_error(void);
+
+/* Host-only: Eq.3's integer key count from a fraction, k = clamp(ceil(f*N - 1e-9), 1, N) (reading C6: plain fp
+ * ceil is wrong, e.g. 0.07*100 = 7.000000000000001). f in (0,1], N >= 1; errors CONFIG / INVALID_SHAPE. */
+int bsa_resolve_k(double f, int32_t N, int32_t* k);
+
+/* Host-only: the z = U(1 - k/n) of Eq.3 that bsa_select_kv_blocks uses for (k, N): the standard
+ * normal quantile (reading C14) of 1 - k/N clamped to [1/(2N), 1 - 1/(2N)] (Acklam's approximation refined by
+ * two Halley steps on erfc). k in [1, N]; for k == N the threshold itself is bypassed (reading C15) but z is
+ * still defined (it is what BSA_KV_UNIFIED_PROB uses). */
+int bsa_kv_quantile(int32_t k, int32_t N, double* z);
 
 /* Host-only sizes for allocation: N blocks, Lq kept queries per (b,h) (= sum over blocks of the
  * per-block kept counts, which depend only on geometry and r), and the largest per-block kept
@@ -90,7 +113,7 @@ int bsa_block_partition(const bsa_geom* g, double r, int32_t* block_off, int32_t
  *   donor      [B,Hh,L]  out  donor token of every token (itself if kept)
  *   q_pooled   [B,Hh,N,d] out fp64 block means of Q; may be NULL
  *   q_packed   [B,Hh,Lq,d] out bf16 rows of the kept queries in kept_tok order (Q^s); may be NULL */
-int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q,
+int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q,
                        const int32_t* kept_off, int32_t* kept_tok, int32_t* donor, double* q_pooled, void* q_packed,
                        void* stream);
 
@@ -100,7 +123,7 @@ int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32
  *          (empty -> {argmax}); k == N: C = all blocks.
  *   Admit the shortest prefix of C ordered by (s desc, j asc) whose exp(s - max) mass reaches
  *   tau * total (tau >= 1: all of C).
- *   q_pooled  [B,Hh,N,d] fp64 from bsa_select_queries, or NULL (then Q is pooled here)
+ *   q_pooled  [B,Hh,N,d] fp64 from bsa_select_queries, or NULL (then Q is pooled here; else Q.ptr may be NULL)
  *   q2k_num   [B,Hh,N]   out |S_i|;   q2k_idx [B,Hh,N,N] out S_i ascending in row i's first q2k_num
  *                         entries (the rest is left unwritten)
  *   k2q_num   [B,Hh,N]   out number of query blocks admitting KV block j; k2q_idx [B,Hh,N,N] out
@@ -108,8 +131,8 @@ int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32
  *                         may be NULL
  *   thresh    [B,Hh,N]   out p per row (-inf when k == N); may be NULL
  *   ws/ws_bytes          device workspace of at least bsa_workspace_bytes(BSA_OP_SELECT_KV, ...) */
-int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q, const double* q_pooled,
-                         const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
+int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, const double* q_pooled,
+                         bsa_tensor K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
                          int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream);
 
 /* Variant of bsa_select_kv_blocks with the reading of Eq.3/Eq.4 as a parameter (the north_star's
@@ -124,8 +147,8 @@ int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, co
  * The paper's "fixed threshold" KV variant (Table 2) is BSA_KV_TWO_STAGE with k = N. Other
  * arguments, ownership and errors as bsa_select_kv_blocks; an unknown mode is BSA_ERR_CONFIG. */
 enum bsa_kv_mode { BSA_KV_TWO_STAGE = 0, BSA_KV_UNIFIED_PROB = 1 };
-int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q,
-                            const double* q_pooled, const void* K, int32_t k, double tau, int32_t mode,
+int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q,
+                            const double* q_pooled, bsa_tensor K, int32_t k, double tau, int32_t mode,
                             int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num, int32_t* k2q_idx, double* thresh,
                             void* ws, size_t ws_bytes, void* stream);
 
@@ -134,11 +157,12 @@ int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d,
  *   KV blocks admitted by i; O[kept] = O^s, O[pruned t] = O^s[donor(t)]; lse[q] = natural-log
  *   log-sum-exp of the scaled logits (packed order). bf16 tcgen05 MMAs, fp32 accumulation and
  *   online softmax.
- *   q_packed [B,Hh,Lq,d] Q^s from bsa_select_queries, or NULL (then gathered into ws)
- *   O        [B,Hh,L,d] out;  lse [B,Hh,Lq] out fp32;  scale > 0 finite (1/sqrt(d) in the paper) */
-int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
-                 const void* V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
-                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, void* O,
+ *   q_packed [B,Hh,Lq,d] Q^s from bsa_select_queries, or NULL (then gathered from Q into ws; Q.ptr may be NULL
+ *            when q_packed is given)
+ *   O        [B,Hh,L,d] out (strided);  lse [B,Hh,Lq] out fp32;  scale > 0 finite (1/sqrt(d)) */
+int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
+                 bsa_tensor V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
+                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, bsa_tensor O,
                  float* lse, void* ws, size_t ws_bytes, void* stream);
 
 /* a8 — backward of bsa_attn_fwd with the selection held fixed (reading C10):
@@ -146,11 +170,13 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
  *   dV, dK accumulate over admitting query blocks; dQ[kept] = scale * dS K, dQ[pruned] = 0;
  *   tokens of KV blocks no query block admitted get dK = dV = 0.
  *   O and lse are the outputs of bsa_attn_fwd; k2q_* from bsa_select_kv_blocks.
- *   dQ, dK, dV [B,Hh,L,d] out bf16. dQ accumulates through fp32 atomics (order not deterministic). */
-int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
-                 const void* V, const void* O, const void* dO, const void* q_packed, const int32_t* kept_off,
+ *   dQ, dK, dV [B,Hh,L,d] out bf16 (strided; Q.ptr may be NULL when q_packed is given). dQ accumulates in an fp32 workspace through L2 bulk tensor reduce-adds
+ *   (cp.reduce.async.bulk.tensor), one per (query row block, admitted KV block): the summation order is
+ *   not deterministic, so dQ may differ run to run in the last fp32 bits before the bf16 rounding. */
+int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
+                 bsa_tensor V, bsa_tensor O, bsa_tensor dO, const void* q_packed, const int32_t* kept_off,
                  const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
-                 const float* lse, float scale, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                 const float* lse, float scale, bsa_tensor dQ, bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes,
                  void* stream);
 
 /* ---------------------------------------------------------------- Ulysses sequence parallelism
@@ -163,9 +189,17 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
  *   BSA_SP_RECV_TO_HEADS  src [P][B][Hp][Ls][d]  -> dst [B][Hp][P*Ls][d]   (BSA layout, whole sequence)
  *   BSA_SP_HEADS_TO_SEND  src [B][Hp][P*Ls][d]   -> dst [P][B][Hp][Ls][d]  (chunk s: sequence chunk s)
  *   BSA_SP_RECV_TO_SEQ    src [P][B][Hp][Ls][d]  -> dst [B][Ls][Hh][d]     (back to the model layout)
+ * Token-major variants (B = 1: the exchange then needs no reorder on the BSA side at all, because the received
+ * [P][Ls][Hp][d] = [L][Hp][d] buffer is a strided [1, Hp, L, d] bsa_tensor (sh = d, sl = Hp d), and BSA's outputs
+ * written in that layout are already the send buffer of the return exchange):
+ *   BSA_SP_SEQ_TO_SEND_T  src [B][Ls][Hh][d]     -> dst [P][B][Ls][Hp][d]  (chunk p: head group p)
+ *   BSA_SP_RECV_T_TO_SEQ  src [P][B][Ls][Hp][d]  -> dst [B][Ls][Hh][d]     (back to the model layout)
  * Errors: BSA_ERR_INVALID_SHAPE for non-positive sizes, d % 8 != 0 or misaligned pointers;
  * BSA_ERR_CONFIG for Hh % P != 0 or an unknown mode. */
-enum bsa_sp_mode { BSA_SP_SEQ_TO_SEND = 0, BSA_SP_RECV_TO_HEADS = 1, BSA_SP_HEADS_TO_SEND = 2, BSA_SP_RECV_TO_SEQ = 3 };
+enum bsa_sp_mode {
+  BSA_SP_SEQ_TO_SEND = 0, BSA_SP_RECV_TO_HEADS = 1, BSA_SP_HEADS_TO_SEND = 2, BSA_SP_RECV_TO_SEQ = 3,
+  BSA_SP_SEQ_TO_SEND_T = 4, BSA_SP_RECV_T_TO_SEQ = 5
+};
 int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int32_t P, const void* src, void* dst,
                     void* stream);
 

@@ -18,6 +18,7 @@ import torch
 __all__ = [
     "BSAError", "Geometry", "lib", "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
     "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout", "Selection", "select", "resolve_k",
+    "kv_quantile", "tensor_desc",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +33,23 @@ class BSAError(RuntimeError):
 
 class _CGeom(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("T", "H", "W", "ct", "ch", "cw", "ut", "uh", "uw")]
+
+
+class _CTensor(ctypes.Structure):
+    """include/bsa.h bsa_tensor: bf16 [B, Hh, L, d], element (b, h, n, c) at ptr[b sb + h sh + n sl + c]."""
+    _fields_ = [("ptr", ctypes.c_void_p), ("sb", ctypes.c_int64), ("sh", ctypes.c_int64), ("sl", ctypes.c_int64)]
+
+
+def tensor_desc(t) -> _CTensor:
+    """bsa_tensor of a bf16 CUDA tensor shaped [B, Hh, L, d] with contiguous channels (any batch / head / token
+    strides, e.g. x.transpose(1, 2) of a model's [B, L, Hh, d]); a NULL descriptor for None. Marshalling only."""
+    if t is None:
+        return _CTensor(None, 0, 0, 0)
+    if t.dim() != 4 or t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise BSAError(f"expected a bf16 CUDA tensor [B, Hh, L, d], got {tuple(t.shape)} {t.dtype} {t.device}")
+    if t.stride(3) != 1:
+        raise BSAError("the d channels of each row must be contiguous (stride(-1) == 1)")
+    return _CTensor(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
 
 
 @dataclass(frozen=True)
@@ -72,6 +90,7 @@ def lib() -> ctypes.CDLL:
             raise BSAError(f"{LIB_PATH} is missing: run `python -m paper_2509_01085_b200.build` (no fallback path)")
         L = ctypes.CDLL(LIB_PATH)
         gp = ctypes.POINTER(_CGeom)
+        _T = _CTensor
         L.bsa_version.restype = _I
         L.bsa_strerror.restype = ctypes.c_char_p
         L.bsa_strerror.argtypes = [_I]
@@ -79,13 +98,15 @@ def lib() -> ctypes.CDLL:
         L.bsa_sizes.argtypes = [gp, _D, _P, _P, _P]
         L.bsa_workspace_bytes.argtypes = [_I, gp, _D, _I, _I, _I, ctypes.POINTER(_S)]
         L.bsa_block_partition.argtypes = [gp, _D, _P, _P, _P, _P, _P]
-        L.bsa_select_queries.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]
-        L.bsa_select_kv_blocks.argtypes = [gp, _I, _I, _I, _P, _P, _P, _I, _D, _P, _P, _P, _P, _P, _P, _S, _P]
-        L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _S, _P]
-        L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _P,
-                                   _P, _P, _S, _P]
+        L.bsa_select_queries.argtypes = [gp, _D, _I, _I, _I, _T, _P, _P, _P, _P, _P, _P]
+        L.bsa_select_kv_blocks.argtypes = [gp, _I, _I, _I, _T, _P, _T, _I, _D, _P, _P, _P, _P, _P, _P, _S, _P]
+        L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _P, _P, _P, _P, _P, _P, _F, _T, _P, _P, _S, _P]
+        L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _T, _T, _P, _P, _P, _P, _P, _P, _P, _F, _T, _T,
+                                   _T, _P, _S, _P]
         L.bsa_sp_relayout.argtypes = [_I, _I, _I, _I, _I, _I, _P, _P, _P]
-        L.bsa_select_kv_blocks_ex.argtypes = [gp, _I, _I, _I, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _P, _S, _P]
+        L.bsa_select_kv_blocks_ex.argtypes = [gp, _I, _I, _I, _T, _P, _T, _I, _D, _I, _P, _P, _P, _P, _P, _P, _S, _P]
+        L.bsa_resolve_k.argtypes = [_D, _I, _P]
+        L.bsa_kv_quantile.argtypes = [_I, _I, _P]
         L.bsa_launch_count.restype = ctypes.c_int64
         L.bsa_launch_count.argtypes = []
         L.bsa_timing_enable.argtypes = [_I]
@@ -93,7 +114,7 @@ def lib() -> ctypes.CDLL:
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
-                  "bsa_select_kv_blocks_ex"):
+                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -119,6 +140,21 @@ def _need_cuda(*ts):
     for t in ts:
         if t is not None and (not t.is_cuda or not t.is_contiguous()):
             raise BSAError("libbsa expects contiguous CUDA tensors")
+
+
+def _need_rows(shape, *ts):
+    """Strided [B, Hh, L, d] bf16 operands: shape and channel contiguity (strides are checked by the library)."""
+    for t in ts:
+        if t is not None and (tuple(t.shape) != tuple(shape) or t.dtype != torch.bfloat16 or not t.is_cuda
+                              or t.stride(-1) != 1):
+            raise BSAError(f"expected a bf16 CUDA [B, Hh, L, d] = {tuple(shape)} tensor with contiguous channels, got "
+                           f"{tuple(t.shape)} {t.dtype} stride {t.stride()}")
+
+
+def _need_i32(name, t, shape):
+    if t is None or tuple(t.shape) != tuple(shape) or t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+        got = None if t is None else (tuple(t.shape), t.dtype)
+        raise BSAError(f"{name}: expected a contiguous int32 CUDA tensor of shape {tuple(shape)}, got {got}")
 
 
 def bsa_sizes(g: Geometry, r: float):
@@ -159,15 +195,16 @@ def bsa_select_queries(g: Geometry, r: float, Q: torch.Tensor, kept_off: torch.T
                        packed: bool = True):
     """a2+a3 (Eq.2): returns kept_tok [B,Hh,Lq], donor [B,Hh,L], q_pooled [B,Hh,N,d] fp64 or None,
     q_packed [B,Hh,Lq,d] bf16 or None."""
-    _need_cuda(Q, kept_off)
     B, Hh, L, d = Q.shape
+    _need_rows((B, Hh, g.L, d), Q)
     N, Lq, _ = bsa_sizes(g, r)
+    _need_i32("kept_off", kept_off, (N + 1,))
     dev = Q.device
     kept = torch.empty(B, Hh, Lq, dtype=torch.int32, device=dev)
     donor = torch.empty(B, Hh, L, dtype=torch.int32, device=dev)
     qp = torch.empty(B, Hh, N, d, dtype=torch.float64, device=dev) if pooled else None
     qs = torch.empty(B, Hh, Lq, d, dtype=torch.bfloat16, device=dev) if packed else None
-    _check(lib().bsa_select_queries(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(kept_off), _ptr(kept), _ptr(donor),
+    _check(lib().bsa_select_queries(ctypes.byref(g.c()), r, B, Hh, d, tensor_desc(Q), _ptr(kept_off), _ptr(kept), _ptr(donor),
                                     _ptr(qp), _ptr(qs), _stream(dev)), "bsa_select_queries")
     return kept, donor, qp, qs
 
@@ -180,8 +217,9 @@ def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, 
     """a4-a6 (Eq.3, Eq.4): returns q2k_num [B,Hh,N], q2k_idx [B,Hh,N,N] (row i valid up to q2k_num),
     k2q_num, k2q_idx (or None), thresh (or None). mode = KV_UNIFIED_PROB selects SPEC's unified_prob reading
     (bsa_select_kv_blocks_ex; tau unused)."""
-    _need_cuda(Q, K, q_pooled)
     B, Hh, L, d = K.shape
+    _need_rows((B, Hh, g.L, d), Q, K)
+    _need_cuda(q_pooled)
     N = bsa_sizes(g, 1.0)[0]
     dev = K.device
     num = torch.empty(B, Hh, N, dtype=torch.int32, device=dev)
@@ -191,7 +229,7 @@ def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, 
     th = torch.empty(B, Hh, N, dtype=torch.float64, device=dev) if with_thresh else None
     nb = bsa_workspace_bytes(OP_SELECT_KV, g, 1.0, B, Hh, d)
     ws = _ws(nb, dev)
-    _check(lib().bsa_select_kv_blocks_ex(ctypes.byref(g.c()), B, Hh, d, _ptr(Q), _ptr(q_pooled), _ptr(K), int(k),
+    _check(lib().bsa_select_kv_blocks_ex(ctypes.byref(g.c()), B, Hh, d, tensor_desc(Q), _ptr(q_pooled), tensor_desc(K), int(k),
                                          float(tau), int(mode), _ptr(num), _ptr(idx), _ptr(knum), _ptr(kidx), _ptr(th),
                                          _ptr(ws), nb, _stream(dev)), "bsa_select_kv_blocks_ex")
     return num, idx, knum, kidx, th
@@ -199,41 +237,62 @@ def bsa_select_kv_blocks(g: Geometry, Q: torch.Tensor, K: torch.Tensor, k: int, 
 
 def bsa_attn_fwd(g: Geometry, r: float, Q, K, V, kept_off, kept_tok, donor, q2k_num, q2k_idx, scale=None,
                  q_packed=None, out=None, lse=None):
-    """a7 (Eq.5) + fill: returns O [B,Hh,L,d] bf16 and lse [B,Hh,Lq] fp32."""
-    _need_cuda(Q, K, V, kept_off, kept_tok, donor, q2k_num, q2k_idx, q_packed)
+    """a7 (Eq.5) + fill: returns O [B,Hh,L,d] bf16 and lse [B,Hh,Lq] fp32. Q, K, V, out may be strided
+    [B, Hh, L, d] views (contiguous channels)."""
     B, Hh, L, d = K.shape
-    Lq = kept_tok.shape[-1]
+    N, Lq, _ = bsa_sizes(g, r)
     dev = K.device
+    O = torch.empty(B, Hh, L, d, dtype=torch.bfloat16, device=dev) if out is None else out
+    _need_rows((B, Hh, g.L, d), Q, K, V, O)
+    _need_i32("kept_off", kept_off, (N + 1,))
+    _need_i32("kept_tok", kept_tok, (B, Hh, Lq))
+    _need_i32("donor", donor, (B, Hh, L))
+    _need_i32("q2k_num", q2k_num, (B, Hh, N))
+    _need_i32("q2k_idx", q2k_idx, (B, Hh, N, N))
+    if q_packed is not None and (tuple(q_packed.shape) != (B, Hh, Lq, d) or not q_packed.is_contiguous()):
+        raise BSAError("q_packed must be a contiguous [B, Hh, Lq, d] bf16 tensor")
     scale = 1.0 / math.sqrt(d) if scale is None else scale
-    O = torch.empty_like(K) if out is None else out
     lse = torch.empty(B, Hh, Lq, dtype=torch.float32, device=dev) if lse is None else lse
+    if tuple(lse.shape) != (B, Hh, Lq) or lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise BSAError("lse must be a contiguous fp32 [B, Hh, Lq] tensor")
     nb = bsa_workspace_bytes(OP_ATTN_FWD, g, r, B, Hh, d)
     ws = _ws(nb, dev)
-    _check(lib().bsa_attn_fwd(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(q_packed),
-                              _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(q2k_num), _ptr(q2k_idx), float(scale),
-                              _ptr(O), _ptr(lse), _ptr(ws), nb, _stream(dev)), "bsa_attn_fwd")
+    _check(lib().bsa_attn_fwd(ctypes.byref(g.c()), r, B, Hh, d, tensor_desc(Q), tensor_desc(K), tensor_desc(V),
+                              _ptr(q_packed), _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(q2k_num), _ptr(q2k_idx),
+                              float(scale), tensor_desc(O), _ptr(lse), _ptr(ws), nb, _stream(dev)), "bsa_attn_fwd")
     return O, lse
 
 
 def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, donor, k2q_num, k2q_idx, lse,
-                 scale=None, q_packed=None, ws=None):
-    """a8: returns dQ, dK, dV [B,Hh,L,d] bf16."""
-    _need_cuda(Q, K, V, O, dO, kept_off, kept_tok, donor, k2q_num, k2q_idx, lse, q_packed)
+                 scale=None, q_packed=None, ws=None, out=None):
+    """a8: returns dQ, dK, dV [B,Hh,L,d] bf16 (into `out` = (dQ, dK, dV) if given; strided views allowed)."""
     B, Hh, L, d = K.shape
+    N, Lq, _ = bsa_sizes(g, r)
     dev = K.device
+    mk = lambda: torch.empty(B, Hh, L, d, dtype=torch.bfloat16, device=dev)  # noqa: E731
+    dQ, dK, dV = (mk(), mk(), mk()) if out is None else out
+    _need_rows((B, Hh, g.L, d), Q, K, V, O, dO, dQ, dK, dV)
+    _need_i32("kept_off", kept_off, (N + 1,))
+    _need_i32("kept_tok", kept_tok, (B, Hh, Lq))
+    _need_i32("donor", donor, (B, Hh, L))
+    _need_i32("k2q_num", k2q_num, (B, Hh, N))
+    _need_i32("k2q_idx", k2q_idx, (B, Hh, N, N))
+    if tuple(lse.shape) != (B, Hh, Lq) or lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise BSAError("lse must be a contiguous fp32 [B, Hh, Lq] tensor")
+    if q_packed is not None and (tuple(q_packed.shape) != (B, Hh, Lq, d) or not q_packed.is_contiguous()):
+        raise BSAError("q_packed must be a contiguous [B, Hh, Lq, d] bf16 tensor")
     scale = 1.0 / math.sqrt(d) if scale is None else scale
-    dQ, dK, dV = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
     nb = bsa_workspace_bytes(OP_ATTN_BWD, g, r, B, Hh, d)
     if ws is None or ws.numel() < nb:
         ws = _ws(nb, dev)
-    _check(lib().bsa_attn_bwd(ctypes.byref(g.c()), r, B, Hh, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(dO),
-                              _ptr(q_packed), _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(k2q_num),
-                              _ptr(k2q_idx), _ptr(lse), float(scale), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(ws), nb,
-                              _stream(dev)), "bsa_attn_bwd")
+    T = tensor_desc
+    _check(lib().bsa_attn_bwd(ctypes.byref(g.c()), r, B, Hh, d, T(Q), T(K), T(V), T(O), T(dO), _ptr(q_packed),
+                              _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(k2q_num), _ptr(k2q_idx), _ptr(lse),
+                              float(scale), T(dQ), T(dK), T(dV), _ptr(ws), nb, _stream(dev)), "bsa_attn_bwd")
     return dQ, dK, dV
 
 
-SP_SEQ_TO_SEND, SP_RECV_TO_HEADS, SP_HEADS_TO_SEND, SP_RECV_TO_SEQ = 0, 1, 2, 3
+SP_SEQ_TO_SEND, SP_RECV_TO_HEADS, SP_HEADS_TO_SEND, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND_T, SP_RECV_T_TO_SEQ = 0, 1, 2, 3, 4, 5
 
 
 def bsa_sp_relayout(mode: int, src: torch.Tensor, dst: torch.Tensor, B: int, Ls: int, Hh: int, d: int, P: int):
@@ -248,8 +307,19 @@ def bsa_sp_relayout(mode: int, src: torch.Tensor, dst: torch.Tensor, B: int, Ls:
 
 
 def resolve_k(f: float, N: int) -> int:
-    """Eq.3 key count from a fraction: clamp(ceil(f*N - 1e-9), 1, N) (reading C6)."""
-    return max(1, min(N, math.ceil(f * N - 1e-9)))
+    """Eq.3 key count from a fraction: clamp(ceil(f*N - 1e-9), 1, N) (reading C6), computed by the library
+    (bsa_resolve_k, host only)."""
+    k = _I()
+    _check(lib().bsa_resolve_k(float(f), int(N), ctypes.byref(k)), "bsa_resolve_k")
+    return k.value
+
+
+def kv_quantile(k: int, N: int) -> float:
+    """Eq.3's z = U(1 - k/N) (argument clamped to [1/(2N), 1 - 1/(2N)]) exactly as bsa_select_kv_blocks uses it
+    (bsa_kv_quantile, host only)."""
+    z = _D()
+    _check(lib().bsa_kv_quantile(int(k), int(N), ctypes.byref(z)), "bsa_kv_quantile")
+    return z.value
 
 
 @dataclass

@@ -56,6 +56,23 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// A strided [B, Hh, L, d] operand (include/bsa.h bsa_tensor) -> kernel view. NULL pointers pass when !required.
+int check_tensor(const bsa_tensor& t, const char* name, int Hh, int d, bool required, bsa::Rows* out) {
+  if (!t.ptr) {
+    if (required) return fail(BSA_ERR_SELECTION_MISMATCH, "tensor %s is NULL", name);
+    *out = bsa::Rows{nullptr, 0, 0, 0, Hh};
+    return BSA_OK;
+  }
+  if (!aligned16(t.ptr)) return fail(BSA_ERR_INVALID_SHAPE, "tensor %s is not 16-byte aligned", name);
+  if (t.sb < 0 || t.sh < 0 || t.sl < d || (t.sb | t.sh | t.sl) & 7 || t.sb >= (1LL << 38) || t.sh >= (1LL << 38) ||
+      t.sl >= (1LL << 30))
+    return fail(BSA_ERR_INVALID_SHAPE,
+                "tensor %s: strides (sb, sh, sl) = (%lld, %lld, %lld) must be non-negative multiples of 8 elements "
+                "with sl >= d = %d", name, (long long)t.sb, (long long)t.sh, (long long)t.sl, d);
+  *out = bsa::Rows{static_cast<bsa::bf16*>(t.ptr), t.sb, t.sh, t.sl, Hh};
+  return BSA_OK;
+}
+
 // Host geometry + validation shared by every entry point.
 int check_geom(const bsa_geom* g, bsa::Geo* out) {
   if (!g) return fail(BSA_ERR_INVALID_SHAPE, "geometry is NULL");
@@ -163,6 +180,14 @@ int check_attn_geom(const bsa::Geo& G, double r, int* Lq, int* SR) {
   return BSA_OK;
 }
 
+// Eq.3's U(1 - k/n) with the argument clamped to [1/(2n), 1 - 1/(2n)] (reading C14).
+double eq3_z(int k, int N) {
+  double u = 1.0 - static_cast<double>(k) / N;
+  const double lo = 1.0 / (2.0 * N), hi = 1.0 - 1.0 / (2.0 * N);
+  u = u < lo ? lo : (u > hi ? hi : u);
+  return bsa::normal_quantile(u);
+}
+
 }  // namespace
 
 #define CHECK(x)                 \
@@ -173,7 +198,23 @@ int check_attn_geom(const bsa::Geo& G, double r, int* Lq, int* SR) {
 
 extern "C" {
 
-int bsa_version(void) { return 1; }
+int bsa_version(void) { return 2; }
+
+int bsa_resolve_k(double f, int32_t N, int32_t* k) {
+  if (N < 1) return fail(BSA_ERR_INVALID_SHAPE, "N must be >= 1 (got %d)", N);
+  if (!(f > 0.0 && f <= 1.0)) return fail(BSA_ERR_CONFIG, "key fraction f must be in (0,1] (got %g)", f);
+  if (!k) return fail(BSA_ERR_SELECTION_MISMATCH, "k is NULL");
+  *k = bsa::keep_count(f, N);
+  return BSA_OK;
+}
+
+int bsa_kv_quantile(int32_t k, int32_t N, double* z) {
+  if (N < 1) return fail(BSA_ERR_INVALID_SHAPE, "N must be >= 1 (got %d)", N);
+  if (k < 1 || k > N) return fail(BSA_ERR_CONFIG, "k must be in [1, N=%d] (got %d)", N, k);
+  if (!z) return fail(BSA_ERR_SELECTION_MISMATCH, "z is NULL");
+  *z = eq3_z(k, N);
+  return BSA_OK;
+}
 
 const char* bsa_strerror(int s) {
   switch (s) {
@@ -238,47 +279,53 @@ int bsa_block_partition(const bsa_geom* g, double r, int32_t* block_off, int32_t
   return BSA_OK;
 }
 
-int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q,
+int bsa_select_queries(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q,
                        const int32_t* kept_off, int32_t* kept_tok, int32_t* donor, double* q_pooled, void* q_packed,
                        void* stream) {
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_r(r));
   CHECK(check_dims(B, Hh, d));
-  if (!Q || !kept_off || !kept_tok || !donor)
-    return fail(BSA_ERR_SELECTION_MISMATCH, "Q, kept_off, kept_tok and donor are required");
-  if (!aligned16(Q) || (q_packed && !aligned16(q_packed))) return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  bsa::Rows Qv;
+  CHECK(check_tensor(Q, "Q", Hh, d, true, &Qv));
+  if (!kept_off || !kept_tok || !donor)
+    return fail(BSA_ERR_SELECTION_MISMATCH, "kept_off, kept_tok and donor are required");
+  if (q_packed && !aligned16(q_packed)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned q_packed");
   CHECK(check_device());
   int lq = 0, mk = 0;
   host_sizes(G, r, &lq, &mk);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(BSA_K_SELECT_Q, 1, st, [&] {
-    return bsa::launch_select_queries(G, r, B * Hh, d, lq, static_cast<const bsa::bf16*>(Q), kept_off, kept_tok, donor,
-                                      q_pooled, static_cast<bsa::bf16*>(q_packed), st);
+    return bsa::launch_select_queries(G, r, B * Hh, d, lq, Qv, kept_off, kept_tok, donor, q_pooled,
+                                      static_cast<bsa::bf16*>(q_packed), st);
   });
   if (e != cudaSuccess) return cuda_fail(e, "select_queries");
   return BSA_OK;
 }
 
-int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q, const double* q_pooled,
-                         const void* K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
+int bsa_select_kv_blocks(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, const double* q_pooled,
+                         bsa_tensor K, int32_t k, double tau, int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num,
                          int32_t* k2q_idx, double* thresh, void* ws, size_t ws_bytes, void* stream) {
   return bsa_select_kv_blocks_ex(g, B, Hh, d, Q, q_pooled, K, k, tau, BSA_KV_TWO_STAGE, q2k_num, q2k_idx, k2q_num,
                                  k2q_idx, thresh, ws, ws_bytes, stream);
 }
 
-int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, const void* Q,
-                            const double* q_pooled, const void* K, int32_t k, double tau, int32_t mode,
+int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q,
+                            const double* q_pooled, bsa_tensor K, int32_t k, double tau, int32_t mode,
                             int32_t* q2k_num, int32_t* q2k_idx, int32_t* k2q_num, int32_t* k2q_idx, double* thresh,
                             void* ws, size_t ws_bytes, void* stream) {
   if (mode != BSA_KV_TWO_STAGE && mode != BSA_KV_UNIFIED_PROB) return fail(BSA_ERR_CONFIG, "unknown KV mode %d", mode);
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_dims(B, Hh, d));
+  if (G.N > 4096)
+    return fail(BSA_ERR_INVALID_SHAPE, "KV selection supports N <= 4096 blocks (got %d)", G.N);
   if (k < 1 || k > G.N) return fail(BSA_ERR_CONFIG, "k must be in [1, N=%d] (got %d)", G.N, k);
   if (!(tau > 0.0 && tau <= 1.0)) return fail(BSA_ERR_CONFIG, "tau must be in (0,1] (got %g)", tau);
-  if (!K || (!Q && !q_pooled) || !q2k_num || !q2k_idx)
-    return fail(BSA_ERR_SELECTION_MISMATCH, "K, Q or q_pooled, q2k_num and q2k_idx are required");
+  bsa::Rows Qv, Kv;
+  CHECK(check_tensor(K, "K", Hh, d, true, &Kv));
+  CHECK(check_tensor(Q, "Q", Hh, d, q_pooled == nullptr, &Qv));
+  if (!q2k_num || !q2k_idx) return fail(BSA_ERR_SELECTION_MISMATCH, "q2k_num and q2k_idx are required");
   if ((k2q_num == nullptr) != (k2q_idx == nullptr))
     return fail(BSA_ERR_SELECTION_MISMATCH, "k2q_num and k2q_idx must be both given or both NULL");
   size_t BH = static_cast<size_t>(B) * Hh;
@@ -294,21 +341,13 @@ int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d,
   uint32_t* bits = reinterpret_cast<uint32_t*>(base + w.bits);
   int* ovf = reinterpret_cast<int*>(base + w.ovf);
   cudaError_t e = timed(BSA_K_POOL, 1, st, [&] {
-    return bsa::launch_pool(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(K), Kc, st);
+    return bsa::launch_pool(G, static_cast<int>(BH), d, Kv, Kc, st);
   });
   if (e == cudaSuccess && !q_pooled)
-    e = timed(BSA_K_POOL, 1, st, [&] {
-      return bsa::launch_pool(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(Q), Qc, st);
-    });
+    e = timed(BSA_K_POOL, 1, st, [&] { return bsa::launch_pool(G, static_cast<int>(BH), d, Qv, Qc, st); });
   if (e == cudaSuccess)
     e = timed(BSA_K_SCORES, 1, st, [&] { return bsa::launch_scores(G.N, static_cast<int>(BH), d, Qc, Kc, S, st); });
-  double z = 0.0;
-  if (k < G.N || mode == BSA_KV_UNIFIED_PROB) {  // unified_prob has no k = N bypass (C28)
-    double u = 1.0 - static_cast<double>(k) / G.N;
-    double lo = 1.0 / (2.0 * G.N), hi = 1.0 - 1.0 / (2.0 * G.N);
-    u = u < lo ? lo : (u > hi ? hi : u);
-    z = bsa::normal_quantile(u);
-  }
+  const double z = (k < G.N || mode == BSA_KV_UNIFIED_PROB) ? eq3_z(k, G.N) : 0.0;  // unified: no k = N bypass
   if (e == cudaSuccess)
     e = timed(BSA_K_ADMIT, (k < G.N && mode == BSA_KV_TWO_STAGE) ? 2 : 1, st, [&] {
       return bsa::launch_admit(G.N, static_cast<int>(BH), S, k, z, tau, mode == BSA_KV_UNIFIED_PROB ? 1 : 0, q2k_num,
@@ -323,19 +362,23 @@ int bsa_select_kv_blocks_ex(const bsa_geom* g, int32_t B, int32_t Hh, int32_t d,
   return BSA_OK;
 }
 
-int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
-                 const void* V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
-                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, void* O,
+int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
+                 bsa_tensor V, const void* q_packed, const int32_t* kept_off, const int32_t* kept_tok,
+                 const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx, float scale, bsa_tensor O,
                  float* lse, void* ws, size_t ws_bytes, void* stream) {
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_r(r));
   CHECK(check_dims(B, Hh, d));
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(BSA_ERR_CONFIG, "scale must be positive and finite");
-  if (!K || !V || !kept_off || !kept_tok || !donor || !q2k_num || !q2k_idx || !O || !lse || (!q_packed && !Q))
+  bsa::Rows Qv, Kv, Vv, Ov;
+  CHECK(check_tensor(Q, "Q", Hh, d, q_packed == nullptr, &Qv));
+  CHECK(check_tensor(K, "K", Hh, d, true, &Kv));
+  CHECK(check_tensor(V, "V", Hh, d, true, &Vv));
+  CHECK(check_tensor(O, "O", Hh, d, true, &Ov));
+  if (!kept_off || !kept_tok || !donor || !q2k_num || !q2k_idx || !lse)
     return fail(BSA_ERR_SELECTION_MISMATCH, "missing required pointer");
-  if (!aligned16(K) || !aligned16(V) || !aligned16(O) || (Q && !aligned16(Q)) || (q_packed && !aligned16(q_packed)))
-    return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  if (q_packed && !aligned16(q_packed)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned q_packed");
   int Lq = 0, SR = 0;
   CHECK(check_attn_geom(G, r, &Lq, &SR));
   size_t BH = static_cast<size_t>(B) * Hh;
@@ -348,14 +391,12 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* kv_img = base + w.kv;
   cudaError_t e = timed(BSA_K_KV_IMAGE, 1, st, [&] {
-    return bsa::launch_kv_image(G, static_cast<int>(BH), d, static_cast<const bsa::bf16*>(K),
-                                static_cast<const bsa::bf16*>(V), kv_img, st);
+    return bsa::launch_kv_image(G, static_cast<int>(BH), d, Kv, Vv, kv_img, st);
   });
   if (e == cudaSuccess && !Qs) {
     bsa::bf16* dst = reinterpret_cast<bsa::bf16*>(base + w.qs);
     e = timed(BSA_K_GATHER, 1, st, [&] {
-      return bsa::launch_gather_rows(static_cast<int>(BH), G.L, Lq, d, static_cast<const bsa::bf16*>(Q), kept_tok, dst,
-                                     st);
+      return bsa::launch_gather_rows(static_cast<int>(BH), Lq, d, Qv, kept_tok, dst, st);
     });
     Qs = dst;
   }
@@ -365,9 +406,8 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.d = d;
   a.Lq = Lq;
   a.SR = SR;
-  a.Q = static_cast<const bsa::bf16*>(Q);
-  a.K = static_cast<const bsa::bf16*>(K);
-  a.V = static_cast<const bsa::bf16*>(V);
+  a.K = Kv;
+  a.V = Vv;
   a.Qs = Qs;
   a.kept_off = kept_off;
   a.kept_tok = kept_tok;
@@ -375,7 +415,7 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.q2k_num = q2k_num;
   a.q2k_idx = q2k_idx;
   a.scale = scale;
-  a.O = static_cast<bsa::bf16*>(O);
+  a.O = Ov;
   a.lse = lse;
   a.kv_img = kv_img;
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
@@ -384,22 +424,28 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   return BSA_OK;
 }
 
-int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, const void* Q, const void* K,
-                 const void* V, const void* O, const void* dO, const void* q_packed, const int32_t* kept_off,
+int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
+                 bsa_tensor V, bsa_tensor O, bsa_tensor dO, const void* q_packed, const int32_t* kept_off,
                  const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
-                 const float* lse, float scale, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                 const float* lse, float scale, bsa_tensor dQ, bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes,
                  void* stream) {
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_r(r));
   CHECK(check_dims(B, Hh, d));
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(BSA_ERR_CONFIG, "scale must be positive and finite");
-  if (!K || !V || !O || !dO || !kept_off || !kept_tok || !donor || !k2q_num || !k2q_idx || !lse || !dQ || !dK ||
-      !dV || (!q_packed && !Q))
+  bsa::Rows Qv, Kv, Vv, Ov, dOv, dQv, dKv, dVv;
+  CHECK(check_tensor(Q, "Q", Hh, d, q_packed == nullptr, &Qv));
+  CHECK(check_tensor(K, "K", Hh, d, true, &Kv));
+  CHECK(check_tensor(V, "V", Hh, d, true, &Vv));
+  CHECK(check_tensor(O, "O", Hh, d, true, &Ov));
+  CHECK(check_tensor(dO, "dO", Hh, d, true, &dOv));
+  CHECK(check_tensor(dQ, "dQ", Hh, d, true, &dQv));
+  CHECK(check_tensor(dK, "dK", Hh, d, true, &dKv));
+  CHECK(check_tensor(dV, "dV", Hh, d, true, &dVv));
+  if (!kept_off || !kept_tok || !donor || !k2q_num || !k2q_idx || !lse)
     return fail(BSA_ERR_SELECTION_MISMATCH, "missing required pointer");
-  const void* ptrs[] = {Q, K, V, O, dO, q_packed, dQ, dK, dV};
-  for (const void* ptr : ptrs)
-    if (ptr && !aligned16(ptr)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned tensor");
+  if (q_packed && !aligned16(q_packed)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned q_packed");
   int Lq = 0, SR = 0;
   CHECK(check_attn_geom(G, r, &Lq, &SR));
   size_t BH = static_cast<size_t>(B) * Hh;
@@ -414,22 +460,22 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   if (!Qs) {
     bsa::bf16* dst = reinterpret_cast<bsa::bf16*>(base + w.qs);
     e = timed(BSA_K_GATHER, 1, st, [&] {
-      return bsa::launch_gather_rows(static_cast<int>(BH), G.L, Lq, d, static_cast<const bsa::bf16*>(Q), kept_tok, dst,
-                                     st);
+      return bsa::launch_gather_rows(static_cast<int>(BH), Lq, d, Qv, kept_tok, dst, st);
     });
     Qs = dst;
   }
   bsa::BwdArgs a;
   a.g = G;
+  a.B = B;
+  a.Hh = Hh;
   a.BH = static_cast<int>(BH);
   a.d = d;
   a.Lq = Lq;
   a.SR = SR;
-  a.Q = static_cast<const bsa::bf16*>(Q);
-  a.K = static_cast<const bsa::bf16*>(K);
-  a.V = static_cast<const bsa::bf16*>(V);
-  a.O = static_cast<const bsa::bf16*>(O);
-  a.dO = static_cast<const bsa::bf16*>(dO);
+  a.K = Kv;
+  a.V = Vv;
+  a.O = Ov;
+  a.dO = dOv;
   a.Qs = Qs;
   a.kept_off = kept_off;
   a.kept_tok = kept_tok;
@@ -438,14 +484,17 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.k2q_idx = k2q_idx;
   a.lse = lse;
   a.scale = scale;
-  a.dQ = static_cast<bsa::bf16*>(dQ);
-  a.dK = static_cast<bsa::bf16*>(dK);
-  a.dV = static_cast<bsa::bf16*>(dV);
+  a.dQ = dQv;
+  a.dK = dKv;
+  a.dV = dVv;
   a.qdo_img = base + w.img;
   a.lsed = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
-  if (e == cudaSuccess) e = timed(BSA_K_ATTN_BWD, 1, st, [&] { return bsa::launch_bwd_main(a, st); });
+  const bool one_launch = (B == 1) || (Kv.sb == Hh * Kv.sh && Vv.sb == Hh * Vv.sh && dKv.sb == Hh * dKv.sh &&
+                                       dVv.sb == Hh * dVv.sh);
+  if (e == cudaSuccess)
+    e = timed(BSA_K_ATTN_BWD, one_launch ? 1 : B, st, [&] { return bsa::launch_bwd_main(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 2, st, [&] { return bsa::launch_bwd_finalize(a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_bwd");
   return BSA_OK;
@@ -458,7 +507,7 @@ int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int3
   if (B < 1 || Ls < 1 || Hh < 1 || P < 1) return fail(BSA_ERR_INVALID_SHAPE, "B, Ls, Hh, P must be >= 1");
   if (d < 8 || d % 8) return fail(BSA_ERR_INVALID_SHAPE, "d must be a positive multiple of 8 (got %d)", d);
   if (Hh % P) return fail(BSA_ERR_CONFIG, "Hh = %d heads do not split over P = %d ranks", Hh, P);
-  if (mode < BSA_SP_SEQ_TO_SEND || mode > BSA_SP_RECV_TO_SEQ) return fail(BSA_ERR_CONFIG, "unknown mode %d", mode);
+  if (mode < BSA_SP_SEQ_TO_SEND || mode > BSA_SP_RECV_T_TO_SEQ) return fail(BSA_ERR_CONFIG, "unknown mode %d", mode);
   if (!src || !dst || !aligned16(src) || !aligned16(dst))
     return fail(BSA_ERR_INVALID_SHAPE, "src/dst must be non-NULL and 16-byte aligned");
   CHECK(check_device());

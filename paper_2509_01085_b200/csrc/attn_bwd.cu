@@ -25,7 +25,7 @@
 namespace bsa {
 
 bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
-bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int BH);
+bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int heads, long long sl, long long sh);
 bool make_map_rows_f32(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
 
 __device__ __forceinline__ float ex2b(float x) {
@@ -50,8 +50,8 @@ __device__ __forceinline__ float ex2b(float x) {
 template <int D>
 __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR, const int* __restrict__ kept_off,
                                                   const int* __restrict__ kept_tok, const int* __restrict__ donor,
-                                                  const bf16* __restrict__ Qs, const bf16* __restrict__ dO,
-                                                  const bf16* __restrict__ O, const float* __restrict__ lse,
+                                                  const bf16* __restrict__ Qs, const Rows dO, const Rows O,
+                                                  const float* __restrict__ lse,
                                                   uint8_t* __restrict__ qdo_img, float* __restrict__ lsed,
                                                   float* __restrict__ dQacc) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t bi = static_cast<size_t>(bh) * g.N + blk;
   const size_t head = static_cast<size_t>(bh) * g.L;
+  const bf16* doh = dO.head(bh);
+  const bf16* oh = O.head(bh);
   const Box x = block_box(g, blk);
   const int n = box_size(x);
   const int ko = kept_off[blk], nk = kept_off[blk + 1] - ko;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
   __syncthreads();
   for (int v = threadIdx.x; v < n * (D / 8); v += blockDim.x) {
     const int i = v / (D / 8), c = (v % (D / 8)) * 8;
-    *reinterpret_cast<uint4*>(s_do + i * D + c) = *reinterpret_cast<const uint4*>(dO + (head + s_tok[i]) * D + c);
+    *reinterpret_cast<uint4*>(s_do + i * D + c) = *reinterpret_cast<const uint4*>(doh + s_tok[i] * dO.sl + c);
   }
   __syncthreads();
   const int ch0 = lane * PER;
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
       }
     }
     float dsum = 0.f;
-    const bf16* orow = O + (head + tok) * D + ch0;
+    const bf16* orow = oh + tok * O.sl + ch0;
     bf16 hv[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
@@ -188,8 +190,8 @@ struct BwdParams {
   const int* k2q_num;
   const int* k2q_idx;
   float* dQacc;
-  bf16* dK;
-  bf16* dV;
+  int bh0;             // first (b,h) of this launch: blockIdx.y + bh0 indexes the internal buffers, blockIdx.y
+                       // is the head coordinate of the K/V/dK/dV tensor maps
   float scale_log2;
   float scale;
 };
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bh = blockIdx.y;
+  const int bh = p.bh0 + static_cast<int>(blockIdx.y), hc = static_cast<int>(blockIdx.y);
   const int G = p.G, SR = p.SR;
   const int j_first = blockIdx.x * BWD_NB, j_end = min_i(j_first + BWD_NB, g.N);
   // per KV block of this CTA: admitting query blocks, chunks, rotation of the chunk order (concurrent CTAs
@@ -398,8 +400,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
           mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
           for (int cb = 0; cb < NCB; ++cb) {
-            tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-            tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+            tma_load_5d(sK + cb * BT * 128, &p.mK, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
+            tma_load_5d(sV + cb * BT * 128, &p.mV, &bar_kv, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
           }
         }
         __syncwarp();
@@ -594,8 +596,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       if (row == 0) {
         const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
         for (int cb = 0; cb < NCB; ++cb) {
-          tma_store_5d(&p.mdK, sP + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
-          tma_store_5d(&p.mdV, sdS + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, bh);
+          tma_store_5d(&p.mdK, sP + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
+          tma_store_5d(&p.mdV, sdS + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
@@ -702,24 +704,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 }
 
 // ------------------------------------------------------------------------------------ finalize
-__global__ void k_bwd_zero_pruned(int BH, int L, int d, const int* __restrict__ donor, bf16* __restrict__ dQ) {
+__global__ void k_bwd_zero_pruned(int BH, int L, int d, const int* __restrict__ donor, const Rows dQ) {
   size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int vpr = d / 8;
   if (v >= static_cast<size_t>(BH) * L * vpr) return;
   size_t rowi = v / vpr;
   int c = static_cast<int>(v % vpr) * 8;
-  if (donor[rowi] != static_cast<int>(rowi % L))
-    *reinterpret_cast<uint4*>(dQ + rowi * d + c) = make_uint4(0, 0, 0, 0);
+  const int t = static_cast<int>(rowi % L);
+  if (donor[rowi] != t)
+    *reinterpret_cast<uint4*>(dQ.row(static_cast<int>(rowi / L), t) + c) = make_uint4(0, 0, 0, 0);
 }
 
-__global__ void k_bwd_finalize(int BH, int L, int Lq, int d, float scale, const int* __restrict__ kept_tok,
-                               const float* __restrict__ dQacc, bf16* __restrict__ dQ) {
+__global__ void k_bwd_finalize(int BH, int Lq, int d, float scale, const int* __restrict__ kept_tok,
+                               const float* __restrict__ dQacc, const Rows dQ) {
   size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int vpr = d / 8;
   if (v >= static_cast<size_t>(BH) * Lq * vpr) return;
   size_t prow = v / vpr;
   int c = static_cast<int>(v % vpr) * 8;
-  size_t bh = prow / Lq;
+  const int bh = static_cast<int>(prow / Lq);
   int tok = kept_tok[prow];
   const float4* src = reinterpret_cast<const float4*>(dQacc + prow * d + c);
   float4 a = src[0], b = src[1];
@@ -730,17 +733,21 @@ __global__ void k_bwd_finalize(int BH, int L, int Lq, int d, float scale, const 
   o.y = *reinterpret_cast<uint32_t*>(&h1);
   o.z = *reinterpret_cast<uint32_t*>(&h2);
   o.w = *reinterpret_cast<uint32_t*>(&h3);
-  *reinterpret_cast<uint4*>(dQ + (bh * L + tok) * d + c) = o;
+  *reinterpret_cast<uint4*>(dQ.row(bh, tok) + c) = o;
 }
 
 template <int D, int BT>
-static cudaError_t run_bwd(const BwdParams& p, int BH, cudaStream_t st) {
+static cudaError_t run_bwd(const BwdParams& p, int heads, cudaStream_t st) {
   constexpr int smem = BwdSmem<D, BT>::TOTAL;
   cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_attn_bwd<D, BT><<<dim3((p.g.N + BWD_NB - 1) / BWD_NB, BH), BWD_THREADS, smem, st>>>(p);
+  k_attn_bwd<D, BT><<<dim3((p.g.N + BWD_NB - 1) / BWD_NB, heads), BWD_THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
+
+// The K/V/dK/dV tensor maps index heads with one stride: one launch over all B*Hh heads when the batch stride
+// continues the head stride (sb == Hh sh, e.g. contiguous [B, Hh, L, d], or B == 1), else one launch per batch.
+static bool heads_uniform(const Rows& x, int B) { return B == 1 || x.sb == x.Hh * x.sh; }
 
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
   const dim3 prep_blocks(a.g.N, a.BH);  // one CTA per (b,h, query block)
@@ -764,23 +771,30 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.k2q_num = a.k2q_num;
   p.k2q_idx = a.k2q_idx;
   p.dQacc = a.dQacc;
-  p.dK = a.dK;
-  p.dV = a.dV;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.scale = a.scale;
   p.qdo_img = a.qdo_img;
-  if (!make_map_5d(&p.mK, a.K, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
-  if (!make_map_5d(&p.mV, a.V, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
-  if (!make_map_5d(&p.mdK, a.dK, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
-  if (!make_map_5d(&p.mdV, a.dV, a.g, a.d, a.BH)) return cudaErrorInvalidValue;
   p.lsed = a.lsed;
   p.dq_rows = a.SR < 16 ? a.SR : 16;
   if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
-  if (a.d == 128 && a.g.BT == 64) return run_bwd<128, 64>(p, a.BH, st);
-  if (a.d == 128 && a.g.BT == 32) return run_bwd<128, 32>(p, a.BH, st);
-  if (a.d == 64 && a.g.BT == 64) return run_bwd<64, 64>(p, a.BH, st);
-  if (a.d == 64 && a.g.BT == 32) return run_bwd<64, 32>(p, a.BH, st);
-  return cudaErrorInvalidValue;
+  const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
+                   heads_uniform(a.dV, a.B);
+  const int launches = one ? 1 : a.B, heads = one ? a.BH : a.Hh;
+  for (int b = 0; b < launches; ++b) {
+    const Rows* ts[4] = {&a.K, &a.V, &a.dK, &a.dV};
+    CUtensorMap* ms[4] = {&p.mK, &p.mV, &p.mdK, &p.mdV};
+    for (int t = 0; t < 4; ++t)
+      if (!make_map_5d(ms[t], ts[t]->p + b * ts[t]->sb, a.g, a.d, heads, ts[t]->sl, ts[t]->sh))
+        return cudaErrorInvalidValue;
+    p.bh0 = b * a.Hh;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (a.d == 128 && a.g.BT == 64) e = run_bwd<128, 64>(p, heads, st);
+    else if (a.d == 128 && a.g.BT == 32) e = run_bwd<128, 32>(p, heads, st);
+    else if (a.d == 64 && a.g.BT == 64) e = run_bwd<64, 64>(p, heads, st);
+    else if (a.d == 64 && a.g.BT == 32) e = run_bwd<64, 32>(p, heads, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
@@ -788,7 +802,7 @@ cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
   size_t tz = static_cast<size_t>(a.BH) * a.g.L * (a.d / 8);
   k_bwd_zero_pruned<<<static_cast<unsigned>((tz + 255) / 256), 256, 0, st>>>(a.BH, a.g.L, a.d, a.donor, a.dQ);
   size_t tf = rows * (a.d / 8);
-  k_bwd_finalize<<<static_cast<unsigned>((tf + 255) / 256), 256, 0, st>>>(a.BH, a.g.L, a.Lq, a.d, a.scale, a.kept_tok,
+  k_bwd_finalize<<<static_cast<unsigned>((tf + 255) / 256), 256, 0, st>>>(a.BH, a.Lq, a.d, a.scale, a.kept_tok,
                                                                           a.dQacc, a.dQ);
   return cudaGetLastError();
 }

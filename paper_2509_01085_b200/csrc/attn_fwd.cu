@@ -58,7 +58,7 @@ struct FwdParams {
   const int* q2k_num;
   const int* q2k_idx;
   float scale_log2;  // scale * log2(e)
-  bf16* O;
+  Rows O;            // raster output, strided
   float* lse;
   unsigned long long clsmask[8];  // key-validity mask of each block-extent class (host-computed, C23)
 };
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     bf16* orow = nullptr;
     if (valid) {
       int tok = p.kept_tok[prow_idx];
-      orow = p.O + (static_cast<size_t>(bh) * g.L + tok) * D;
+      orow = p.O.row(bh, tok);
       if (group == 0) p.lse[prow_idx] = (m + log2f(l)) * 0.6931471805599453f;
     }
     const float s0 = a0 * inv, s1 = a1 * inv;
@@ -589,14 +589,15 @@ bool make_map_rows_f32(CUtensorMap* m, const void* base, int d, size_t rows, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 5D block map over a raster [BH, T, H, W, d] bf16 tensor, box {64, cw, ch, ct, 1}, 128B swizzle.
-bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int BH) {
+// 5D block map over `heads` raster heads of a bf16 tensor, [heads][T][H][W][d] with token stride sl and head
+// stride sh (elements; d contiguous), box {64, cw, ch, ct, 1}, 128B swizzle. base = token 0 of head 0.
+bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int heads, long long sl, long long sh) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[5] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.H),
-                        static_cast<cuuint64_t>(g.T), static_cast<cuuint64_t>(BH)};
-  cuuint64_t rs = static_cast<cuuint64_t>(d) * 2;
-  cuuint64_t str[4] = {rs, rs * g.W, rs * g.W * g.H, rs * g.W * g.H * g.T};
+                        static_cast<cuuint64_t>(g.T), static_cast<cuuint64_t>(heads)};
+  cuuint64_t rs = static_cast<cuuint64_t>(sl) * 2;
+  cuuint64_t str[4] = {rs, rs * g.W, rs * g.W * g.H, static_cast<cuuint64_t>(sh) * 2};
   cuuint32_t box[5] = {64, static_cast<cuuint32_t>(g.cw), static_cast<cuuint32_t>(g.ch),
                        static_cast<cuuint32_t>(g.ct), 1};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
@@ -655,14 +656,14 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
 // order (lt, lh, lw), out-of-grid rows of ragged blocks zero — so one KV step is ONE contiguous bulk
 // copy (small TMA boxes cost ~500 cycles each; one 32 KB request per step keeps ~128 KB in flight).
 template <int D, int BT>
-__global__ void __launch_bounds__(256) k_kv_image(Geo g, const bf16* __restrict__ K, const bf16* __restrict__ V,
-                                                  uint8_t* __restrict__ img) {
+__global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Rows V, uint8_t* __restrict__ img) {
   constexpr int CPR = D / 8;        // 16-byte chunks per row
   constexpr int CHUNKS = BT * CPR;  // per tensor
   const int j = blockIdx.x, bh = blockIdx.y;
   const Box x = block_box(g, j);
   uint8_t* dst = img + (static_cast<size_t>(bh) * g.N + j) * (2 * BT * D * 2);
-  const size_t head = static_cast<size_t>(bh) * g.L;
+  const bf16* kh = K.head(bh);
+  const bf16* vh = V.head(bh);
   for (int v = threadIdx.x; v < 2 * CHUNKS; v += blockDim.x) {
     const int t = v / CHUNKS, w = v % CHUNKS;
     const int r = w / CPR, c = w % CPR;
@@ -670,14 +671,13 @@ __global__ void __launch_bounds__(256) k_kv_image(Geo g, const bf16* __restrict_
     uint4 val = make_uint4(0, 0, 0, 0);
     if (lt < x.e[0] && lh < x.e[1] && lw < x.e[2]) {
       const size_t tok = (static_cast<size_t>(x.o[0] + lt) * g.H + (x.o[1] + lh)) * g.W + (x.o[2] + lw);
-      val = *reinterpret_cast<const uint4*>((t ? V : K) + (head + tok) * D + c * 8);
+      val = *reinterpret_cast<const uint4*>((t ? vh + tok * V.sl : kh + tok * K.sl) + c * 8);
     }
     *reinterpret_cast<uint4*>(dst + t * (BT * D * 2) + (c >> 3) * (BT * 128) + sw128_off(r, c & 7)) = val;
   }
 }
 
-cudaError_t launch_kv_image(const Geo& g, int BH, int d, const bf16* K, const bf16* V, uint8_t* img,
-                            cudaStream_t st) {
+cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st) {
   dim3 grid(g.N, BH);
   if (d == 128 && g.BT == 64) k_kv_image<128, 64><<<grid, 256, 0, st>>>(g, K, V, img);
   else if (d == 128 && g.BT == 32) k_kv_image<128, 32><<<grid, 256, 0, st>>>(g, K, V, img);
@@ -688,17 +688,19 @@ cudaError_t launch_kv_image(const Geo& g, int BH, int d, const bf16* K, const bf
 }
 
 // Fill (reading C9): O[t] = O^s[donor(t)] for pruned t; one 16-byte chunk per thread.
-__global__ void k_fill(int BH, int L, int d, const int* __restrict__ donor, bf16* __restrict__ O) {
+__global__ void k_fill(int BH, int L, int d, const int* __restrict__ donor, const Rows O) {
   size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int vpr = d / 8;
   if (v >= static_cast<size_t>(BH) * L * vpr) return;
   size_t rowi = v / vpr;
   int c = static_cast<int>(v % vpr) * 8;
-  size_t bh = rowi / L;
+  const int bh = static_cast<int>(rowi / L);
   int t = static_cast<int>(rowi % L);
   int dn = donor[rowi];
-  if (dn != t)
-    *reinterpret_cast<uint4*>(O + rowi * d + c) = *reinterpret_cast<const uint4*>(O + (bh * L + dn) * d + c);
+  if (dn != t) {
+    bf16* oh = O.head(bh);
+    *reinterpret_cast<uint4*>(oh + t * O.sl + c) = *reinterpret_cast<const uint4*>(oh + dn * O.sl + c);
+  }
 }
 
 // debug: record the per-step timeline of CTA `cta` into dev_buf ([6][1024] u64), or disable (NULL)
@@ -709,7 +711,7 @@ cudaError_t debug_trace_fwd(void* dev_buf, int cta) {
   return e;
 }
 
-cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st) {
+cudaError_t launch_fill(int BH, int L, int d, const int* donor, Rows O, cudaStream_t st) {
   size_t total = static_cast<size_t>(BH) * L * (d / 8);
   k_fill<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, L, d, donor, O);
   return cudaGetLastError();

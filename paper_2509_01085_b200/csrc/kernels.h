@@ -10,14 +10,27 @@ namespace bsa {
 
 using bf16 = __nv_bfloat16;
 
+// A [B, Hh, L, d] bf16 tensor given by element strides (include/bsa.h bsa_tensor; d contiguous): element
+// (b, h, n, c) is p[b sb + h sh + n sl + c]. Kernels index heads by bh = b Hh + h.
+struct Rows {
+  bf16* p;
+  long long sb, sh, sl;
+  int Hh;
+  __host__ __device__ __forceinline__ bf16* head(int bh) const {
+    const int b = bh / Hh;
+    return p + b * sb + static_cast<long long>(bh - b * Hh) * sh;
+  }
+  __host__ __device__ __forceinline__ bf16* row(int bh, long long n) const { return head(bh) + n * sl; }
+};
+
 // a1 partition
 cudaError_t launch_partition(const Geo& g, double r, int* block_off, int* block_tok, int* block_ext, int* kept_off,
                              cudaStream_t st);
 // a2+a3 query selection (one pass over Q)
-cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, const bf16* Q, const int* kept_off,
+cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, Rows Q, const int* kept_off,
                                   int* kept_tok, int* donor, double* q_pooled, bf16* q_packed, cudaStream_t st);
 // a2 block pooling in fp64
-cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, cudaStream_t st);
+cudaError_t launch_pool(const Geo& g, int BH, int d, Rows X, double* Xc, cudaStream_t st);
 // a4 pooled block scores S[bh][i][j] = Qc[i].Kc[j] / sqrt(d)
 cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st);
 // a5+a6 threshold + admission per row; sets bit i of kvbits[bh][j] for every admitted (i, j)
@@ -28,16 +41,13 @@ cudaError_t launch_k2q(int N, int BH, const uint32_t* qbits, uint32_t* kvbits, i
                        cudaStream_t st);
 
 // gather Q^s rows (kept queries) into packed [BH, Lq, d]
-cudaError_t launch_gather_rows(int BH, int L, int Lq, int d, const bf16* X, const int* kept_tok, bf16* out,
-                               cudaStream_t st);
+cudaError_t launch_gather_rows(int BH, int Lq, int d, Rows X, const int* kept_tok, bf16* out, cudaStream_t st);
 
 // a7 forward: tcgen05 sparse attention over packed Q^s, then the donor fill
 struct FwdArgs {
   Geo g;
   int BH, d, Lq, SR;  // SR = query rows per slot (power of two >= max kept per block)
-  const bf16* Q;      // raster [BH, L, d]
-  const bf16* K;
-  const bf16* V;
+  Rows K, V;         // raster, strided
   const bf16* Qs;     // packed [BH, Lq, d]
   const int* kept_off;
   const int* kept_tok;
@@ -45,16 +55,15 @@ struct FwdArgs {
   const int* q2k_num;
   const int* q2k_idx;
   float scale;
-  bf16* O;
+  Rows O;
   float* lse;
   const uint8_t* kv_img;  // workspace: K|V block images (launch_kv_image)
 };
-cudaError_t launch_kv_image(const Geo& g, int BH, int d, const bf16* K, const bf16* V, uint8_t* img,
-                            cudaStream_t st);
+cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
 cudaError_t debug_trace_fwd(void* dev_buf, int cta);
 cudaError_t debug_trace_bwd(void* dev_buf, int cta);
-cudaError_t launch_fill(int BH, int L, int d, const int* donor, bf16* O, cudaStream_t st);
+cudaError_t launch_fill(int BH, int L, int d, const int* donor, Rows O, cudaStream_t st);
 
 // Ulysses sequence parallelism: row reorders around the all-to-all (sp.cu)
 cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, const void* src, void* dst,
@@ -63,12 +72,8 @@ cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, co
 // a8 backward
 struct BwdArgs {
   Geo g;
-  int BH, d, Lq, SR;
-  const bf16* Q;
-  const bf16* K;
-  const bf16* V;
-  const bf16* O;
-  const bf16* dO;
+  int B, Hh, BH, d, Lq, SR;
+  Rows K, V, O, dO;    // raster, strided
   const bf16* Qs;      // packed
   const int* kept_off;
   const int* kept_tok;
@@ -77,9 +82,7 @@ struct BwdArgs {
   const int* k2q_idx;
   const float* lse;
   float scale;
-  bf16* dQ;
-  bf16* dK;
-  bf16* dV;
+  Rows dQ, dK, dV;
   // workspace
   uint8_t* qdo_img;  // [BH, N] query-block images of Q^s|dO^s, SR*d*4 bytes each (k_bwd_prep)
   float* lsed;       // [BH, N, 2, SR]: per query block LSE*log2(e) of its SR rows, then D of its SR rows

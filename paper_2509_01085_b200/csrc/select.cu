@@ -194,7 +194,7 @@ __device__ __forceinline__ void block_gram(const bf16* sq, int DS, int BTp, floa
 #define BSA_SELQ_MIN_BLOCKS 6
 #endif
 template <int D>
-__global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo g, double r, int Lq, const bf16* __restrict__ Q,
+__global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo g, double r, int Lq, const Rows Q,
                                                         const int* __restrict__ kept_off, int* __restrict__ kept_tok,
                                                         int* __restrict__ donor, double* __restrict__ q_pooled,
                                                         bf16* __restrict__ q_packed) {
@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo
   const Box x = block_box(g, b);
   const int n = box_size(x);
   const size_t head = static_cast<size_t>(bh) * g.L;
+  const bf16* qh = Q.head(bh);
   for (int i = threadIdx.x; i < n; i += blockDim.x) tok[i] = box_token(g, x, i);
   __syncthreads();
   // rows -> smem (16-byte vectors)
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo
   for (int v = threadIdx.x; v < BTp * VPR; v += blockDim.x) {
     int i = v / VPR, c = (v % VPR) * 8;
     *reinterpret_cast<uint4*>(sq + i * DS + c) =
-        i < n ? *reinterpret_cast<const uint4*>(Q + (head + tok[i]) * D + c) : make_uint4(0, 0, 0, 0);
+        i < n ? *reinterpret_cast<const uint4*>(qh + tok[i] * Q.sl + c) : make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
   block_gram<D>(sq, DS, BTp, gram, GS);  // read by the donor search below (after later barriers)
@@ -359,7 +360,7 @@ static size_t select_smem(int BT, int D) {
   return BTp * (D + 8) * 2 + static_cast<size_t>(BT) * 16 + static_cast<size_t>(BT) * 6 * 4 + BTp * (BTp + 1) * 4;
 }
 
-cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, const bf16* Q, const int* kept_off,
+cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, Rows Q, const int* kept_off,
                                   int* kept_tok, int* donor, double* q_pooled, bf16* q_packed, cudaStream_t st) {
   dim3 grid(g.N, BH);
   size_t sm = select_smem(g.BT, d);
@@ -378,7 +379,7 @@ cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq,
 // Partial sums are fp64 sums of bf16 values, i.e. exact (bf16 has an 8-bit significand), so the
 // fixed-order combination below equals the sequential ascending-token sum of the oracle.
 template <int D>
-__global__ void __launch_bounds__(128) k_pool(Geo g, const bf16* __restrict__ X, double* __restrict__ Xc) {
+__global__ void __launch_bounds__(128) k_pool(Geo g, const Rows X, double* __restrict__ Xc) {
   constexpr int CH = D / 8;      // 8-channel chunks per row (16 or 8)
   constexpr int TG = 128 / CH;   // token groups (8 or 16)
   __shared__ double part[TG][D];
@@ -386,10 +387,10 @@ __global__ void __launch_bounds__(128) k_pool(Geo g, const bf16* __restrict__ X,
   const int ck = threadIdx.x % CH, tg = threadIdx.x / CH;
   const Box x = block_box(g, b);
   const int n = box_size(x);
-  const size_t head = static_cast<size_t>(bh) * g.L;
+  const bf16* xh = X.head(bh);
   double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = tg; i < n; i += TG) {
-    uint4 v = *reinterpret_cast<const uint4*>(X + (head + box_token(g, x, i)) * D + ck * 8);
+    uint4 v = *reinterpret_cast<const uint4*>(xh + box_token(g, x, i) * X.sl + ck * 8);
     const __nv_bfloat162* pv = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(128) k_pool(Geo g, const bf16* __restrict__ X,
   }
 }
 
-cudaError_t launch_pool(const Geo& g, int BH, int d, const bf16* X, double* Xc, cudaStream_t st) {
+cudaError_t launch_pool(const Geo& g, int BH, int d, Rows X, double* Xc, cudaStream_t st) {
   dim3 grid(g.N, BH);
   if (d == 128) k_pool<128><<<grid, 128, 0, st>>>(g, X, Xc);
   else k_pool<64><<<grid, 128, 0, st>>>(g, X, Xc);
@@ -849,8 +850,9 @@ cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double
   // ovf[0] = overflow count, ovf[1..] = overflow rows
   e = cudaMemsetAsync(ovf, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = min_i((rows + ADMIT_WARPS - 1) / ADMIT_WARPS, sms * 4);
   const int wsm = ADMIT_WARPS * (ADMIT_CAP * 12 + 128 * 4);
   e = cudaFuncSetAttribute(k_admit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
@@ -922,7 +924,7 @@ cudaError_t launch_k2q(int N, int BH, const uint32_t* qbits, uint32_t* kvbits, i
 }
 
 // ------------------------------------------------------------------------------------ gather
-__global__ void k_gather_rows(int BH, int L, int Lq, int d, const bf16* __restrict__ X, const int* __restrict__ kept_tok,
+__global__ void k_gather_rows(int BH, int Lq, int d, const Rows X, const int* __restrict__ kept_tok,
                               bf16* __restrict__ out) {
   size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int vpr = d / 8;
@@ -930,15 +932,14 @@ __global__ void k_gather_rows(int BH, int L, int Lq, int d, const bf16* __restri
   if (v >= rows * vpr) return;
   size_t prow = v / vpr;
   int c = static_cast<int>(v % vpr) * 8;
-  size_t bh = prow / Lq;
+  const int bh = static_cast<int>(prow / Lq);
   int tok = kept_tok[prow];
-  *reinterpret_cast<uint4*>(out + prow * d + c) = *reinterpret_cast<const uint4*>(X + (bh * L + tok) * d + c);
+  *reinterpret_cast<uint4*>(out + prow * d + c) = *reinterpret_cast<const uint4*>(X.row(bh, tok) + c);
 }
 
-cudaError_t launch_gather_rows(int BH, int L, int Lq, int d, const bf16* X, const int* kept_tok, bf16* out,
-                               cudaStream_t st) {
+cudaError_t launch_gather_rows(int BH, int Lq, int d, Rows X, const int* kept_tok, bf16* out, cudaStream_t st) {
   size_t total = static_cast<size_t>(BH) * Lq * (d / 8);
-  k_gather_rows<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, L, Lq, d, X, kept_tok, out);
+  k_gather_rows<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, Lq, d, X, kept_tok, out);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,10 @@
 //   RECV_TO_HEADS  [P][B][Hp][Ls][d]     -> [B][Hp][P Ls][d]    chunk s = sequence chunk s (BSA layout)
 //   HEADS_TO_SEND  [B][Hp][P Ls][d]      -> [P][B][Hp][Ls][d]   chunk s = sequence chunk s (fwd: O; bwd: dQ, dK, dV)
 //   RECV_TO_SEQ    [P][B][Hp][Ls][d]     -> [B][Ls][Hh][d]      chunk p = head group p (back to the model)
+//   SEQ_TO_SEND_T  [B][Ls][Hh][d]        -> [P][B][Ls][Hp][d]   token-major chunks (B = 1: what arrives is the
+//                                                                whole sequence of Hp heads as [L][Hp][d], a
+//                                                                strided [1, Hp, L, d] view BSA reads in place)
+//   RECV_T_TO_SEQ  [P][B][Ls][Hp][d]     -> [B][Ls][Hh][d]      back to the model from token-major chunks
 //
 // Pure data movement, HBM-bound: one 16-byte vector per thread, destination-ordered so the writes are
 // fully coalesced and every source row (2 d bytes, >= 128 B) is read as whole sectors.
@@ -44,13 +48,28 @@ __global__ void __launch_bounds__(256) k_sp_relayout(int B, int Ls, int Hh, int 
     const int h = static_cast<int>(t % Hp), b = static_cast<int>(t / Hp);
     const int s = static_cast<int>(n / Ls), l = static_cast<int>(n % Ls);
     srow = ((static_cast<size_t>(s) * B + b) * Hp + h) * Ls + l;
-  } else {
+  } else if (MODE == 3) {
     // dst [B][Ls][Hh]  <-  src [P][B][Hp][Ls]
     const int hh = static_cast<int>(row % Hh);
     const size_t t = row / Hh;
     const int l = static_cast<int>(t % Ls), b = static_cast<int>(t / Ls);
     const int p = hh / Hp, h = hh % Hp;
     srow = ((static_cast<size_t>(p) * B + b) * Hp + h) * Ls + l;
+  } else if (MODE == 4) {
+    // dst [P][B][Ls][Hp]  <-  src [B][Ls][Hh]
+    const int h = static_cast<int>(row % Hp);
+    size_t t = row / Hp;
+    const int l = static_cast<int>(t % Ls);
+    t /= Ls;
+    const int b = static_cast<int>(t % B), p = static_cast<int>(t / B);
+    srow = (static_cast<size_t>(b) * Ls + l) * Hh + static_cast<size_t>(p) * Hp + h;
+  } else {
+    // dst [B][Ls][Hh]  <-  src [P][B][Ls][Hp]
+    const int hh = static_cast<int>(row % Hh);
+    const size_t t = row / Hh;
+    const int l = static_cast<int>(t % Ls), b = static_cast<int>(t / Ls);
+    const int p = hh / Hp, h = hh % Hp;
+    srow = ((static_cast<size_t>(p) * B + b) * Ls + l) * Hp + h;
   }
   dst[row * vpr + c] = src[srow * vpr + c];
 }
@@ -67,7 +86,9 @@ cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, co
     case 0: k_sp_relayout<0><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
     case 1: k_sp_relayout<1><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
     case 2: k_sp_relayout<2><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
-    default: k_sp_relayout<3><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
+    case 3: k_sp_relayout<3><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
+    case 4: k_sp_relayout<4><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
+    default: k_sp_relayout<5><<<blocks, 256, 0, st>>>(B, Ls, Hh, P, vpr, s, o, total); break;
   }
   return cudaGetLastError();
 }

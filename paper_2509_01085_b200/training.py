@@ -10,7 +10,8 @@ forward/backward and the paper's annealed sparsity schedule (§4 Implem
 
 Selection (Eq.2-Eq.4) is piecewise constant in Q and K and is held fixed in the backward (reading C10);
 the gradients are those of bsa_attn_bwd. Every step runs in libbsa's kernels; this module only keeps a
-BSAAttention per (r, k, tau) setting and allocates the tensors autograd hands out.
+BSAAttention per query keep ratio r (the only knob that changes buffer sizes; k and tau are set per call) and
+allocates the tensors autograd hands out.
 """
 
 from __future__ import annotations
@@ -69,10 +70,13 @@ class AnnealSchedule:
 class _BSAFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, Q, K, V, layer):
-        O = torch.empty_like(Q)
+        B, Hh, L, d = Q.shape
+        O = torch.empty(B, Hh, L, d, dtype=Q.dtype, device=Q.device)
         layer.forward(Q, K, V, out=O)
         layer._fwd_count = getattr(layer, "_fwd_count", 0) + 1
         ctx.layer, ctx.count = layer, layer._fwd_count
+        # saved through autograd: an in-place edit of Q, K, V or O before backward raises a version error
+        ctx.save_for_backward(Q, K, V, O)
         return O
 
     @staticmethod
@@ -81,8 +85,12 @@ class _BSAFunction(torch.autograd.Function):
         if layer._fwd_count != ctx.count:
             raise BSAError("BSA backward after another forward through the same layer: the layer holds the "
                            "selection and statistics of its last forward only (use one layer per call site)")
-        grads = tuple(torch.empty_like(dO) for _ in range(3))
-        layer.backward(dO.contiguous(), out=grads)
+        Q, K, V, O = ctx.saved_tensors
+        if dO.stride(-1) != 1:
+            dO = dO.contiguous()
+        B, Hh, L, d = Q.shape
+        grads = tuple(torch.empty(B, Hh, L, d, dtype=Q.dtype, device=Q.device) for _ in range(3))
+        layer.backward(dO, out=grads, saved=(Q, K, V, O))
         return (*grads, None)
 
 
@@ -110,16 +118,16 @@ class BSASelfAttention(torch.nn.Module):
     def _layer(self):
         from .runner import BSAAttention
         N = bsa_sizes(self.geom, self.r)[0]
-        key = (self.r, resolve_k(self.f, N), self.tau)
-        lay = self._layers.get(key)
+        lay = self._layers.get(self.r)
         if lay is None:
-            # one preallocated layer per (r, k, tau) setting; a schedule visits at most ~cap/increment of them,
-            # older ones are dropped to bound memory
-            if len(self._layers) >= 4:
+            # buffers depend on r only (k and tau are per-call knobs); the schedule moves r monotonically, so at
+            # most the current and the previous layer are kept
+            while len(self._layers) >= 2:
                 self._layers.pop(next(iter(self._layers)))
-            lay = BSAAttention(self.geom, key[0], key[1], key[2], self.B, self.Hh, self.d, device=self.device,
+            lay = BSAAttention(self.geom, self.r, 1.0, 1.0, self.B, self.Hh, self.d, device=self.device,
                                scale=1.0 / math.sqrt(self.d))
-            self._layers[key] = lay
+            self._layers[self.r] = lay
+        lay.set_knobs(resolve_k(self.f, N), self.tau)
         return lay
 
     def forward(self, Q, K, V):

@@ -7,8 +7,13 @@ So, as in Ulysses, one all-to-all per tensor regathers the sequence per head gro
 [p Hp, (p+1) Hp), Hp = Hh/P), BSA runs locally and unchanged on [B, Hp, L, d], and one all-to-all per
 output returns to the token-sharded layout:
 
+    B = 1 (the long-video config): token-major chunks, one reorder per direction
+    forward : Q, K, V  --SEQ_TO_SEND_T, a2a-->  [L][Hp][d] read in place as a strided [1, Hp, L, d] bsa_tensor
+              BSAAttention writes O in that same layout = the send buffer  --a2a, RECV_T_TO_SEQ-->  O [1, Ls, Hh, d]
+    backward: dO like Q; dQ, dK, dV like O
+    B > 1: head-major chunks, two reorders per direction
     forward : Q, K, V  --SEQ_TO_SEND, a2a, RECV_TO_HEADS-->  BSAAttention.forward  --HEADS_TO_SEND, a2a, RECV_TO_SEQ-->  O
-    backward: dO       --(same as Q)-->                      BSAAttention.backward --(same as O)-->  dQ, dK, dV
+    P = 1: no exchange and no reorder at all: [B, L, Hh, d] is passed as the strided view x.transpose(1, 2).
 
 The reorders are libbsa kernels (bsa_sp_relayout, csrc/sp.cu); the exchange is
 torch.distributed.all_to_all_single (NCCL over NVLink/NVSwitch on GPUs; gloo in the CPU tests).
@@ -25,7 +30,8 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-from . import SP_HEADS_TO_SEND, SP_RECV_TO_HEADS, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND, BSAError, Geometry, bsa_sp_relayout
+from . import (SP_HEADS_TO_SEND, SP_RECV_T_TO_SEQ, SP_RECV_TO_HEADS, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND, SP_SEQ_TO_SEND_T,
+               BSAError, Geometry, bsa_sp_relayout)
 
 
 def _cuda_relayout(mode, src, dst, B, Ls, Hh, d, P):
@@ -34,7 +40,8 @@ def _cuda_relayout(mode, src, dst, B, Ls, Hh, d, P):
 
 class UlyssesBSA:
     """BSA over a token-sharded sequence. `attention` is the per-rank layer on Hp heads (default:
-    runner.BSAAttention); `relayout` is the row-reorder primitive (default: the libbsa kernel)."""
+    runner.BSAAttention; it must accept strided [B, Hp, L, d] views and an `out` tensor); `relayout` is the
+    row-reorder primitive (default: the libbsa kernel)."""
 
     def __init__(self, geom: Geometry, r: float, f, tau: float, B: int, Hh: int, d: int, group=None, device="cuda",
                  attention=None, relayout: Callable | None = None, dtype=torch.bfloat16):
@@ -48,61 +55,84 @@ class UlyssesBSA:
         self.g, self.B, self.Hh, self.d = geom, B, Hh, d
         self.Hp, self.Ls = Hh // self.P, geom.L // self.P
         self.device = torch.device(device)
+        self.dtype = dtype
         if attention is None:
             from .runner import BSAAttention
             attention = BSAAttention(geom, r, f, tau, B, self.Hp, d, device=self.device)
         self.layer = attention
         self._relayout = relayout or _cuda_relayout
-        n = B * self.Ls * Hh * d
+        # token-major exchange (B == 1) needs no reorder on the BSA side; B > 1 uses head-major chunks
+        self.token_major = B == 1
+        n = B * self.Ls * Hh * d if self.P > 1 else 0
         mk = dict(dtype=dtype, device=self.device)
-        # per exchanged tensor: send / receive buffers (flat [P][B][Hp][Ls][d]) and the head-layout result
-        # (P = 1: the head layout is reached by one reorder, no exchange buffers)
-        nx = n if self.P > 1 else 0
-        self._send = [torch.empty(nx, **mk) for _ in range(3)]
-        self._recv = [torch.empty(nx, **mk) for _ in range(3)]
-        self._heads = [torch.empty(B, self.Hp, geom.L, d, **mk) for _ in range(3)]
-        # dO gets its own buffers: Q^h, K^h, V^h stay saved for the backward
-        self._dO_bufs = (torch.empty(nx, **mk), torch.empty(nx, **mk), torch.empty(B, self.Hp, geom.L, d, **mk))
+        # per exchanged input (Q, K, V, dO): send and receive buffers, flat [P][chunk]
+        self._send = [torch.empty(n, **mk) for _ in range(4)]
+        self._recv = [torch.empty(n, **mk) for _ in range(4)]
+        # per output (O, dQ, dK, dV): the tensor BSA writes (= the send buffer when token-major) and the receive buffer
+        self._out = [torch.empty(n, **mk) for _ in range(4)]
+        self._out_recv = [torch.empty(n, **mk) for _ in range(4)]
+        nh = B * self.Hp * geom.L * d if (self.P > 1 and not self.token_major) else 0
+        self._heads = [torch.empty(nh, **mk) for _ in range(4)]  # B > 1: head-major [B][Hp][L][d] inputs
 
     # ---------------------------------------------------------------- exchanges
     def _a2a(self, recv, send, async_op=False):
-        if self.P == 1:
-            recv.copy_(send)
-            return None
         return dist.all_to_all_single(recv, send, group=self.group, async_op=async_op)
 
+    def _check(self, x, what):
+        if tuple(x.shape) != (self.B, self.Ls, self.Hh, self.d):
+            raise BSAError(f"Ulysses: {what} must be [B, Ls, Hh, d] = {(self.B, self.Ls, self.Hh, self.d)}, "
+                           f"got {tuple(x.shape)}")
+
+    def _heads_view(self, flat):
+        """[L][Hp][d] (token-major, B = 1) -> strided [1, Hp, L, d]; [B][Hp][L][d] -> [B, Hp, L, d]."""
+        if self.token_major:
+            return flat.view(1, self.g.L, self.Hp, self.d).transpose(1, 2)
+        return flat.view(self.B, self.Hp, self.g.L, self.d)
+
     def _send_heads(self, i, x):
-        """[B, Ls, Hh, d] (this rank's tokens) -> async exchange into slot i; returns the work handle."""
-        if x.shape != (self.B, self.Ls, self.Hh, self.d):
-            raise BSAError(f"Ulysses: expected [B, Ls, Hh, d] = {(self.B, self.Ls, self.Hh, self.d)}, got {tuple(x.shape)}")
-        if self.P == 1:  # [1][B][Hh][L][d] is already the head layout: no exchange, no second reorder
-            self._relayout(SP_SEQ_TO_SEND, x.contiguous(), self._heads[i], self.B, self.Ls, self.Hh, self.d, 1)
-            return None
-        self._relayout(SP_SEQ_TO_SEND, x.contiguous(), self._send[i], self.B, self.Ls, self.Hh, self.d, self.P)
+        """[B, Ls, Hh, d] (this rank's tokens) -> (async) exchange into slot i; returns the work handle."""
+        self._check(x, "input")
+        mode = SP_SEQ_TO_SEND_T if self.token_major else SP_SEQ_TO_SEND
+        self._relayout(mode, x.contiguous(), self._send[i], self.B, self.Ls, self.Hh, self.d, self.P)
         return self._a2a(self._recv[i], self._send[i], async_op=True)
 
     def _recv_heads(self, i, work):
-        if self.P == 1:
-            return self._heads[i]
         if work is not None:
             work.wait()
+        if self.token_major:
+            return self._heads_view(self._recv[i])
         self._relayout(SP_RECV_TO_HEADS, self._recv[i], self._heads[i], self.B, self.Ls, self.Hh, self.d, self.P)
-        return self._heads[i]
+        return self._heads_view(self._heads[i])
 
-    def _to_seq(self, x, i=0):
-        """[B, Hp, L, d] (this rank's heads) -> [B, Ls, Hh, d] (this rank's tokens, all heads)."""
+    def _out_view(self, i):
+        """Where BSA writes output i: token-major, it is the send buffer of the return exchange itself."""
+        return self._heads_view(self._out[i]) if self.token_major else \
+            self._out[i].new_empty(self.B, self.Hp, self.g.L, self.d)
+
+    def _to_seq(self, i, x):
+        """BSA output i (the _out_view tensor x) -> [B, Ls, Hh, d] (this rank's tokens, all heads)."""
         out = torch.empty(self.B, self.Ls, self.Hh, self.d, dtype=x.dtype, device=x.device)
-        if self.P == 1:  # x is [1][B][Hh][L][d]: one reorder back to the model layout
-            self._relayout(SP_RECV_TO_SEQ, x.contiguous(), out, self.B, self.Ls, self.Hh, self.d, 1)
-            return out
-        self._relayout(SP_HEADS_TO_SEND, x.contiguous(), self._send[i], self.B, self.Ls, self.Hh, self.d, self.P)
-        self._a2a(self._recv[i], self._send[i])
-        self._relayout(SP_RECV_TO_SEQ, self._recv[i], out, self.B, self.Ls, self.Hh, self.d, self.P)
+        if self.token_major:
+            send, mode = self._out[i], SP_RECV_T_TO_SEQ
+        else:
+            self._relayout(SP_HEADS_TO_SEND, x.contiguous(), self._out[i], self.B, self.Ls, self.Hh, self.d, self.P)
+            send, mode = self._out[i], SP_RECV_TO_SEQ
+        self._a2a(self._out_recv[i], send)
+        self._relayout(mode, self._out_recv[i], out, self.B, self.Ls, self.Hh, self.d, self.P)
         return out
 
     # ---------------------------------------------------------------- layer
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
         """q, k, v: [B, Ls, Hh, d] token shards -> O [B, Ls, Hh, d]."""
+        if self.P == 1:  # the model layout is a strided [B, Hh, L, d] view: nothing to move
+            for x, w in ((q, "q"), (k, "k"), (v, "v")):
+                self._check(x, w)
+            O = torch.empty(self.B, self.Ls, self.Hh, self.d, dtype=q.dtype, device=q.device)
+            Qh, Kh, Vh = (x.transpose(1, 2) for x in (q, k, v))
+            self.layer.select(Qh, Kh)
+            self.layer._saved = (Qh, Kh, Vh)
+            self.layer.attend(Qh, Kh, Vh, out=O.transpose(1, 2))
+            return O
         wq = self._send_heads(0, q)
         wk = self._send_heads(1, k)
         wv = self._send_heads(2, v)
@@ -111,20 +141,17 @@ class UlyssesBSA:
         self.layer.select(Qh, Kh)            # a1-a6 run while V is in flight
         Vh = self._recv_heads(2, wv)
         self.layer._saved = (Qh, Kh, Vh)
-        O = self.layer.attend(Qh, Kh, Vh)    # a7 + fill
-        return self._to_seq(O)
+        O = self.layer.attend(Qh, Kh, Vh, out=self._out_view(0))    # a7 + fill
+        return self._to_seq(0, O)
 
     def backward(self, dO: torch.Tensor):
         """dO: [B, Ls, Hh, d] -> (dQ, dK, dV), each [B, Ls, Hh, d]."""
-        s, r, h = self._dO_bufs
-        if dO.shape != (self.B, self.Ls, self.Hh, self.d):
-            raise BSAError("Ulysses: dO must be [B, Ls, Hh, d]")
+        self._check(dO, "dO")
         if self.P == 1:
-            self._relayout(SP_SEQ_TO_SEND, dO.contiguous(), h, self.B, self.Ls, self.Hh, self.d, 1)
-        else:
-            self._relayout(SP_SEQ_TO_SEND, dO.contiguous(), s, self.B, self.Ls, self.Hh, self.d, self.P)
-            self._a2a(r, s)
-            self._relayout(SP_RECV_TO_HEADS, r, h, self.B, self.Ls, self.Hh, self.d, self.P)
-        dQ, dK, dV = self.layer.backward(h)
-        # the send/recv slots of Q, K, V are free again (their head layouts live in self._heads)
-        return self._to_seq(dQ, 0), self._to_seq(dK, 1), self._to_seq(dV, 2)
+            outs = [torch.empty(self.B, self.Ls, self.Hh, self.d, dtype=dO.dtype, device=dO.device) for _ in range(3)]
+            self.layer.backward(dO.transpose(1, 2), out=tuple(x.transpose(1, 2) for x in outs))
+            return tuple(outs)
+        dOh = self._recv_heads(3, self._send_heads(3, dO))
+        grads = [self._out_view(i) for i in (1, 2, 3)]
+        grads = self.layer.backward(dOh, out=tuple(grads))
+        return tuple(self._to_seq(i, x) for i, x in zip((1, 2, 3), grads))

@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the parity records (tests/parity_util.RECORDS) to $BSA_PARITY_OUT, if set."""
+    out = os.environ.get("BSA_PARITY_OUT")
+    if not out:
+        return
+    try:
+        import json
+
+        import parity_util
+    except Exception:  # pragma: no cover
+        return
+    if not parity_util.RECORDS:
+        return
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    with open(out, "w") as f:
+        json.dump({"exitstatus": int(exitstatus), "records": parity_util.RECORDS}, f, indent=1)

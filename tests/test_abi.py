@@ -2,6 +2,7 @@
 include/bsa.h declares, and its host-only logic (sizes, workspace sizing, validation) is right."""
 
 import ctypes
+import math
 import os
 import re
 
@@ -21,7 +22,7 @@ def built():
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "bsa.h")).read()
-    return sorted(set(re.findall(r"\b(bsa_[a-z_0-9]+)\s*\(", text)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(bsa_[a-z_0-9]+)\s*\(", text, re.M)))
 
 
 def test_exports_every_header_symbol():
@@ -83,23 +84,25 @@ def test_validation_errors_before_any_launch():
     assert L.bsa_sizes(ctypes.byref(zero.c()), 0.5, None, None, None) == 1
     n = ctypes.c_size_t()
     assert L.bsa_workspace_bytes(2, ctypes.byref(g.c()), 0.5, 1, 2, 96, ctypes.byref(n)) == 1  # d unsupported
+    T = bsa._CTensor
+    t16 = T(256, 2 * 256 * 64, 256 * 64, 64)  # a well-formed contiguous [1, 2, 256, 64] descriptor (never read)
     # select_kv: k out of range -> CONFIG before any device access
-    rc = L.bsa_select_kv_blocks(ctypes.byref(g.c()), 1, 2, 64, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 0, 0.9,
+    rc = L.bsa_select_kv_blocks(ctypes.byref(g.c()), 1, 2, 64, t16, None, t16, 0, 0.9,
                                 ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None, ctypes.c_void_p(16), 1 << 30,
                                 None)
     assert rc == 2 and b"k must be" in L.bsa_last_error()
-    rc = L.bsa_select_kv_blocks(ctypes.byref(g.c()), 1, 2, 64, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 3, 1.5,
+    rc = L.bsa_select_kv_blocks(ctypes.byref(g.c()), 1, 2, 64, t16, None, t16, 3, 1.5,
                                 ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None, ctypes.c_void_p(16), 1 << 30,
                                 None)
     assert rc == 2 and b"tau" in L.bsa_last_error()
     # attention with an unsupported block size
     g3 = bsa.Geometry(4, 8, 8, 1, 2, 2)
-    rc = L.bsa_attn_fwd(ctypes.byref(g3.c()), 0.5, 1, 1, 64, *([ctypes.c_void_p(256)] * 9), ctypes.c_float(0.1),
-                        ctypes.c_void_p(256), ctypes.c_void_p(256), None, 0, None)
+    rc = L.bsa_attn_fwd(ctypes.byref(g3.c()), 0.5, 1, 1, 64, t16, t16, t16, *([ctypes.c_void_p(256)] * 6),
+                        ctypes.c_float(0.1), t16, ctypes.c_void_p(256), None, 0, None)
     assert rc == 1 and b"ct*ch*cw" in L.bsa_last_error()
     assert L.bsa_strerror(4) == b"unsupported device (needs sm_100a)"
     # selection variant: unknown KV mode -> CONFIG
-    rc = L.bsa_select_kv_blocks_ex(ctypes.byref(g.c()), 1, 2, 64, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 3,
+    rc = L.bsa_select_kv_blocks_ex(ctypes.byref(g.c()), 1, 2, 64, t16, None, t16, 3,
                                    0.9, 7, ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None,
                                    ctypes.c_void_p(16), 1 << 30, None)
     assert rc == 2 and b"KV mode" in L.bsa_last_error()
@@ -109,6 +112,39 @@ def test_validation_errors_before_any_launch():
     assert L.bsa_sp_relayout(0, 1, 16, 8, 12, 4, ctypes.c_void_p(256), ctypes.c_void_p(512), None) == 1
     assert L.bsa_sp_relayout(0, 1, 16, 8, 128, 4, ctypes.c_void_p(258), ctypes.c_void_p(512), None) == 1
     assert L.bsa_sp_relayout(9, 1, 16, 8, 128, 4, ctypes.c_void_p(256), ctypes.c_void_p(512), None) == 2
+
+
+def test_strided_tensor_validation():
+    """bsa_tensor checks (include/bsa.h): 16-byte aligned pointer, strides non-negative multiples of 8 elements,
+    token stride >= d -> BSA_ERR_INVALID_SHAPE before any device access; a NULL required tensor -> SELECTION_MISMATCH."""
+    L = bsa.lib()
+    T = bsa._CTensor
+    g = bsa.Geometry(4, 8, 8, 2, 4, 4)
+    out = (ctypes.c_int32 * 16)()
+    ok = T(256, 2 * 256 * 64, 256 * 64, 64)
+    bshd = T(256, 256 * 2 * 64, 64, 2 * 64)  # a model's [B, L, Hh, d] layout: accepted
+    bad = {"misaligned": T(258, 2 * 256 * 64, 256 * 64, 64), "stride_not_8": T(256, 2 * 256 * 64, 256 * 64, 68),
+           "sl_lt_d": T(256, 2 * 256 * 64, 256 * 64, 32), "negative": T(256, -8, 256 * 64, 64)}
+    for name, t in bad.items():
+        rc = L.bsa_select_queries(ctypes.byref(g.c()), 0.5, 1, 2, 64, t, out, out, out, None, None, None)
+        assert rc == 1, name
+    rc = L.bsa_select_queries(ctypes.byref(g.c()), 0.5, 1, 2, 64, T(None, 0, 0, 0), out, out, out, None, None, None)
+    assert rc == 3 and b"NULL" in L.bsa_last_error()
+    # well-formed descriptors pass validation (the call then fails on the missing device, not on the shapes)
+    for t in (ok, bshd):
+        rc = L.bsa_select_queries(ctypes.byref(g.c()), 0.5, 1, 2, 64, t, out, out, out, None, None, None)
+        assert rc not in (1, 2, 3), L.bsa_last_error()
+
+
+def test_tensor_desc_strides():
+    """The binding's descriptor of a [B, L, Hh, d] tensor viewed as [B, Hh, L, d] carries the model layout's strides."""
+    import torch
+    x = torch.empty(2, 100, 3, 64, dtype=torch.bfloat16)  # [B, L, Hh, d]
+    v = x.transpose(1, 2)
+    assert (v.stride(0), v.stride(1), v.stride(2), v.stride(3)) == (100 * 3 * 64, 64, 3 * 64, 1)
+    qkv = torch.empty(1, 100, 3, 4, 64, dtype=torch.bfloat16)  # fused [B, L, 3, Hh, d] projection
+    q = qkv[:, :, 0].transpose(1, 2)
+    assert (q.stride(0), q.stride(1), q.stride(2)) == (100 * 3 * 4 * 64, 64, 3 * 4 * 64)
 
 
 def test_workspace_sizes_monotone():
@@ -121,15 +157,54 @@ def test_workspace_sizes_monotone():
 
 
 def test_host_quantile_matches_stdlib():
-    """The library's host Phi^-1 (Acklam + Halley) agrees with statistics.NormalDist; exercised
-    through bsa_select_kv_blocks' thresholds on the GPU, checked here via a tiny C shim-free path:
-    the oracle's bisection and the stdlib agree (pinned in test_oracle_pins), so we compare the
-    threshold the GPU reports in the gpu tests. Here: stdlib vs oracle at the BASELINE k fractions."""
+    """The library's own Eq.3 quantile (bsa_kv_quantile: Acklam + Halley on the host, reading C14) against
+    statistics.NormalDist, an independent stdlib routine, at every k of the BASELINE geometries' N and at the
+    clamped ends 1/(2N), 1 - 1/(2N)."""
     import statistics
+    nd = statistics.NormalDist()
+    for N in (8, 100, 624, 1440, 2640, 4096):
+        ks = sorted(set([1, 2, N // 2, N - 1, N] + list(range(1, N + 1, max(1, N // 97)))))
+        for k in ks:
+            u = min(max(1 - k / N, 1 / (2 * N)), 1 - 1 / (2 * N))
+            z = bsa.kv_quantile(k, N)
+            ref = nd.inv_cdf(u)
+            assert abs(z - ref) <= 1e-12 * max(1.0, abs(ref)), (k, N, z, ref)
+    assert bsa.kv_quantile(312, 624) == 0.0  # u = 1/2 exactly
+    with pytest.raises(bsa.BSAError):
+        bsa.kv_quantile(0, 8)
+    with pytest.raises(bsa.BSAError):
+        bsa.kv_quantile(9, 8)
+
+
+def test_resolve_k_rounding_rule():
+    """Reading C6 behind the ABI (bsa_resolve_k): k = clamp(ceil(f N - 1e-9), 1, N), checked against exact rational
+    arithmetic (fractions.Fraction) where plain float ceil goes wrong (0.07 * 100, 0.55 * 1440)."""
+    from fractions import Fraction
+    assert bsa.resolve_k(0.07, 100) == 7 and math.ceil(0.07 * 100) == 8
+    assert bsa.resolve_k(0.55, 1440) == 792
+    assert bsa.resolve_k(0.1, 624) == 63 and bsa.resolve_k(0.1, 1440) == 144 and bsa.resolve_k(0.1, 2640) == 264
+    assert bsa.resolve_k(1e-9, 624) == 1 and bsa.resolve_k(1.0, 624) == 624
     for N in (8, 624, 1440, 2640):
-        for f in (0.1, 0.5, 0.9):
-            k = bsa.resolve_k(f, N)
-            if k >= N:
-                continue
-            u = 1 - k / N
-            assert abs(orc.normal_quantile(u) - statistics.NormalDist().inv_cdf(u)) < 1e-12
+        for num in range(1, 100):
+            f = num / 100
+            exact = -((-Fraction(num, 100) * N) // 1)  # ceil of the exact rational f N
+            assert bsa.resolve_k(f, N) == max(1, min(N, exact)), (f, N)
+    for bad in (0.0, -0.1, 1.5):
+        with pytest.raises(bsa.BSAError):
+            bsa.resolve_k(bad, 624)
+
+
+def test_selection_rejects_more_than_4096_blocks():
+    """N > 4096 is rejected by bsa_select_kv_blocks(_ex) with BSA_ERR_INVALID_SHAPE before any device access
+    (the admission bitmaps and the attention kernels' lists are sized for N <= 4096; include/bsa.h)."""
+    L = bsa.lib()
+    g = bsa.Geometry(41, 45, 80, 2, 2, 4)  # 21 x 23 x 20 = 9660 blocks
+    assert bsa.bsa_sizes(g, 0.5)[0] > 4096
+    for fn in ("bsa_select_kv_blocks", "bsa_select_kv_blocks_ex"):
+        t = bsa._CTensor(256, 2 * g.L * 64, g.L * 64, 64)
+        args = [ctypes.byref(g.c()), 1, 2, 64, t, None, t, 3, 0.9]
+        if fn.endswith("_ex"):
+            args.append(0)
+        args += [ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None, ctypes.c_void_p(16), 1 << 40, None]
+        rc = getattr(L, fn)(*args)
+        assert rc == 1 and b"4096" in L.bsa_last_error(), fn

@@ -549,3 +549,98 @@ def test_unified_brute_force_and_monotone(seed):
         if prev is not None:  # larger k: smaller quantile, smaller p, never more blocks (C28)
             assert (num <= prev).all()
         prev = num
+
+
+# ----------------------------------------------------------------------------- near-tie margins (C24)
+# The GPU-vs-oracle protocol excuses a selection disagreement only when the oracle's own decision margin is
+# below 1e-6. These pins tie the margins to closed forms on the worked examples, so a margin
+# that came out ~0 (turning real mismatches into "near-ties") or too large fails here.
+def _deg_cos(a):
+    return math.cos(math.radians(a))
+
+
+def test_query_margins_worked_example_E_q():
+    """E_q (Eq.2): unit gap at the keep cut = c_(5th) - c_(4th) of the ascending cosines =
+    cos 45 - cos 60 = (sqrt 2 - 1)/2 for every token of the unit; donor margin of a pruned token p = best - second
+    best of cos(theta_p - theta_j) over the kept j (angles 90, 60, 170, 120); kept tokens: no margin (DBL_MAX)."""
+    e = GOLD["E_q"]
+    g = orc.Geom(2, 2, 2, 2, 2, 2)
+    ang = e["angles_deg_offsets_0_to_6"] + [0.0]  # offset 7 = the centre, at 0 degrees
+    Q = _unit_vectors(ang)[None]
+    s = orc.select_queries(g, e["r"], Q)
+    gap = (math.sqrt(2.0) - 1.0) / 2.0
+    assert np.allclose(s["unit_margin"][0], gap, rtol=0, atol=1e-12)
+    kept_angles = [ang[t] for t in e["kept"]]
+    for t in e["pruned"]:
+        c = sorted((_deg_cos(ang[t] - a) for a in kept_angles), reverse=True)
+        assert abs(s["donor_margin"][0, t] - (c[0] - c[1])) < 1e-12, t
+    for t in e["kept"]:
+        assert s["donor_margin"][0, t] > 1e300
+    # closed forms spelled out: 10 deg -> cos 50 - cos 80, 30 -> cos 30 - cos 60, 45 -> cos 15 - cos 45, centre -> cos 60
+    assert abs(s["donor_margin"][0, 1] - (_deg_cos(50) - _deg_cos(80))) < 1e-12
+    assert abs(s["donor_margin"][0, 7] - 0.5) < 1e-12
+
+
+def test_query_margins_vanish_on_exact_ties():
+    """An exact cosine tie at the keep cut (S:219's example) has unit margin 0, and a pruned token equidistant
+    from two kept tokens has donor margin 0: both would be counted as near-ties, never as mismatches."""
+    g = orc.Geom(1, 1, 4, 1, 1, 4)  # centre local offset 2
+    Q = np.array([[[1.0, 3.0], [1.0, -3.0], [1.0, 0.0], [1.0, 3.0]]])
+    s = orc.select_queries(g, 0.5, Q)
+    # ascending cosines: c0 = c1 = c3 < c2 = 1; the cut between the 2nd and 3rd is a tie
+    assert s["unit_margin"][0].tolist() == [0.0] * 4
+    assert s["donor_margin"][0, 2] == 0.0  # cos(q2, q0) == cos(q2, q1)
+    assert s["donor_margin"][0, 3] > 0.5  # q3 == q0: cos 1 vs cos(q0, q1) = -0.8
+
+
+def _kv_margins(k, tau):
+    out = _kv_from_row(GOLD["E_kv"]["s"], k, tau)
+    return out["thr_margin"][0, 0], out["mass_margin"][0, 0], out["order_margin"][0, 0]
+
+
+def test_kv_margins_worked_example_E_kv():
+    """E_kv (Eq.3, Eq.4) on s = (2,1,0,-1), sigma = sqrt(5)/2, p = 1/2 + sigma z_k with z from
+    statistics.NormalDist (independent): thr margin = min_j |s_j - p| / max(|s_j|, |p|, sigma); mass margin = the
+    smaller distance of the cumulative exp mass to tau E on either side of the cut, / E; order margin =
+    (s_(l) - s_(l+1)) / max(sigma, |s_(l+1)|) between the last admitted and the first rejected candidate."""
+    s = np.array(GOLD["E_kv"]["s"], float)
+    sig = math.sqrt(5.0) / 2.0
+    nd = statistics.NormalDist()
+    BIG = 1e300
+    for k in (1, 2, 3):
+        p = 0.5 + sig * nd.inv_cdf(1 - k / 4)
+        want = min(abs(sj - p) / max(abs(sj), abs(p), sig) for sj in s)
+        assert abs(_kv_margins(k, 0.9)[0] - want) < 1e-12, k
+    assert _kv_margins(4, 0.9)[0] > BIG  # k = N: no threshold (C15)
+    # closed forms: k = 2 -> p = 1/2, margin 1/(2 sigma) = 1/sqrt 5; k = 1 -> (p - 1)/p
+    assert abs(_kv_margins(2, 0.9)[0] - 1 / math.sqrt(5)) < 1e-12
+    e = [math.exp(-t) for t in range(4)]  # exp(s - max) in sorted order
+    cases = [  # (k, tau, admitted l, candidates)
+        (1, 0.7, 1, 1), (1, 0.9, 1, 1), (2, 0.7, 1, 2), (2, 0.9, 2, 2), (3, 0.7, 2, 3), (3, 0.9, 2, 3),
+        (4, 0.7, 2, 4), (4, 0.9, 3, 4)]
+    for k, tau, ell, nc in cases:
+        E = sum(e[:nc])
+        cum, prev = sum(e[:ell]), sum(e[:ell - 1])
+        mass = abs(cum - tau * E) / E if ell == 1 else min(abs(cum - tau * E), abs(prev - tau * E)) / E
+        order = (s[ell - 1] - s[ell]) / max(sig, abs(s[ell])) if ell < nc else None
+        thr, mm, om = _kv_margins(k, tau)
+        assert abs(mm - mass) < 1e-12, (k, tau, mm, mass)
+        if order is None:
+            assert om > BIG
+        else:
+            assert abs(om - order) < 1e-12, (k, tau)
+    # tau = 1: the whole candidate set, no mass cut (C18)
+    assert _kv_margins(3, 1.0)[1] > BIG and _kv_margins(3, 1.0)[2] > BIG
+
+
+def test_kv_margins_vanish_on_exact_ties():
+    """A score exactly at the threshold p has thr margin 0; two candidates with equal score at the admission cut
+    have order margin 0; a cumulative mass exactly at tau E has mass margin 0."""
+    # s = (1, -1): mu = 0, k = N/2 -> p = mu = 0 ... make a score sit exactly on p: s = (1, 0, -1), k with z = 0
+    # needs k/N = 1/2; use N = 4: s = (1, 0, 0, -1), k = 2 -> p = 0 = s_1 = s_2
+    out = _kv_from_row([1.0, 0.0, 0.0, -1.0], 2, 0.9)
+    assert out["thr_margin"][0, 0] == 0.0
+    # equal scores at the cut: s = (1, 1), k = N (all candidates), tau = 0.5: l = 1, order margin 0
+    out = _kv_from_row([1.0, 1.0], 2, 0.5)
+    assert out["q2k_num"][0, 0] == 1 and out["order_margin"][0, 0] == 0.0
+    assert out["mass_margin"][0, 0] == 0.0  # cum = 1 = 0.5 * 2 exactly

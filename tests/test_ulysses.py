@@ -19,8 +19,8 @@ import torch.multiprocessing as mp
 
 import bsa_gen
 import oracle as orc
-from paper_2509_01085_b200 import (SP_HEADS_TO_SEND, SP_RECV_TO_HEADS, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND, Geometry,
-                                   resolve_k)
+from paper_2509_01085_b200 import (SP_HEADS_TO_SEND, SP_RECV_T_TO_SEQ, SP_RECV_TO_HEADS, SP_RECV_TO_SEQ,
+                                   SP_SEQ_TO_SEND, SP_SEQ_TO_SEND_T, Geometry, resolve_k)
 
 
 def ref_relayout(mode, src, dst, B, Ls, Hh, d, P):
@@ -32,8 +32,12 @@ def ref_relayout(mode, src, dst, B, Ls, Hh, d, P):
         out = src.reshape(P, B, Hp, Ls, d).permute(1, 2, 0, 3, 4)
     elif mode == SP_HEADS_TO_SEND:  # [B][Hp][P Ls][d] -> [P][B][Hp][Ls][d]
         out = src.reshape(B, Hp, P, Ls, d).permute(2, 0, 1, 3, 4)
-    else:                           # [P(head group)][B][Hp][Ls][d] -> [B][Ls][Hh][d]
+    elif mode == SP_RECV_TO_SEQ:    # [P(head group)][B][Hp][Ls][d] -> [B][Ls][Hh][d]
         out = src.reshape(P, B, Hp, Ls, d).permute(1, 3, 0, 2, 4)
+    elif mode == SP_SEQ_TO_SEND_T:  # [B][Ls][Hh][d] -> [P][B][Ls][Hp][d]
+        out = src.reshape(B, Ls, P, Hp, d).permute(2, 0, 1, 3, 4)
+    else:                           # SP_RECV_T_TO_SEQ: [P(head group)][B][Ls][Hp][d] -> [B][Ls][Hh][d]
+        out = src.reshape(P, B, Ls, Hp, d).permute(1, 2, 0, 3, 4)
     dst.view(-1).copy_(out.reshape(-1))
     return dst
 
@@ -58,6 +62,7 @@ def emulate(relayout, x_seq_shards, B, Ls, Hh, d, P, forward=True):
 
 @pytest.mark.parametrize("P,B,Hh", [(1, 1, 3), (2, 1, 4), (4, 2, 8), (2, 2, 6)])
 def test_relayout_roundtrip_cpu(P, B, Hh):
+    """Head-major chunks (SEQ_TO_SEND / RECV_TO_HEADS / HEADS_TO_SEND / RECV_TO_SEQ) round-trip."""
     L, d = 24, 16
     Ls = L // P
     x = torch.randn(B, L, Hh, d, dtype=torch.float64)
@@ -71,6 +76,33 @@ def test_relayout_roundtrip_cpu(P, B, Hh):
         assert torch.equal(back[s], shards[s])
 
 
+@pytest.mark.parametrize("P,Hh", [(1, 3), (2, 4), (4, 8), (3, 6)])
+def test_token_major_exchange_cpu(P, Hh):
+    """B = 1 token-major path: after SEQ_TO_SEND_T and the all-to-all, rank p's receive buffer read as the strided
+    [1, Hp, L, d] view IS heads [p Hp, (p+1) Hp) of the whole sequence (no reorder); written back in that layout and
+    exchanged again, RECV_T_TO_SEQ restores each rank's [1, Ls, Hh, d] shard."""
+    B, L, d = 1, 24, 16
+    Ls, Hp = L // P, Hh // P
+    x = torch.randn(B, L, Hh, d, dtype=torch.float64)
+    shards = [x[:, s * Ls:(s + 1) * Ls] for s in range(P)]
+    sends = []
+    for sh in shards:
+        buf = torch.empty(sh.numel(), dtype=sh.dtype)
+        ref_relayout(SP_SEQ_TO_SEND_T, sh.contiguous(), buf, B, Ls, Hh, d, P)
+        sends.append(buf.view(P, -1))
+    recvs = [torch.cat([sends[s][p] for s in range(P)]) for p in range(P)]
+    for p in range(P):
+        view = recvs[p].view(1, L, Hp, d).transpose(1, 2)  # what BSA reads, strides (L Hp d, d, Hp d)
+        assert view.stride()[1:] == (d, Hp * d, 1)
+        assert torch.equal(view, x.permute(0, 2, 1, 3)[:, p * Hp:(p + 1) * Hp])
+    # return path: the outputs, written in the received layout, are the send buffers
+    back_recv = [torch.cat([recvs[s].view(P, -1)[p] for s in range(P)]) for p in range(P)]
+    for s in range(P):
+        out = torch.empty(B, Ls, Hh, d, dtype=x.dtype)
+        ref_relayout(SP_RECV_T_TO_SEQ, back_recv[s], out, B, Ls, Hh, d, P)
+        assert torch.equal(out, shards[s])
+
+
 class OracleLayer:
     """The per-rank attention slot of UlyssesBSA filled with the fp64 oracle (test infrastructure)."""
 
@@ -82,16 +114,18 @@ class OracleLayer:
         self.qs = orc.select_queries(self.og, self.r, Q)
         self.kv = orc.select_kv(self.og, Q, K, self.k, self.tau)
 
-    def attend(self, Qh, Kh, Vh):
+    def attend(self, Qh, Kh, Vh, out=None):
         O, _ = orc.attn_fwd(self.og, self.r, Qh[0].numpy(), Kh[0].numpy(), Vh[0].numpy(), self.qs["kept_tok"],
                             self.qs["donor"], self.kv["q2k_num"], self.kv["q2k_idx"], self.scale)
-        return torch.from_numpy(np.ascontiguousarray(O))[None]
+        O = torch.from_numpy(np.ascontiguousarray(O))[None]
+        return O if out is None else out.copy_(O)
 
-    def backward(self, dOh):
+    def backward(self, dOh, out=None):
         Q, K, V = (t[0].numpy() for t in self._saved)
         g = orc.attn_bwd(self.og, self.r, Q, K, V, dOh[0].numpy(), self.qs["kept_tok"], self.qs["donor"],
                          self.kv["q2k_num"], self.kv["q2k_idx"], self.scale)
-        return tuple(torch.from_numpy(np.ascontiguousarray(x))[None] for x in g)
+        g = tuple(torch.from_numpy(np.ascontiguousarray(x))[None] for x in g)
+        return g if out is None else tuple(o.copy_(x) for o, x in zip(out, g))
 
 
 GRID, BLOCK, HH, D, R, F, TAU = (4, 8, 8), (2, 4, 4), 4, 64, 0.5, 0.5, 0.9
@@ -159,7 +193,8 @@ def test_ulysses_gloo_two_ranks_equals_single_process_oracle():
 def test_sp_relayout_kernels_match_permutes(B, Ls, Hh, d, P):
     import paper_2509_01085_b200 as bsa
     shapes = {SP_SEQ_TO_SEND: (B, Ls, Hh, d), SP_RECV_TO_HEADS: (P, B, Hh // P, Ls, d),
-              SP_HEADS_TO_SEND: (B, Hh // P, P * Ls, d), SP_RECV_TO_SEQ: (P, B, Hh // P, Ls, d)}
+              SP_HEADS_TO_SEND: (B, Hh // P, P * Ls, d), SP_RECV_TO_SEQ: (P, B, Hh // P, Ls, d),
+              SP_SEQ_TO_SEND_T: (B, Ls, Hh, d), SP_RECV_T_TO_SEQ: (P, B, Ls, Hh // P, d)}
     g = torch.Generator().manual_seed(5)
     for mode, shp in shapes.items():
         src = torch.randn(*shp, generator=g).to(torch.bfloat16).cuda()
