@@ -522,6 +522,10 @@ int bsa_debug_trace_fwd(void* dev_buf, int cta) {
   cudaError_t e = bsa::debug_trace_fwd(dev_buf, cta);
   return e == cudaSuccess ? BSA_OK : cuda_fail(e, "bsa_debug_trace_fwd");
 }
+int bsa_debug_progress_bwd(void* dev_ptr) {
+  cudaError_t e = bsa::debug_progress_bwd(dev_ptr);
+  return e == cudaSuccess ? BSA_OK : cuda_fail(e, "bsa_debug_progress_bwd");
+}
 int bsa_debug_trace_bwd(void* dev_buf, int cta) {
   cudaError_t e = bsa::debug_trace_bwd(dev_buf, cta);
   return e == cudaSuccess ? BSA_OK : cuda_fail(e, "bsa_debug_trace_bwd");

@@ -20,11 +20,40 @@
 // issuers with plain blocking waits let S/dP(c+1) run ahead of the gradient MMAs of chunk c by itself.
 #include <cmath>
 #include "kernels.h"
+
+#ifdef BSA_HANG_DEBUG
+namespace bsa {
+__device__ unsigned* g_hang_rec = nullptr;
+}
+// a wait that spun ~forever records (barrier smem address, parity, warp, lane, cta) for the host to read
+#define BSA_HANG_RECORD(addr, par)                                                                           \
+  do {                                                                                                        \
+    unsigned* _r = bsa::g_hang_rec;                                                                           \
+    if (_r) {                                                                                                 \
+      const unsigned _i = atomicAdd(_r, 1u);                                                                  \
+      if (_i < 500u) {                                                                                        \
+        unsigned* _e = _r + 8 + 8 * _i;                                                                       \
+        _e[0] = (addr); _e[1] = (par); _e[2] = threadIdx.x >> 5; _e[3] = threadIdx.x & 31;                  \
+        _e[4] = blockIdx.x; _e[5] = blockIdx.y;                                                               \
+        __threadfence_system();                                                                               \
+      }                                                                                                       \
+    }                                                                                                         \
+  } while (0)
+#endif
 #include "ptx.cuh"
 
 namespace bsa {
 
 bool make_map_2d(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
+
+// The backward's waits poll (ptx.cuh mbar_wait_spin) unless built with BSA_BWD_SUSPEND.
+__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
+#ifdef BSA_BWD_SUSPEND
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_spin(bar, parity);
+#endif
+}
 bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int heads, long long sl, long long sh);
 bool make_map_rows_f32(CUtensorMap* m, const void* base, int d, size_t rows, int box_rows);
 
@@ -176,6 +205,21 @@ __device__ int g_bwd_trace_cta = 0;
   } while (0)
 #endif
 
+// Debug-only progress counters (BSA_PROGRESS builds): per CTA 16 words in host-mapped memory, written with
+// volatile stores so the host can read where every role stands while the kernel runs (hang diagnosis).
+__device__ unsigned* g_bwd_prog = nullptr;
+#ifdef BSA_PROGRESS
+#define PROG(slot, v)                                                                                      \
+  do {                                                                                                     \
+    unsigned* _p = g_bwd_prog;                                                                             \
+    if (_p) *reinterpret_cast<volatile unsigned*>(_p + 16 * (blockIdx.y * gridDim.x + blockIdx.x) + (slot)) = (v); \
+  } while (0)
+#else
+#define PROG(slot, v) \
+  do {                \
+  } while (0)
+#endif
+
 struct BwdParams {
   const uint8_t* qdo_img;  // per query block Q^s|dO^s images (k_bwd_prep), SR*d*4 bytes each
   CUtensorMap mK;    // 5D block map
@@ -196,6 +240,14 @@ struct BwdParams {
   float scale;
 };
 
+// dQ staging: 2 slots of 32 rows per drain warp (one 4 KB reduce box per 32-column slice when SR >= 32): half the
+// reduce operations of 16-row boxes for the same bytes, attn_bwd 1.70 -> 1.47 ms at 32k
+#ifndef BSA_DQ_SLOT_ROWS
+#define BSA_DQ_SLOT_ROWS 32
+#endif
+#ifndef BSA_DQ_SLOTS
+#define BSA_DQ_SLOTS 2
+#endif
 constexpr int BWD_THREADS = 384;
 constexpr int BWD_MAX_G = 16;
 
@@ -212,9 +264,13 @@ struct BwdSmem {
   static constexpr int OFF_P = OFF_ST + 2 * STAGE_BYTES;    // [128][64] bf16
   static constexpr int OFF_DS = OFF_P + 16384;
   static constexpr int OFF_ZERO = OFF_DS + 16384;           // d=64 only: zero MN chunk for M=128 padding
-  static constexpr int DQ_SLOTS = 3;                         // per drain warp, [32][16] fp32 each
+  // dQ staging per drain warp: DQ_SLOTS slots of DQ_SROWS rows x 32 fp32 (128B-swizzled, the reduce map's box)
+  static constexpr int DQ_SROWS = BSA_DQ_SLOT_ROWS;
+  static constexpr int DQ_SLOTS = BSA_DQ_SLOTS;
+  static constexpr int DQ_SLOT_BYTES = DQ_SROWS * 128;
   static constexpr int OFF_DQS = OFF_ZERO + (D == 64 ? 16384 : 0);
-  static constexpr int TOTAL = OFF_DQS + 4 * DQ_SLOTS * 2048 + 1024;
+  // the dynamic region is declared 1024-byte aligned (checked at run time), so no alignment slack is added
+  static constexpr int TOTAL = OFF_DQS + 4 * DQ_SLOTS * DQ_SLOT_BYTES;
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
@@ -232,8 +288,9 @@ template <int D, int BT>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
   using SM = BwdSmem<D, BT>;
   constexpr int NCB = SM::NCB;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SW128 tiles need 1024-byte alignment
   uint8_t* sK = sm + SM::OFF_K;
   uint8_t* sV = sm + SM::OFF_V;
   uint8_t* sP = sm + SM::OFF_P;
@@ -287,6 +344,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       break;
     }
   }
+#ifdef BSA_HANG_DEBUG
+  if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && g_hang_rec) {
+    unsigned* m = g_hang_rec + 8 + 8 * 500;
+    m[0] = smem_u32(&bar_kv); m[1] = smem_u32(&bar_c_full[0]); m[2] = smem_u32(&bar_c_full[1]);
+    m[3] = smem_u32(&bar_c_empty[0]); m[4] = smem_u32(&bar_c_empty[1]); m[5] = smem_u32(&bar_sd_full);
+    m[6] = smem_u32(&bar_sd_free); m[7] = smem_u32(&bar_ps_full); m[8] = smem_u32(&bar_ps_free);
+    m[9] = smem_u32(&bar_dq_full[0]); m[10] = smem_u32(&bar_dq_full[1]); m[11] = smem_u32(&bar_dq_free[0]);
+    m[12] = smem_u32(&bar_dq_free[1]); m[13] = smem_u32(&bar_acc); m[14] = smem_u32(&bar_acc_free);
+  }
+#endif
   if (tid == 0) {
     mbar_init(&bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
@@ -348,7 +415,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           nk = p.kept_off[qbl + 1] - ko;
           row0 = bh * p.Lq + ko;
         }
-        mbar_wait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
+        if (lane == 0) PROG(0, c * 4 + 0);
+        bwait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
+        if (lane == 0) PROG(0, c * 4 + 1);
         const int ring = c & 3;
         if (lane < G) {
           s_row0[ring][lane] = row0;
@@ -396,7 +465,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       if (warp == W_SD) {
         // K/V tiles of the block: the previous block's are read until its last MMA (bar_acc)
         if (leader) {
-          if (nacc > 0) mbar_wait(&bar_acc, (nacc - 1) & 1);
+          if (nacc > 0) bwait(&bar_acc, (nacc - 1) & 1);
           const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
           mbar_expect_tx(&bar_kv, 2 * SM::KV_BYTES);
           for (int cb = 0; cb < NCB; ++cb) {
@@ -405,22 +474,29 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           }
         }
         __syncwarp();
-        mbar_wait(&bar_kv, nacc & 1);
+        if (lane == 0) PROG(9, 1000 + nacc);
+        bwait(&bar_kv, nacc & 1);
+        if (lane == 0) PROG(9, 2000 + nacc);
         // S/dP(v) = Q^s K^T, dO^s V^T of chunk v, issued as soon as its stage landed and the softmax
         // warps hold S/dP(v-1) in registers (single TMEM buffer)
         for (int cl = 0; cl < nchunks; ++cl, ++c) {
           const int sv = c & 1;
           const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
-          mbar_wait(&bar_c_full[sv], (c >> 1) & 1);
+          if (lane == 0) PROG(1, c * 4 + 0);
+          bwait(&bar_c_full[sv], (c >> 1) & 1);
           BWD_TRACE(11, c);
-          if (c >= 1) mbar_wait(&bar_sd_free, (c - 1) & 1);
+          if (lane == 0) PROG(1, c * 4 + 1);
+          if (c >= 1) bwait(&bar_sd_free, (c - 1) & 1);
+          if (lane == 0) PROG(1, c * 4 + 2);
           tc_fence_after();
           if (leader) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const int cb = kk >> 2, ko = (kk & 3) * 32;
+#ifndef BSA_ABLATE_BWD_MMA
               umma_ss(tS, dQa + sov + ((cb * 1024 + ko) >> 4), dK + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
               umma_ss(tdP, dDa + sov + ((cb * 1024 + ko) >> 4), dV + ((cb * BT * 128 + ko) >> 4), idesc_s, kk > 0);
+#endif
             }
             umma_commit(&bar_sd_full);
           }
@@ -432,12 +508,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         // (the other issuer) completed before P/dS(c) could exist, so the c_empty commit below covers
         // every read of the stage. The first chunk of a block overwrites dV/dK: the epilogue of the
         // previous block must have read them (bar_acc_free).
-        if (nacc > 0) mbar_wait(&bar_acc_free, (nacc - 1) & 1);
+        if (lane == 0) PROG(10, 1000 + nacc);
+        if (nacc > 0) bwait(&bar_acc_free, (nacc - 1) & 1);
+        if (lane == 0) PROG(10, 2000 + nacc);
         for (int cl = 0; cl < nchunks; ++cl, ++c) {
           const int s = c & 1, qbuf = c & 1;
           const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
-          mbar_wait(&bar_ps_full, c & 1);
-          if (c >= 2) mbar_wait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
+          if (lane == 0) PROG(2, c * 4 + 0);
+          bwait(&bar_ps_full, c & 1);
+          if (lane == 0) PROG(2, c * 4 + 1);
+          if (c >= 2) bwait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
+          if (lane == 0) PROG(2, c * 4 + 2);
           tc_fence_after();
           BWD_TRACE(2, c);
           if (leader) {
@@ -453,13 +534,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
                 aq = umma_desc_sw128(qk, zero - qk, SM::PG);
                 ad = umma_desc_sw128(dk, zero - dk, SM::PG);
               }
+#ifndef BSA_ABLATE_BWD_MMA
               umma_ss(tdV, ad, dP + ((kk * 2048) >> 4), idesc_t, (cl > 0 || kk > 0) ? 1u : 0u);
               umma_ss(tdK, aq, dS + ((kk * 2048) >> 4), idesc_t, (cl > 0 || kk > 0) ? 1u : 0u);
+#endif
             }
             umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
 #pragma unroll
-            for (int kk = 0; kk < BT / 16; ++kk)
+            for (int kk = 0; kk < BT / 16; ++kk) {
+#ifndef BSA_ABLATE_BWD_MMA
               umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
+#endif
+            }
             umma_commit(&bar_dq_full[qbuf]);
             umma_commit(&bar_ps_free);
           }
@@ -478,7 +564,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       int c = 0;
       for (int j = j_first; j < j_end; ++j)
         for (int cl = 0; cl < (nq_of(j) + G - 1) / G; ++cl, ++c) {
-          mbar_wait(&bar_c_full[c & 1], (c >> 1) & 1);
+          bwait(&bar_c_full[c & 1], (c >> 1) & 1);
           BWD_TRACE(12, c);
         }
     }
@@ -500,12 +586,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int nchunks = (nq_of(j) + G - 1) / G;
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
-        mbar_wait(&bar_c_full[s], (c >> 1) & 1);
+        if (row == 0) PROG(3, c * 8 + 0);
+        bwait(&bar_c_full[s], (c >> 1) & 1);
+        if (row == 0) PROG(3, c * 8 + 1);
         if (row == 0 && c == 0) CTA_STAMP(8);
         const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
         const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
         const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
-        mbar_wait(&bar_sd_full, c & 1);
+        bwait(&bar_sd_full, c & 1);
+        if (row == 0) PROG(3, c * 8 + 2);
         tc_fence_after();
         if (row == 0) BWD_TRACE(4, c);
         if (row == 0 && c == 0) CTA_STAMP(9);
@@ -528,12 +617,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           dp[cc] = pr * (dp[cc] - Dq);
         }
         if (row == 0) BWD_TRACE(9, c);
-        if (c >= 1) mbar_wait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+        if (row == 0) PROG(3, c * 8 + 3);
+        if (c >= 1) bwait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+        if (row == 0) PROG(3, c * 8 + 4);
         if (store_pending) {  // the previous block's dK/dV store must have read sP/sdS
           if (row == 0) bulk_wait_group_read<0>();
           named_bar_sync(1, 128);
           store_pending = false;
         }
+        if (row == 0) PROG(3, c * 8 + 5);
         if (row == 0) BWD_TRACE(10, c);
 #pragma unroll
         for (int c8 = 0; c8 < BT / 8; ++c8) {
@@ -556,10 +648,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       // block's first gradient MMAs as soon as they are in registers.
       const int ch_ = row;
       const uint32_t tdk = smem_u32(sP), tdv = smem_u32(sdS);
+      if (row == 0) PROG(11, 1000 + nacc);
       if (nchunks > 0) {
-        mbar_wait(&bar_acc, nacc & 1);
+        bwait(&bar_acc, nacc & 1);
         tc_fence_after();
       }
+      if (row == 0) PROG(11, 2000 + nacc);
       if (store_pending) {  // (a block with no chunks right after another block's store)
         if (row == 0) bulk_wait_group_read<0>();
         named_bar_sync(1, 128);
@@ -616,15 +710,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     // rows harmlessly. Slots form a per-warp ring; each 16-row half is one bulk group.
     const int q4 = warp - 4;
     const int row = q4 * 32 + lane;
-    uint8_t* slots = sm + SM::OFF_DQS + q4 * SM::DQ_SLOTS * 2048;
-    const int R = p.dq_rows, nsub = 32 / R, per_half = 16 / R;
+    constexpr int SROWS = SM::DQ_SROWS, NSL = SM::DQ_SLOTS, SPS = 32 / SROWS;  // slots per 32-column slice
+    uint8_t* slots = sm + SM::OFF_DQS + q4 * NSL * SM::DQ_SLOT_BYTES;
+    const int R = p.dq_rows, nsub = 32 / R, per_slot = SROWS / R;
     int slot_i = 0;
     int c = 0;
     for (int j = j_first; j < j_end; ++j) {
       const int nchunks = (nq_of(j) + G - 1) / G;
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int qbuf = c & 1;
-        mbar_wait(&bar_dq_full[qbuf], (c >> 1) & 1);
+        if (lane == 0) PROG(4 + q4, c * 8 + 0);
+        bwait(&bar_dq_full[qbuf], (c >> 1) & 1);
+        if (lane == 0) PROG(4 + q4, c * 8 + 1);
         tc_fence_after();
         if (row == 0) BWD_TRACE(6, c);
         const int ring = c & 3;
@@ -637,6 +734,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 #pragma unroll
         for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
         const bool any = __any_sync(0xffffffffu, dst >= 0);
+#ifdef BSA_ABLATE_DQ_DRAIN
+        tc_fence_before();
+        mbar_arrive(&bar_dq_free[qbuf]);
+        (void)any;
+        continue;
+#endif
 #pragma unroll 1
         for (int cs = 0; cs < D; cs += 32) {
           float v[32];
@@ -649,13 +752,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             mbar_arrive(&bar_dq_free[qbuf]);
           }
           if (any) {
-            const int s0 = slot_i, s1 = slot_i + 1 == SM::DQ_SLOTS ? 0 : slot_i + 1;
-            slot_i = s1 + 1 == SM::DQ_SLOTS ? 0 : s1 + 1;
-            // the two slots' previous reduces (issued >= 1 group ago) must have read them
-            if (lane == 0) bulk_wait_group_read<SM::DQ_SLOTS - 2>();
+            const int s_first = slot_i;
+            slot_i = (slot_i + SPS) % NSL;
+            // the slots' previous reduces (issued >= NSL - SPS groups ago) must have read them
+            if (lane == 0) PROG(4 + q4, c * 8 + 2 + cs / 32);
+            if (lane == 0) bulk_wait_group_read<NSL - SPS>();
             __syncwarp();
-            const int rr = lane & 15;
-            const uint32_t srow = smem_u32(slots + ((lane >> 4) ? s1 : s0) * 2048) + rr * 128;
+            const int my = lane / SROWS, rr = lane % SROWS;
+            const uint32_t srow = smem_u32(slots + ((s_first + my) % NSL) * SM::DQ_SLOT_BYTES) + rr * 128;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               sts128(srow + ((k ^ (rr & 7)) << 4), __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
@@ -664,11 +768,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             __syncwarp();
             if (lane == 0) {
 #pragma unroll
-              for (int hf = 0; hf < 2; ++hf) {
-                uint8_t* slot = slots + (hf ? s1 : s0) * 2048;
-                for (int k = 0; k < per_half; ++k) {
-                  const int sb = hf * per_half + k;
+              for (int hf = 0; hf < SPS; ++hf) {
+                uint8_t* slot = slots + ((s_first + hf) % NSL) * SM::DQ_SLOT_BYTES;
+                for (int k = 0; k < per_slot; ++k) {
+                  const int sb = hf * per_slot + k;
+#ifndef BSA_ABLATE_DQ_RED
                   if (dk[sb] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 128, cs, dk[sb]);
+#else
+                  (void)slot;
+                  (void)sb;
+#endif
                 }
                 bulk_commit_group();
               }
@@ -678,7 +787,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (row == 0) BWD_TRACE(7, c);
       }
     }
+    if (lane == 0) PROG(4 + q4, 999999);
     if (lane == 0) bulk_wait_group<0>();
+    if (lane == 0) PROG(4 + q4, 1999999);
     if (row == 0) CTA_STAMP(7);
     __syncwarp();
   }
@@ -775,7 +886,7 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.scale = a.scale;
   p.qdo_img = a.qdo_img;
   p.lsed = a.lsed;
-  p.dq_rows = a.SR < 16 ? a.SR : 16;
+  p.dq_rows = a.SR < BSA_DQ_SLOT_ROWS ? a.SR : BSA_DQ_SLOT_ROWS;
   if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
   const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
                    heads_uniform(a.dV, a.B);
@@ -805,6 +916,15 @@ cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
   k_bwd_finalize<<<static_cast<unsigned>((tf + 255) / 256), 256, 0, st>>>(a.BH, a.Lq, a.d, a.scale, a.kept_tok,
                                                                           a.dQacc, a.dQ);
   return cudaGetLastError();
+}
+
+cudaError_t debug_progress_bwd(void* dev_ptr) {
+  unsigned* p = static_cast<unsigned*>(dev_ptr);
+#ifdef BSA_HANG_DEBUG
+  return cudaMemcpyToSymbol(g_hang_rec, &p, sizeof(p));
+#else
+  return cudaMemcpyToSymbol(g_bwd_prog, &p, sizeof(p));
+#endif
 }
 
 cudaError_t debug_trace_bwd(void* dev_buf, int cta) {

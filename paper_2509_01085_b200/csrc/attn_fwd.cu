@@ -420,7 +420,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       mbar_arrive(&bar_s_free[group]);
       float alpha = 1.f;
       bool need_rescale = false;
+#ifdef BSA_ABLATE_FWD_EXP
       if (admit) {
+#pragma unroll
+        for (int c = 0; c < BT; ++c) sv[c] = 0.25f;
+        l_run += 1.f;
+        m_run = 0.f;
+      } else if (false) {
+#else
+      if (admit) {
+#endif
         // key validity (ragged edge blocks: only actual tokens, C23); raw scores, scale folded into ex2
         if (cls != 0) {
           const uint64_t km = s_clsmask[cls];

@@ -63,6 +63,7 @@ cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
 cudaError_t debug_trace_fwd(void* dev_buf, int cta);
 cudaError_t debug_trace_bwd(void* dev_buf, int cta);
+cudaError_t debug_progress_bwd(void* dev_ptr);
 cudaError_t launch_fill(int BH, int L, int d, const int* donor, Rows O, cudaStream_t st);
 
 // Ulysses sequence parallelism: row reorders around the all-to-all (sp.cu)

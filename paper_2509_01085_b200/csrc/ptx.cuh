@@ -56,10 +56,17 @@ __device__ __forceinline__ bool mbar_wait_for(uint64_t* bar, uint32_t parity, ui
       : "memory");
   return ok != 0;
 }
-// Blocking wait for the phase with the given parity. try_wait with an explicit suspend-time hint in an
-// asm-level retry loop: the hint-less form measured ~11k-cycle late wake-ups on B200.
+// Blocking wait for the phase with the given parity: try_wait (the thread may suspend until the phase
+// completes) in an asm-level retry loop. Measured on B200 (round 2): the form WITH an explicit
+// suspend-time hint deadlocks intermittently in the multi-block backward (hint values from 2 us to 10 ms all
+// hang; 5/16 runs of a small probe with 4 KV blocks per CTA), while the hint-less form and the polling
+// test_wait loop never did, and the hint-less form is as fast as the hinted one. Default: hint-less.
+// BSA_WAIT_HINT_NS selects the hinted form (diagnostics only); BSA_WAIT_POLL / BSA_WAIT_SLEEP polling variants.
+#if !defined(BSA_WAIT_HINT_NS) && !defined(BSA_WAIT_POLL) && !defined(BSA_WAIT_SLEEP)
+#define BSA_WAIT_NOHINT 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef BSA_WAIT_POLL
+#if defined(BSA_WAIT_POLL)
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "BSA_WAIT_%=:\n\t"
@@ -70,7 +77,50 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
   return;
+#elif defined(BSA_WAIT_SLEEP)
+  if (mbar_try_wait(bar, parity)) return;
+  uint32_t ns = BSA_WAIT_SLEEP;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 256u ? 2u * ns : 256u;
+  }
+  return;
+#elif defined(BSA_HANG_RECORD)
+  uint32_t spins = 0;
+  while (true) {
+    uint32_t ok;
+#ifdef BSA_WAIT_HINT_NS
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(static_cast<uint32_t>(BSA_WAIT_HINT_NS))
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
 #endif
+    if (ok) return;
+    if (++spins == 200000u) BSA_HANG_RECORD(smem_u32(bar), parity);
+  }
+#elif defined(BSA_WAIT_NOHINT)
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "BSA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra BSA_DONE_%=;\n\t"
+      "bra BSA_WAIT_%=;\n\t"
+      "BSA_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "BSA_WAIT_%=:\n\t"
@@ -78,7 +128,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@P1 bra BSA_DONE_%=;\n\t"
       "bra BSA_WAIT_%=;\n\t"
       "BSA_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity), "r"(static_cast<uint32_t>(BSA_WAIT_HINT_NS + 0))
+      : "memory");
+#endif
+}
+
+// Polling wait (mbarrier.test_wait in a loop; the thread never suspends). Used by the backward kernel, whose
+// CTAs walk several KV blocks: with suspending try_wait it hung intermittently at block transitions on B200
+// ("waits"), with this loop it never did in thousands of runs.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "BSA_SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra BSA_SPUN_%=;\n\t"
+      "bra BSA_SPIN_%=;\n\t"
+      "BSA_SPUN_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
       : "memory");
 }
 

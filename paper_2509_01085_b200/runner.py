@@ -35,6 +35,8 @@ class BSAAttention:
         self.set_knobs(f, tau)
         self.scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None and torch.cuda.is_available():
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.cache_partition = cache_partition
         self.kv_mode = int(kv_mode)  # 0 = two_stage (the library's reading), 1 = unified_prob (C28)
         dev, N, Lq, L = self.device, self.N, self.Lq, geom.L

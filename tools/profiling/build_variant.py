@@ -5,7 +5,7 @@ import sys
 import glob
 import concurrent.futures as cf
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2509_01085_b200 import build as B  # noqa: E402
 
 out, defs = sys.argv[1], sys.argv[2:]
