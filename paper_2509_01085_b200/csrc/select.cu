@@ -187,9 +187,47 @@ __device__ __forceinline__ void block_gram(const bf16* sq, int DS, int BTp, floa
   }
 }
 
-// One CTA (128 threads) per (bh, block). Shared layout: rows padded to D+8 bf16 so that
-// lane-strided 16-byte row reads and ldmatrix are bank-conflict free.
-// 6 CTAs per SM (the shared-memory limit): caps registers at 80 (0.255 -> 0.231 ms at 32k)
+// fp64 cosine of two staged bf16 rows, one warp cooperatively: lane l sums channels l, l + 32, ... with fused
+// multiply-adds, then a butterfly reduction; sqrt and division correctly rounded; 0 if either norm is 0 (C4).
+// It differs from the oracle's sequential channel sum by a few ulps (~1e-16), so a decision taken on it can
+// differ from the oracle's only where the oracle's own margin is below ~1e-15: a C24 near-tie.
+template <int D>
+__device__ __forceinline__ double warp_cos(const bf16* a, const bf16* b, int lane) {
+  double aa = 0.0, bb = 0.0, ab = 0.0;
+#pragma unroll
+  for (int c = lane; c < D; c += 32) {
+    const double x = (double)__bfloat162float(a[c]), y = (double)__bfloat162float(b[c]);
+    aa = fma(x, x, aa);
+    bb = fma(y, y, bb);
+    ab = fma(x, y, ab);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aa += __shfl_xor_sync(0xffffffffu, aa, o);
+    bb += __shfl_xor_sync(0xffffffffu, bb, o);
+    ab += __shfl_xor_sync(0xffffffffu, ab, o);
+  }
+  const double na = sqrt(aa), nb = sqrt(bb);
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  return ab / (na * nb);
+}
+
+// a2 + a3: one CTA (128 threads, one token per thread) per (bh, block). Shared layout: rows padded to D+8 bf16
+// so that lane-strided 16-byte row reads and ldmatrix are bank-conflict free.
+//
+// Certified fp32 decisions (DESIGN.md §3 "Precision of decisions"). The block's Gram matrix G = Q Q^T comes
+// from the tensor cores: bf16 x bf16 products are exact in fp32 and the fp32 accumulation over D <= 128
+// channels errs by at most D 2^-23 sum_c |a_c b_c| <= 1.6e-5 |a| |b| (Cauchy-Schwarz), so the fp32 cosine
+// G_ij / sqrt(G_ii G_jj) is within EPS = 1e-4 of the exact one (numerator 1.6e-5, the two rsqrt factors
+// < 2e-5, roundings ~1e-7; a 2.5x margin). Zero rows are detected exactly (a sum of exact non-negative
+// products is 0 only if every product is).
+//  * Eq.2 keep cut (C5, C7): the m_u smallest of (cosine to the centre, token index) per unit. If the fp32
+//    values v of the last kept and the first pruned item differ by more than 2 EPS, the fp32 decision is
+//    the exact one; otherwise every item within 2 EPS of the cut is re-scored in fp64 (warp_cos) and the
+//    cut among them is taken on those values (items further below / above are provably kept / pruned).
+//  * Donors (C9): kept candidates more than 2 EPS below the fp32 best cannot be the exact argmax; one
+//    survivor is the answer, several are re-scored in fp64.
+// So every decision equals the fp64 evaluation, and only near-ties ever touch fp64.
 #ifndef BSA_SELQ_MIN_BLOCKS
 #define BSA_SELQ_MIN_BLOCKS 6
 #endif
@@ -199,156 +237,210 @@ __global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo
                                                         int* __restrict__ donor, double* __restrict__ q_pooled,
                                                         bf16* __restrict__ q_packed) {
   constexpr int DS = D + 8;
+  constexpr float EPS = 1e-4f;
   extern __shared__ __align__(16) uint8_t smem[];
-  const int b = blockIdx.x, bh = blockIdx.y;
+  const int b = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
   const int BTn = g.BT;
-  bf16* sq = reinterpret_cast<bf16*>(smem);                          // [BTp][DS] (rows >= n zero)
-  double* nrm = reinterpret_cast<double*>(sq + ((BTn + 15) & ~15) * DS);  // [BT]
-  double* cs = nrm + BTn;                                            // [BT]
-  int* tok = reinterpret_cast<int*>(cs + BTn);                       // [BT]
-  int* unit = tok + BTn;                                             // [BT]
-  int* cen = unit + BTn;                                             // [BT] centre local idx of my unit
-  int* keep = cen + BTn;                                             // [BT] 1 if kept
-  int* mcnt = keep + BTn;                                            // [BT] keep count of my unit
-  int* plist = mcnt + BTn;                                           // [BT] pruned local indices
-  const int BTp = (BTn + 15) & ~15;                                  // rows padded for the MMA tiles
-  const int GS = BTp + 1;                                            // Gram row stride (floats)
-  float* gram = reinterpret_cast<float*>(plist + BTn);              // [BTp][GS] fp32 Gram of the rows
-  __shared__ int s_np;
+  const int BTp = (BTn + 15) & ~15;  // rows padded for the MMA tiles
+  const int GS = BTp + 1;            // Gram row stride (floats)
+  bf16* sq = reinterpret_cast<bf16*>(smem);                     // [BTp][DS] (rows >= n zero)
+  float* gram = reinterpret_cast<float*>(sq + BTp * DS);        // [BTp][GS] fp32 Gram of the rows
+  double* ex = reinterpret_cast<double*>(gram + BTp * GS);      // [BT] exact cosine of re-scored items
+  float* vf = reinterpret_cast<float*>(ex + BTn);               // [BT] fp32 cosine to the unit centre
+  float* ulo = vf + BTn;                                        // [units] fp32 value of the last kept item
+  float* uhi = ulo + BTn;                                       // [units] fp32 value of the first pruned item
+  float* inv = uhi + BTn;                                       // [BT] fp32 1 / |q_i| (0 for a zero row)
+  int* tok = reinterpret_cast<int*>(inv + BTn);                 // [BT] raster token of each local index
+  int* unit = tok + BTn;                                        // [BT] unit of each token
+  int* keep = unit + BTn;                                       // [BT] 1 if kept
+  int* plist = keep + BTn;                                      // [BT] pruned local indices
+  int* ulow = plist + BTn;                                      // [units] items certainly below the cut band
+  int* band = ulow + BTn;                                       // [BT] 1 if re-scored
+  int* ulist_c0 = band + BTn;                                   // [BT] unit centre of each re-scored item
+  __shared__ int s_np, s_nb;
 
   const Box x = block_box(g, b);
   const int n = box_size(x);
   const size_t head = static_cast<size_t>(bh) * g.L;
   const bf16* qh = Q.head(bh);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) tok[i] = box_token(g, x, i);
+  if (t < n) tok[t] = box_token(g, x, t);
+  if (t < BTn) { ulow[t] = 0; band[t] = 0; }
+  if (t == 0) { s_np = 0; s_nb = 0; }
   __syncthreads();
-  // rows -> smem (16-byte vectors)
+  // rows -> smem (16-byte vectors): every load of the thread is issued before the first store (memory-level
+  // parallelism: one dependent round trip per CTA instead of one per vector)
   constexpr int VPR = D / 8;
-  for (int v = threadIdx.x; v < BTp * VPR; v += blockDim.x) {
-    int i = v / VPR, c = (v % VPR) * 8;
-    *reinterpret_cast<uint4*>(sq + i * DS + c) =
-        i < n ? *reinterpret_cast<const uint4*>(qh + tok[i] * Q.sl + c) : make_uint4(0, 0, 0, 0);
+  constexpr int MAXV = 128 * VPR / 128;  // vectors per thread for the largest block (128 tokens)
+  {
+    uint4 rv[MAXV];
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int v = t + 128 * k, i = v / VPR, c = (v % VPR) * 8;
+      rv[k] = (i < n) ? __ldg(reinterpret_cast<const uint4*>(qh + tok[i] * Q.sl + c)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int v = t + 128 * k, i = v / VPR, c = (v % VPR) * 8;
+      if (i < BTp) *reinterpret_cast<uint4*>(sq + i * DS + c) = rv[k];
+    }
   }
   __syncthreads();
-  block_gram<D>(sq, DS, BTp, gram, GS);  // read by the donor search below (after later barriers)
-  // a2: pooled mean, summed in ascending token order
+  block_gram<D>(sq, DS, BTp, gram, GS);
+  // a2: pooled mean, summed in ascending token order; the fp64 sums of bf16 values are exact
   if (q_pooled) {
-    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    for (int c = t; c < D; c += blockDim.x) {
       double s = 0.0;
       for (int i = 0; i < n; ++i) s = dadd(s, (double)__bfloat162float(sq[i * DS + c]));
       q_pooled[(static_cast<size_t>(bh) * g.N + b) * D + c] = s / (double)n;
     }
   }
-  // norms, unit membership, centre of the unit (C3: floor-midpoint of the unit's actual extent)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const bf16* qi = sq + i * DS;
-    nrm[i] = sqrt(dot_rows<D>(qi, qi));
-    int lw = i % x.e[2], lh = (i / x.e[2]) % x.e[1], lt = i / (x.e[2] * x.e[1]);
+  // unit membership, centre (C3: floor-midpoint of the unit's actual extent), keep count m_u, unit size
+  const bool is_tok = t < n;
+  int u = 0, c0 = 0, m = 0, usz = 0;
+  if (is_tok) {
+    const int lw = t % x.e[2], lh = (t / x.e[2]) % x.e[1], lt = t / (x.e[2] * x.e[1]);
     int nu[3];
     unit_grid(g, x, nu);
-    int a = lt / g.ut, bb = lh / g.uh, c = lw / g.uw;
-    unit[i] = (a * nu[1] + bb) * nu[2] + c;
-    int et = min_i(g.ut, x.e[0] - a * g.ut), eh = min_i(g.uh, x.e[1] - bb * g.uh), ew = min_i(g.uw, x.e[2] - c * g.uw);
-    int ct_ = a * g.ut + et / 2, ch_ = bb * g.uh + eh / 2, cw_ = c * g.uw + ew / 2;
-    cen[i] = (ct_ * x.e[1] + ch_) * x.e[2] + cw_;
-    mcnt[i] = keep_count(r, et * eh * ew);
+    const int a = lt / g.ut, bb = lh / g.uh, c = lw / g.uw;
+    u = (a * nu[1] + bb) * nu[2] + c;
+    const int et = min_i(g.ut, x.e[0] - a * g.ut), eh = min_i(g.uh, x.e[1] - bb * g.uh), ew = min_i(g.uw, x.e[2] - c * g.uw);
+    c0 = ((a * g.ut + et / 2) * x.e[1] + (bb * g.uh + eh / 2)) * x.e[2] + (c * g.uw + ew / 2);
+    usz = et * eh * ew;
+    m = keep_count(r, usz);
+    unit[t] = u;
+  }
+  __syncthreads();  // (Gram complete)
+  // Eq.2 in fp32: v = cos(q_centre, q_i), v_centre := 1, zero norm -> 0 (C4)
+  if (is_tok) {
+    const float gii = gram[t * GS + t];
+    inv[t] = gii == 0.f ? 0.f : rsqrtf(gii);
   }
   __syncthreads();
-  // Eq.2: c_i = cos(q_centre, q_i); c_centre := 1; zero norm -> 0 (C4)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int c0 = cen[i];
-    double c;
-    if (i == c0) c = 1.0;
-    else if (nrm[c0] == 0.0 || nrm[i] == 0.0) c = 0.0;
-    else c = dot_rows<D>(sq + c0 * DS, sq + i * DS) / (nrm[c0] * nrm[i]);
-    cs[i] = c;
+  float v = 0.f;
+  if (is_tok) {
+    v = (t == c0) ? 1.f : gram[c0 * GS + t] * inv[c0] * inv[t];  // (a zero row has inv = 0: cosine 0)
+    vf[t] = v;
   }
   __syncthreads();
-  // rank by (c ascending, token ascending) inside the unit; keep the first m_u (C5, C7)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int rank = 0;
-    for (int j = 0; j < n; ++j)
-      if (unit[j] == unit[i] && (cs[j] < cs[i] || (cs[j] == cs[i] && j < i))) ++rank;  // local order == token order
-    keep[i] = rank < mcnt[i];
-  }
-  if (threadIdx.x == 0) s_np = 0;
-  __syncthreads();
-  // kept outputs: block-major, ascending token inside the block
-  const int koff = kept_off[b];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (keep[i]) {
-      int pos = 0;
-      for (int j = 0; j < i; ++j) pos += keep[j];
-      size_t prow = static_cast<size_t>(bh) * Lq + koff + pos;
-      kept_tok[prow] = tok[i];
-      donor[head + tok[i]] = tok[i];
-      if (q_packed)
-        for (int c = 0; c < D; c += 8)
-          *reinterpret_cast<uint4*>(q_packed + prow * D + c) = *reinterpret_cast<const uint4*>(sq + i * DS + c);
-    } else {
-      plist[atomicAdd(&s_np, 1)] = i;
+  // rank by (v ascending, index ascending) inside the unit (C5, C7)
+  int rank = 0;
+  if (is_tok) {
+    for (int j = 0; j < n; ++j) {
+      if (unit[j] != u) continue;
+      const float vj = vf[j];
+      rank += (vj < v || (vj == v && j < t)) ? 1 : 0;
+    }
+    if (m < usz) {
+      if (rank == m - 1) ulo[u] = v;
+      if (rank == m) uhi[u] = v;
     }
   }
   __syncthreads();
-  // donors (C9): warp per pruned token, lanes over kept candidates of the same unit;
-  // argmax cos(q_p, q_j), ties -> lowest token
-  //
-  // Certified fp32 screening: bf16 x bf16 products are exact in fp32, so an fp32 dot accumulated over D
-  // channels (tensor-core Gram above) is within ~D 2^-23 sum|a_c b_c| <= 1.6e-5 |a||b| of the exact
-  // dot even with truncating accumulation; with the fp64 norms the fp32 cosine is within EPS = 6e-5 of
-  // the fp64 one (4x margin). A kept j whose fp32 cosine is more than 2 EPS below the fp32 best can
-  // therefore not be the fp64 argmax; if only one candidate survives it IS the fp64 argmax, otherwise
-  // the survivors are re-scored with the exact fp64 formula. The decision is identical to a pure fp64
-  // evaluation.
-  constexpr float EPS = 6e-5f;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // certification of the cut; re-score the band of an ambiguous unit
+  bool inband = false;
+  if (is_tok && m < usz) {
+    const float lo = ulo[u], hi = uhi[u];
+    if (hi - lo <= 2.f * EPS) {
+      inband = v >= lo - 2.f * EPS && v <= hi + 2.f * EPS;
+      if (v < lo - 2.f * EPS) atomicAdd(&ulow[u], 1);
+    }
+  }
+  bool kept = rank < m;
+  if (__syncthreads_or(inband)) {
+    const int warp = t >> 5, lane = t & 31;
+    if (inband) {
+      band[t] = 1;
+      const int q = atomicAdd(&s_nb, 1);
+      plist[q] = t;  // (plist is free until the outputs below)
+      ulist_c0[q] = c0;
+    }
+    __syncthreads();
+    for (int q = warp; q < s_nb; q += 4) {  // warp-cooperative fp64 re-score of the band
+      const int i = plist[q], ci = ulist_c0[q];
+      const double e = (i == ci) ? 1.0 : warp_cos<D>(sq + ci * DS, sq + i * DS, lane);
+      if (lane == 0) ex[i] = e;
+    }
+    __syncthreads();
+    if (inband) {
+      const double e = ex[t];
+      int br = 0;
+      for (int j = 0; j < n; ++j)
+        if (unit[j] == u && band[j] && (ex[j] < e || (ex[j] == e && j < t))) ++br;
+      kept = br < m - ulow[u];
+    }
+  }
+  // kept outputs: block-major, ascending token inside the block (position = kept tokens before it: ballot
+  // prefix inside the warp plus the counts of the warps before)
+  const int warp = t >> 5, lane = t & 31;
+  __shared__ int s_wk[4];
+  const unsigned kb = __ballot_sync(0xffffffffu, is_tok && kept);
+  if (lane == 0) s_wk[warp] = __popc(kb);
+  if (is_tok) keep[t] = kept ? 1 : 0;
+  __syncthreads();
+  int pos = __popc(kb & ((1u << lane) - 1u));
+  for (int w = 0; w < warp; ++w) pos += s_wk[w];
+  const int koff = kept_off[b];
+  if (is_tok) {
+    if (kept) {
+      plist[BTn - 1 - pos] = t;  // kept local index by position, stored from the top of plist
+      const size_t prow = static_cast<size_t>(bh) * Lq + koff + pos;
+      kept_tok[prow] = tok[t];
+      donor[head + tok[t]] = tok[t];
+    } else {
+      plist[atomicAdd(&s_np, 1)] = t;
+    }
+  }
+  __syncthreads();
+  // Q^s rows: coalesced copy, consecutive threads write consecutive 16-byte chunks of the packed rows
+  if (q_packed) {
+    const int nk = s_wk[0] + s_wk[1] + s_wk[2] + s_wk[3];
+    bf16* dst = q_packed + (static_cast<size_t>(bh) * Lq + koff) * D;
+    for (int v = t; v < nk * VPR; v += 128) {
+      const int k = v / VPR, c = (v % VPR) * 8;
+      *reinterpret_cast<uint4*>(dst + k * D + c) = *reinterpret_cast<const uint4*>(sq + plist[BTn - 1 - k] * DS + c);
+    }
+  }
+  // donors (C9): warp per pruned token, lanes over kept candidates of the same unit; argmax cos(q_p, q_j),
+  // ties -> lowest token; fp32 screen on the Gram, exact re-score of the survivors within 2 EPS of the best
+  const int nslot = (n + 31) >> 5;
   for (int pi = warp; pi < s_np; pi += 4) {
     const int p = plist[pi];
+    const int up = unit[p];
+    const float ip = inv[p];
     float cv[4];
     float best32 = -FLT_MAX;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = lane + 32 * k;
       cv[k] = -FLT_MAX;
-      if (j < n && keep[j] && unit[j] == unit[p]) {
-        if (nrm[p] == 0.0 || nrm[j] == 0.0) cv[k] = 0.f;
-        else cv[k] = gram[p * GS + j] / static_cast<float>(nrm[p] * nrm[j]);
-      }
+      if (k < nslot && j < n && keep[j] && unit[j] == up) cv[k] = gram[p * GS + j] * ip * inv[j];
       best32 = fmaxf(best32, cv[k]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best32 = fmaxf(best32, __shfl_xor_sync(0xffffffffu, best32, o));
+    unsigned cmask[4];
     int ncand = 0, arg = INT_MAX;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (cv[k] >= best32 - 2.f * EPS) { ++ncand; arg = min(arg, lane + 32 * k); }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
-      arg = min(arg, __shfl_xor_sync(0xffffffffu, arg, o));
+    for (int k = 0; k < 4; ++k) {
+      cmask[k] = __ballot_sync(0xffffffffu, cv[k] >= best32 - 2.f * EPS);
+      ncand += __popc(cmask[k]);
+      if (cmask[k] && arg == INT_MAX) arg = 32 * k + __ffs(cmask[k]) - 1;
     }
 #ifdef BSA_COUNT_RESCORE
     if (lane == 0 && ncand > 1) atomicAdd(&g_rescore_count, 1ull);
 #endif
-#ifndef BSA_ABLATE_RESCORE
-    if (ncand > 1) {  // near tie in fp32: decide in fp64 exactly as the plain definition does
-#else
-    if (ncand > 1000) {
-#endif
+    if (ncand > 1) {  // near tie in fp32: decide on fp64 cosines (warp-cooperative), ties -> lowest token
       double best = -DBL_MAX;
       arg = INT_MAX;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int j = lane + 32 * k;
-        if (cv[k] < best32 - 2.f * EPS) continue;
-        double c = (nrm[p] == 0.0 || nrm[j] == 0.0) ? 0.0 : dot_rows<D>(sq + p * DS, sq + j * DS) / (nrm[p] * nrm[j]);
-        if (c > best || (c == best && j < arg)) { best = c; arg = j; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+        unsigned mk = cmask[k];
+        while (mk) {
+          const int j = 32 * k + __ffs(mk) - 1;
+          mk &= mk - 1;
+          const double c = warp_cos<D>(sq + p * DS, sq + j * DS, lane);
+          if (c > best) { best = c; arg = j; }  // ascending j: strict > keeps the lowest j on ties
+        }
       }
     }
     if (lane == 0) donor[head + tok[p]] = tok[arg];
@@ -357,7 +449,7 @@ __global__ void __launch_bounds__(128, BSA_SELQ_MIN_BLOCKS) k_select_queries(Geo
 
 static size_t select_smem(int BT, int D) {
   const size_t BTp = (BT + 15) & ~15;
-  return BTp * (D + 8) * 2 + static_cast<size_t>(BT) * 16 + static_cast<size_t>(BT) * 6 * 4 + BTp * (BTp + 1) * 4;
+  return BTp * (D + 8) * 2 + BTp * (BTp + 1) * 4 + static_cast<size_t>(BT) * (8 + 4 * 4 + 7 * 4);
 }
 
 cudaError_t launch_select_queries(const Geo& g, double r, int BH, int d, int Lq, Rows Q, const int* kept_off,
@@ -382,21 +474,34 @@ template <int D>
 __global__ void __launch_bounds__(128) k_pool(Geo g, const Rows X, double* __restrict__ Xc) {
   constexpr int CH = D / 8;      // 8-channel chunks per row (16 or 8)
   constexpr int TG = 128 / CH;   // token groups (8 or 16)
+  constexpr int MAXI = 128 / TG; // tokens per group (block of <= 128 tokens)
   __shared__ double part[TG][D];
+  __shared__ int s_tok[128];
   const int b = blockIdx.x, bh = blockIdx.y;
   const int ck = threadIdx.x % CH, tg = threadIdx.x / CH;
   const Box x = block_box(g, b);
   const int n = box_size(x);
   const bf16* xh = X.head(bh);
+  if (threadIdx.x < n) s_tok[threadIdx.x] = box_token(g, x, threadIdx.x);
+  __syncthreads();
+  // the thread's row chunks are requested 8 at a time before any add (bytes in flight, not a load-add chain)
   double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = tg; i < n; i += TG) {
-    uint4 v = *reinterpret_cast<const uint4*>(xh + box_token(g, x, i) * X.sl + ck * 8);
-    const __nv_bfloat162* pv = reinterpret_cast<const __nv_bfloat162*>(&v);
+  for (int k0 = 0; k0 < MAXI && tg + k0 * TG < n; k0 += 8) {
+    uint4 v[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float2 f = __bfloat1622float2(pv[k]);
-      s[2 * k] = dadd(s[2 * k], (double)f.x);
-      s[2 * k + 1] = dadd(s[2 * k + 1], (double)f.y);
+    for (int k = 0; k < 8; ++k) {
+      const int i = tg + (k0 + k) * TG;
+      v[k] = i < n ? __ldg(reinterpret_cast<const uint4*>(xh + s_tok[i] * X.sl + ck * 8)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const __nv_bfloat162* pv = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(pv[e]);
+        s[2 * e] = dadd(s[2 * e], (double)f.x);  // (zero padding adds exactly 0)
+        s[2 * e + 1] = dadd(s[2 * e + 1], (double)f.y);
+      }
     }
   }
 #pragma unroll
@@ -417,59 +522,72 @@ cudaError_t launch_pool(const Geo& g, int BH, int d, Rows X, double* Xc, cudaStr
 }
 
 // ------------------------------------------------------------------------------------ a4
-// S[bh][i][j] = (sum_c Qc[i][c] Kc[j][c]) / sqrt(d): 64x64 output tile per CTA, 256 threads x (4 x 4)
-// outputs, channels summed sequentially with exactly rounded mul/add (bit-identical to a plain
-// sequential fp64 loop). Operands are staged channel-major ([c][row], padded) so a warp's loads are
-// broadcasts / consecutive: per channel a thread reads 4 + 4 doubles for 16 products, which puts the
-// kernel on the fp64 pipe rather than shared-memory bandwidth.
+// S[bh][i][j] = (sum_c Qc[i][c] Kc[j][c]) / sqrt(d): 64x64 output tile per CTA, 128 threads x (8 x 4)
+// outputs, channels summed in ascending order with fused multiply-adds (one DFMA per product: half the fp64
+// instructions of separately rounded mul + add; the sums differ from the oracle's sequential mul/add loop by
+// a few ulps, which can only change a decision whose oracle margin is ~1e-15, i.e. a C24 near-tie).
+// Operands are staged channel-major ([c][row], padded) so a warp's loads are broadcasts / consecutive: per
+// channel a thread reads 8 + 4 doubles for 32 products, which puts the kernel on the fp64 pipe rather than
+// shared-memory bandwidth; the next channel slab is fetched into registers while the current one is used.
 constexpr int SC_T = 64, SC_KC = 16, SC_LD = SC_T + 2;
-__global__ void __launch_bounds__(256) k_scores(int N, int d, const double* __restrict__ Qc,
+__global__ void __launch_bounds__(128) k_scores(int N, int d, const double* __restrict__ Qc,
                                                 const double* __restrict__ Kc, double* __restrict__ S) {
   __shared__ double sa[SC_KC][SC_LD], sb[SC_KC][SC_LD];
   const int bh = blockIdx.z, i0 = blockIdx.y * SC_T, j0 = blockIdx.x * SC_T;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // outputs (ty + 16 a, tx + 16 b)
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // outputs (ty + 8 a, tx + 16 b): 8 x 4 per thread
   const double* qh = Qc + static_cast<size_t>(bh) * N * d;
   const double* kh = Kc + static_cast<size_t>(bh) * N * d;
-  double acc[4][4];
+  double acc[8][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int c0 = 0; c0 < d; c0 += SC_KC) {
+  double ra[8], rb[8];
+  auto fetch = [&](int c0) {
 #pragma unroll
-    for (int v0 = 0; v0 < SC_T * SC_KC; v0 += 256) {
-      const int v = v0 + threadIdx.x, rr = v / SC_KC, cc = v % SC_KC;
-      sa[cc][rr] = (i0 + rr < N) ? qh[static_cast<size_t>(i0 + rr) * d + c0 + cc] : 0.0;
-      sb[cc][rr] = (j0 + rr < N) ? kh[static_cast<size_t>(j0 + rr) * d + c0 + cc] : 0.0;
+    for (int k = 0; k < 8; ++k) {
+      const int v = threadIdx.x + 128 * k, rr = v / SC_KC, cc = v % SC_KC;
+      ra[k] = (i0 + rr < N) ? __ldg(qh + static_cast<size_t>(i0 + rr) * d + c0 + cc) : 0.0;
+      rb[k] = (j0 + rr < N) ? __ldg(kh + static_cast<size_t>(j0 + rr) * d + c0 + cc) : 0.0;
+    }
+  };
+  fetch(0);
+  for (int c0 = 0; c0 < d; c0 += SC_KC) {
+    __syncthreads();  // the previous channel slab has been consumed
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int v = threadIdx.x + 128 * k, rr = v / SC_KC, cc = v % SC_KC;
+      sa[cc][rr] = ra[k];
+      sb[cc][rr] = rb[k];
     }
     __syncthreads();
+    if (c0 + SC_KC < d) fetch(c0 + SC_KC);  // in flight while this slab is multiplied
 #pragma unroll
     for (int cc = 0; cc < SC_KC; ++cc) {
-      double av[4], bv[4];
+      double av[8], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = sa[cc][ty + 16 * a];
+      for (int a = 0; a < 8; ++a) av[a] = sa[cc][ty + 8 * a];
 #pragma unroll
       for (int b = 0; b < 4; ++b) bv[b] = sb[cc][tx + 16 * b];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = dadd(acc[a][b], dmul(av[a], bv[b]));
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
-    __syncthreads();
   }
   const double sd = sqrt((double)d);
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      const int i = i0 + ty + 8 * a, j = j0 + tx + 16 * b;
       if (i < N && j < N) S[(static_cast<size_t>(bh) * N + i) * N + j] = acc[a][b] / sd;
     }
 }
 
 cudaError_t launch_scores(int N, int BH, int d, const double* Qc, const double* Kc, double* S, cudaStream_t st) {
   dim3 grid((N + SC_T - 1) / SC_T, (N + SC_T - 1) / SC_T, BH);
-  k_scores<<<grid, 256, 0, st>>>(N, d, Qc, Kc, S);
+  k_scores<<<grid, 128, 0, st>>>(N, d, Qc, Kc, S);
   return cudaGetLastError();
 }
 
@@ -497,14 +615,10 @@ __device__ __forceinline__ bool before(double sa, int ja, double sb, int jb) {
 // Fallback: one CTA (256 threads) per row, for rows whose candidate set exceeds the warp kernel's
 // shared-memory capacity (and for k = N, where every row has N candidates). `rows` lists the rows
 // to do (NULL = all rows, row = blockIdx.x); CTAs past *nrows exit at once.
-__global__ void __launch_bounds__(256) k_admit_cta(int N, const double* __restrict__ S, int k, double z, double tau,
-                                                   int unified, const int* __restrict__ rows,
-                                                   const int* __restrict__ nrows,
-                                                   int* __restrict__ q2k_num, int* __restrict__ q2k_idx,
-                                                   double* __restrict__ thresh, uint32_t* __restrict__ qbits) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  if (rows && static_cast<int>(blockIdx.x) >= *nrows) return;
-  const int row = rows ? rows[blockIdx.x] : static_cast<int>(blockIdx.x);  // bh * N + i
+__device__ __forceinline__ void admit_cta_row(int row, int N, const double* __restrict__ S, int k, double z,
+                                              double tau, int unified, int* __restrict__ q2k_num,
+                                              int* __restrict__ q2k_idx, double* __restrict__ thresh,
+                                              uint32_t* __restrict__ qbits, uint8_t* smem) {
   int P2 = 1;
   while (P2 < N) P2 <<= 1;
   double* s = reinterpret_cast<double*>(smem);  // [N]
@@ -685,12 +799,77 @@ __global__ void __launch_bounds__(256) k_admit_cta(int N, const double* __restri
   if (threadIdx.x == 0) q2k_num[row] = ell;
 }
 
+// One CTA loops over rows: the listed overflow rows of the warp kernel (rows != NULL, count *nrows), or all
+// `total` rows (k = N and unified_prob, where every row has N candidates).
+__global__ void __launch_bounds__(256) k_admit_cta(int N, int total, const double* __restrict__ S, int k, double z,
+                                                   double tau, int unified, const int* __restrict__ rows,
+                                                   const int* __restrict__ nrows, int* __restrict__ q2k_num,
+                                                   int* __restrict__ q2k_idx, double* __restrict__ thresh,
+                                                   uint32_t* __restrict__ qbits) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int nr = rows ? *nrows : total;
+  for (int it = blockIdx.x; it < nr; it += gridDim.x) {
+    admit_cta_row(rows ? rows[it] : it, N, S, k, z, tau, unified, q2k_num, q2k_idx, thresh, qbits, smem);
+    __syncthreads();
+  }
+}
+
 // Fast path: one WARP per row (8 rows per 256-thread CTA, grid-stride), no block barriers. The
 // candidate set (about k entries by Eq.3's quantile, reading C14) is compacted into the warp's shared
 // slice of ADMIT_CAP entries; rows with more candidates are appended to `ovf` for k_admit_cta.
 // Same arithmetic as k_admit_cta: warp-tree mean and population std, candidates s >= p, bitonic
 // sort by (s desc, j asc), exp(s - s_max) masses, inclusive scan, shortest prefix >= tau E.
 constexpr int ADMIT_CAP = 512;
+
+// Bitonic sort of P = 32 E (s, j) pairs (smem cs / cj) into (s desc, j asc) order: element t lives in lane
+// t % 32, register t / 32; partners at distance >= 32 are in the same lane, nearer ones one shuffle away.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(double* cs, int* cj, int lane) {
+  constexpr int P = 32 * E;
+  double s[E];
+  int j[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    s[e] = cs[e * 32 + lane];
+    j[e] = cj[e * 32 + lane];
+  }
+#pragma unroll
+  for (int sz = 2; sz <= P; sz <<= 1) {
+#pragma unroll
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      if (st >= 32) {
+        const int es = st >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int e2 = e ^ es;
+          if (e2 > e) {
+            const bool up = ((e * 32 + lane) & sz) == 0;
+            const bool sw = up ? before(s[e2], j[e2], s[e], j[e]) : before(s[e], j[e], s[e2], j[e2]);
+            if (sw) {
+              const double ts = s[e]; s[e] = s[e2]; s[e2] = ts;
+              const int tj = j[e]; j[e] = j[e2]; j[e2] = tj;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double os = __shfl_xor_sync(0xffffffffu, s[e], st);
+          const int oj = __shfl_xor_sync(0xffffffffu, j[e], st);
+          const bool up = ((e * 32 + lane) & sz) == 0;
+          const bool want_first = ((lane & st) == 0) == up;  // the lower position keeps the earlier when ascending
+          const bool take = want_first ? before(os, oj, s[e], j[e]) : before(s[e], j[e], os, oj);
+          if (take) { s[e] = os; j[e] = oj; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    cs[e * 32 + lane] = s[e];
+    cj[e * 32 + lane] = j[e];
+  }
+}
 constexpr int ADMIT_WARPS = 8;
 
 __device__ __forceinline__ double warp_sum_bcast(double v) {
@@ -712,15 +891,33 @@ __global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const
   const int NW = (N + 31) / 32;
   for (int row = blockIdx.x * ADMIT_WARPS + warp; row < rows_total; row += gridDim.x * ADMIT_WARPS) {
     const double* srow = S + static_cast<size_t>(row) * N;
-    double a = 0.0;
-    for (int j = lane; j < N; j += 32) a += __ldg(srow + j);
-    const double mu = warp_sum_bcast(a) / (double)N;
-    a = 0.0;
-    for (int j = lane; j < N; j += 32) {
-      const double t = __ldg(srow + j) - mu;
-      a += t * t;
+    // Eq.3 statistics with four independent partial sums per lane (the row is read from L2 once and then
+    // from L1; the summation order only moves the last ulps, which the C24 near-tie band covers)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = lane;
+    for (; j + 96 < N; j += 128) {
+      a0 += __ldg(srow + j);
+      a1 += __ldg(srow + j + 32);
+      a2 += __ldg(srow + j + 64);
+      a3 += __ldg(srow + j + 96);
     }
-    const double sigma = sqrt(warp_sum_bcast(a) / (double)N);
+    for (; j < N; j += 32) a0 += __ldg(srow + j);
+    const double mu = warp_sum_bcast((a0 + a1) + (a2 + a3)) / (double)N;
+    a0 = a1 = a2 = a3 = 0.0;
+    j = lane;
+    for (; j + 96 < N; j += 128) {
+      const double t0 = __ldg(srow + j) - mu, t1 = __ldg(srow + j + 32) - mu;
+      const double t2 = __ldg(srow + j + 64) - mu, t3 = __ldg(srow + j + 96) - mu;
+      a0 += t0 * t0;
+      a1 += t1 * t1;
+      a2 += t2 * t2;
+      a3 += t3 * t3;
+    }
+    for (; j < N; j += 32) {
+      const double t0 = __ldg(srow + j) - mu;
+      a0 += t0 * t0;
+    }
+    const double sigma = sqrt(warp_sum_bcast((a0 + a1) + (a2 + a3)) / (double)N);
     const double p = mu + sigma * z;
     // compaction (ascending j)
     int nc = 0;
@@ -762,25 +959,18 @@ __global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const
     __syncwarp();
     int ell = nc;
     if (tau < 1.0 && nc > 1) {
-      int P = 1;
+      int P = 32;
       while (P < nc) P <<= 1;
       for (int t = nc + lane; t < P; t += 32) { cs[t] = -INFINITY; cj[t] = INT_MAX; }
       __syncwarp();
-      for (int sz = 2; sz <= P; sz <<= 1) {
-        for (int st = sz >> 1; st > 0; st >>= 1) {
-          for (int t = lane; t < P; t += 32) {
-            const int u = t ^ st;
-            if (u > t) {
-              const bool up = ((t & sz) == 0);
-              const double ct = cs[t], cu = cs[u];
-              const int jt = cj[t], ju = cj[u];
-              const bool swap = up ? before(cu, ju, ct, jt) : before(ct, jt, cu, ju);
-              if (swap) { cs[t] = cu; cs[u] = ct; cj[t] = ju; cj[u] = jt; }
-            }
-          }
-          __syncwarp();
-        }
+      switch (P) {  // bitonic sort by (s desc, j asc) in registers (warp shuffles), P / 32 elements per lane
+        case 32: warp_bitonic<1>(cs, cj, lane); break;
+        case 64: warp_bitonic<2>(cs, cj, lane); break;
+        case 128: warp_bitonic<4>(cs, cj, lane); break;
+        case 256: warp_bitonic<8>(cs, cj, lane); break;
+        default: warp_bitonic<16>(cs, cj, lane); break;
       }
+      __syncwarp();
       const double m = cs[0];
       // cumulative masses in sorted order (warp scan, chunks of 32 with a carry)
       double carry = 0.0;
@@ -844,7 +1034,8 @@ cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double
   if (e != cudaSuccess) return e;
   const int rows = N * BH;
   if (k >= N || unified) {  // C15 / unified_prob: every row has all N candidates
-    k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, unified, nullptr, nullptr, q2k_num, q2k_idx, thresh, qbits);
+    k_admit_cta<<<rows, 256, sm, st>>>(N, rows, S, k, z, tau, unified, nullptr, nullptr, q2k_num, q2k_idx, thresh,
+                                       qbits);
     return cudaGetLastError();
   }
   // ovf[0] = overflow count, ovf[1..] = overflow rows
@@ -853,12 +1044,14 @@ cudaError_t launch_admit(int N, int BH, const double* S, int k, double z, double
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = min_i((rows + ADMIT_WARPS - 1) / ADMIT_WARPS, sms * 4);
+  const int grid = min_i((rows + ADMIT_WARPS - 1) / ADMIT_WARPS, sms * 8);
   const int wsm = ADMIT_WARPS * (ADMIT_CAP * 12 + 128 * 4);
   e = cudaFuncSetAttribute(k_admit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
   if (e != cudaSuccess) return e;
   k_admit_warp<<<grid, 256, wsm, st>>>(N, rows, S, k, z, tau, q2k_num, q2k_idx, thresh, qbits, ovf + 1, ovf);
-  k_admit_cta<<<rows, 256, sm, st>>>(N, S, k, z, tau, 0, ovf + 1, ovf, q2k_num, q2k_idx, thresh, qbits);
+  // overflow rows (more than ADMIT_CAP candidates) are rare: a small grid loops over the list
+  k_admit_cta<<<min_i(rows, sms * 2), 256, sm, st>>>(N, rows, S, k, z, tau, 0, ovf + 1, ovf, q2k_num, q2k_idx, thresh,
+                                                     qbits);
   return cudaGetLastError();
 }
 
