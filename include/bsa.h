@@ -23,7 +23,8 @@
  *  - Ownership: the caller allocates every buffer (device unless stated) and passes a CUDA stream
  *    (cudaStream_t, passed as void*; NULL = legacy default stream). The library never allocates,
  *    frees or synchronises; every call only enqueues work on `stream` and returns. Calls are
- *    reentrant; the only global state is the thread-local last-error string.
+ *    reentrant; the only global state is the thread-local last-error string and the opt-in
+ *    instrumentation below (a launch counter and event timing).
  *  - Errors: every call returns BSA_OK (0) or an error code; argument validation happens before
  *    any launch, so nothing is written on a validation error. bsa_last_error() gives the message.
  *  - Geometry: grid (T,H,W), block (ct,ch,cw), query-selection unit (ut,uh,uw) (the paper's window
@@ -209,11 +210,11 @@ enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
   BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT, BSA_K_COUNT
 };
-/* Total kernels this thread has launched through libbsa (always counted; cheap). */
+/* Total kernels launched through libbsa by this process (always counted; cheap). */
 int64_t bsa_launch_count(void);
-/* When enabled on the calling thread, every libbsa kernel launch is bracketed by a CUDA event pair
- * recorded on the launch stream (events are created lazily; this is a profiling aid, not for
- * graph capture). */
+/* When enabled (process-wide: autograd runs the backward on its own thread), every libbsa kernel launch is
+ * bracketed by a CUDA event pair recorded on the launch stream (events are created lazily; this is a
+ * profiling aid, not for graph capture). */
 int bsa_timing_enable(int on);
 /* Synchronises on the recorded events, writes per-kernel-id summed milliseconds ms[id] and launch
  * counts launches[id] for id < n (either may be NULL), then clears the record. */

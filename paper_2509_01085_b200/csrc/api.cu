@@ -1,8 +1,10 @@
 // api.cu — the extern "C" boundary of libbsa.so (declared and documented in include/bsa.h).
 // Validates every argument on the host, sizes workspaces, and enqueues the kernels of
 // select.cu / attn_fwd.cu / attn_bwd.cu on the caller's stream. Never allocates or synchronises.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -33,21 +35,24 @@ struct TimedRec {
   int id;
   cudaEvent_t a, b;
 };
-thread_local int64_t g_launches = 0;
-thread_local bool g_timing = false;
-thread_local std::vector<TimedRec> g_recs;
+// Process-wide (autograd runs the backward on its own worker thread, which must be counted and timed too).
+std::atomic<int64_t> g_launches{0};
+std::atomic<bool> g_timing{false};
+std::mutex g_recs_mu;
+std::vector<TimedRec> g_recs;
 
 // Runs one launcher (which may enqueue `nk` kernels) under kernel id `id`.
 template <class F>
 cudaError_t timed(int id, int nk, cudaStream_t st, F&& f) {
   g_launches += nk;
-  if (!g_timing) return f();
+  if (!g_timing.load(std::memory_order_relaxed)) return f();
   TimedRec r{id, nullptr, nullptr};
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
   cudaEventRecord(r.a, st);
   cudaError_t e = f();
   cudaEventRecord(r.b, st);
+  std::lock_guard<std::mutex> lk(g_recs_mu);
   g_recs.push_back(r);
   return e;
 }
@@ -500,7 +505,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   return BSA_OK;
 }
 
-int64_t bsa_launch_count(void) { return g_launches; }
+int64_t bsa_launch_count(void) { return g_launches.load(); }
 
 int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int32_t P, const void* src, void* dst,
                     void* stream) {
@@ -537,6 +542,7 @@ int bsa_timing_enable(int on) {
 }
 
 int bsa_timing_read(double* ms, int32_t* launches, int32_t n) {
+  std::lock_guard<std::mutex> lk(g_recs_mu);
   if (ms)
     for (int i = 0; i < n; ++i) ms[i] = 0.0;
   if (launches)

@@ -99,6 +99,42 @@ def bsa_attention(Q, K, V, layer):
     return _BSAFunction.apply(Q, K, V, layer)
 
 
+class _BSAQKVFunction(torch.autograd.Function):
+    """BSA attention on a fused projection: qkv [B, L, 3, Hh, d] -> O [B, L, Hh, d]. Q, K and V go into the library
+    as strided views of qkv and O is written in the model layout, so the forward moves no activation; the
+    backward writes dQ, dK, dV straight into the three slices of one d(qkv) tensor (include/bsa.h bsa_tensor)."""
+
+    @staticmethod
+    def forward(ctx, qkv, layer):
+        B, L, _, Hh, d = qkv.shape
+        Q, K, V = (qkv[:, :, i].transpose(1, 2) for i in range(3))
+        O = torch.empty(B, L, Hh, d, dtype=qkv.dtype, device=qkv.device)
+        layer.forward(Q, K, V, out=O.transpose(1, 2))
+        layer._fwd_count = getattr(layer, "_fwd_count", 0) + 1
+        ctx.layer, ctx.count = layer, layer._fwd_count
+        ctx.save_for_backward(qkv, O)
+        return O
+
+    @staticmethod
+    def backward(ctx, dO):
+        layer = ctx.layer
+        if layer._fwd_count != ctx.count:
+            raise BSAError("BSA backward after another forward through the same layer (use one layer per call site)")
+        qkv, O = ctx.saved_tensors
+        if dO.stride(-1) != 1:
+            dO = dO.contiguous()
+        dqkv = torch.empty_like(qkv)
+        Q, K, V = (qkv[:, :, i].transpose(1, 2) for i in range(3))
+        grads = tuple(dqkv[:, :, i].transpose(1, 2) for i in range(3))
+        layer.backward(dO.transpose(1, 2), out=grads, saved=(Q, K, V, O.transpose(1, 2)))
+        return dqkv, None
+
+
+def bsa_attention_qkv(qkv, layer):
+    """Differentiable BSA attention of a fused [B, L, 3, Hh, d] projection -> [B, L, Hh, d] (no layout copies)."""
+    return _BSAQKVFunction.apply(qkv, layer)
+
+
 class BSASelfAttention(torch.nn.Module):
     """The attention op of a DiT block with BSA's sparsity: Q, K, V [B, Hh, L, d] bf16 -> O."""
 
@@ -132,3 +168,33 @@ class BSASelfAttention(torch.nn.Module):
 
     def forward(self, Q, K, V):
         return bsa_attention(Q, K, V, self._layer())
+
+    def forward_qkv(self, qkv):
+        """qkv [B, L, 3, Hh, d] (a fused projection) -> O [B, L, Hh, d]."""
+        return bsa_attention_qkv(qkv, self._layer())
+
+
+class DiTAttentionBlock(torch.nn.Module):
+    """The self-attention half of a DiT block (Wan-style, the paper's base model) with BSA as the
+    attention: x [B, L, C] -> LayerNorm -> fused QKV projection [B, L, 3, Hh, d] -> BSA (strided, no copies)
+    -> out-projection -> residual. The projections are plain library GEMMs (torch / cuBLAS); every step of the
+    attention runs in libbsa. C = Hh * d (Wan2.1-1.3B: 12 x 128 = 1536)."""
+
+    def __init__(self, geom: Geometry, B: int, Hh: int, d: int, schedule: AnnealSchedule | None = None,
+                 r: float = 0.5, f: float = 0.1, tau: float = 0.9, device="cuda", dtype=torch.bfloat16):
+        super().__init__()
+        C = Hh * d
+        self.Hh, self.d = Hh, d
+        self.norm = torch.nn.LayerNorm(C, elementwise_affine=False, device=device, dtype=dtype)
+        self.qkv = torch.nn.Linear(C, 3 * C, bias=True, device=device, dtype=dtype)
+        self.out = torch.nn.Linear(C, C, bias=True, device=device, dtype=dtype)
+        self.attn = BSASelfAttention(geom, B, Hh, d, schedule=schedule, r=r, f=f, tau=tau, device=device)
+
+    def set_step(self, step: int):
+        self.attn.set_step(step)
+
+    def forward(self, x):
+        B, L, C = x.shape
+        qkv = self.qkv(self.norm(x)).view(B, L, 3, self.Hh, self.d)
+        o = self.attn.forward_qkv(qkv)
+        return x + self.out(o.reshape(B, L, C))
