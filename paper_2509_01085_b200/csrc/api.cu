@@ -500,7 +500,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
                                        dVv.sb == Hh * dVv.sh);
   if (e == cudaSuccess)
     e = timed(BSA_K_ATTN_BWD, one_launch ? 1 : B, st, [&] { return bsa::launch_bwd_main(a, st); });
-  if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 2, st, [&] { return bsa::launch_bwd_finalize(a, st); });
+  if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 1, st, [&] { return bsa::launch_bwd_finalize(a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_bwd");
   return BSA_OK;
 }

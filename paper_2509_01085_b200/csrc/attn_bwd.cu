@@ -815,36 +815,50 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 }
 
 // ------------------------------------------------------------------------------------ finalize
-__global__ void k_bwd_zero_pruned(int BH, int L, int d, const int* __restrict__ donor, const Rows dQ) {
-  size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int vpr = d / 8;
-  if (v >= static_cast<size_t>(BH) * L * vpr) return;
-  size_t rowi = v / vpr;
-  int c = static_cast<int>(v % vpr) * 8;
-  const int t = static_cast<int>(rowi % L);
-  if (donor[rowi] != t)
-    *reinterpret_cast<uint4*>(dQ.row(static_cast<int>(rowi / L), t) + c) = make_uint4(0, 0, 0, 0);
-}
-
-__global__ void k_bwd_finalize(int BH, int Lq, int d, float scale, const int* __restrict__ kept_tok,
-                               const float* __restrict__ dQacc, const Rows dQ) {
-  size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int vpr = d / 8;
-  if (v >= static_cast<size_t>(BH) * Lq * vpr) return;
-  size_t prow = v / vpr;
-  int c = static_cast<int>(v % vpr) * 8;
-  const int bh = static_cast<int>(prow / Lq);
-  int tok = kept_tok[prow];
-  const float4* src = reinterpret_cast<const float4*>(dQacc + prow * d + c);
-  float4 a = src[0], b = src[1];
-  __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x * scale, a.y * scale), h1 = __floats2bfloat162_rn(a.z * scale, a.w * scale);
-  __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x * scale, b.y * scale), h3 = __floats2bfloat162_rn(b.z * scale, b.w * scale);
-  uint4 o;
-  o.x = *reinterpret_cast<uint32_t*>(&h0);
-  o.y = *reinterpret_cast<uint32_t*>(&h1);
-  o.z = *reinterpret_cast<uint32_t*>(&h2);
-  o.w = *reinterpret_cast<uint32_t*>(&h3);
-  *reinterpret_cast<uint4*>(dQ.row(bh, tok) + c) = o;
+// dQ of one (b,h, block): kept tokens (ascending) take scale * dQacc of their packed row kept_off[b] + rank,
+// pruned tokens get 0 (reading C10). One CTA per block: the block's donors decide kept / pruned, a ballot
+// prefix gives the rank, and every row is written once with 16-byte stores.
+template <int D>
+__global__ void __launch_bounds__(256) k_bwd_finalize(Geo g, int Lq, float scale, const int* __restrict__ kept_off,
+                                                      const int* __restrict__ donor, const float* __restrict__ dQacc,
+                                                      const Rows dQ) {
+  constexpr int MAXT = 128, VPR = D / 8;
+  __shared__ int s_tok[MAXT], s_prow[MAXT], s_wk[8];
+  const int blk = blockIdx.x, bh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Box x = block_box(g, blk);
+  const int n = box_size(x);
+  const int t = threadIdx.x;
+  bool kept = false;
+  if (t < n) {
+    const int tok = box_token(g, x, t);
+    s_tok[t] = tok;
+    kept = __ldg(donor + static_cast<size_t>(bh) * g.L + tok) == tok;
+  }
+  const unsigned kb = __ballot_sync(0xffffffffu, kept);
+  if (lane == 0) s_wk[warp] = __popc(kb);
+  __syncthreads();
+  if (t < n) {
+    int pos = __popc(kb & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += s_wk[w];
+    s_prow[t] = kept ? static_cast<int>(static_cast<size_t>(bh) * Lq + kept_off[blk] + pos) : -1;
+  }
+  __syncthreads();
+  bf16* dqh = dQ.head(bh);
+  for (int v = t; v < n * VPR; v += 256) {
+    const int i = v / VPR, c = (v % VPR) * 8;
+    const int prow = s_prow[i];
+    uint4 o = make_uint4(0, 0, 0, 0);
+    if (prow >= 0) {
+      const float4* src = reinterpret_cast<const float4*>(dQacc + static_cast<size_t>(prow) * D + c);
+      const float4 a = src[0], b = src[1];
+      o.x = pack_bf16(a.x * scale, a.y * scale);
+      o.y = pack_bf16(a.z * scale, a.w * scale);
+      o.z = pack_bf16(b.x * scale, b.y * scale);
+      o.w = pack_bf16(b.z * scale, b.w * scale);
+    }
+    *reinterpret_cast<uint4*>(dqh + s_tok[i] * dQ.sl + c) = o;
+  }
 }
 
 template <int D, int BT>
@@ -909,12 +923,11 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
-  const size_t rows = static_cast<size_t>(a.BH) * a.Lq;
-  size_t tz = static_cast<size_t>(a.BH) * a.g.L * (a.d / 8);
-  k_bwd_zero_pruned<<<static_cast<unsigned>((tz + 255) / 256), 256, 0, st>>>(a.BH, a.g.L, a.d, a.donor, a.dQ);
-  size_t tf = rows * (a.d / 8);
-  k_bwd_finalize<<<static_cast<unsigned>((tf + 255) / 256), 256, 0, st>>>(a.BH, a.Lq, a.d, a.scale, a.kept_tok,
-                                                                          a.dQacc, a.dQ);
+  const dim3 grid(a.g.N, a.BH);
+  if (a.d == 128)
+    k_bwd_finalize<128><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ);
+  else
+    k_bwd_finalize<64><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ);
   return cudaGetLastError();
 }
 

@@ -668,21 +668,32 @@ template <int D, int BT>
 __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Rows V, uint8_t* __restrict__ img) {
   constexpr int CPR = D / 8;        // 16-byte chunks per row
   constexpr int CHUNKS = BT * CPR;  // per tensor
+  constexpr int PER = 2 * CHUNKS / 256;  // chunks per thread (K and V)
   const int j = blockIdx.x, bh = blockIdx.y;
   const Box x = block_box(g, j);
   uint8_t* dst = img + (static_cast<size_t>(bh) * g.N + j) * (2 * BT * D * 2);
   const bf16* kh = K.head(bh);
   const bf16* vh = V.head(bh);
-  for (int v = threadIdx.x; v < 2 * CHUNKS; v += blockDim.x) {
+  // every load of the thread is issued before the first store (memory-level parallelism)
+  uint4 val[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int v = threadIdx.x + 256 * k;
     const int t = v / CHUNKS, w = v % CHUNKS;
     const int r = w / CPR, c = w % CPR;
     const int lw = r % g.cw, lh = (r / g.cw) % g.ch, lt = r / (g.cw * g.ch);
-    uint4 val = make_uint4(0, 0, 0, 0);
+    val[k] = make_uint4(0, 0, 0, 0);
     if (lt < x.e[0] && lh < x.e[1] && lw < x.e[2]) {
-      const size_t tok = (static_cast<size_t>(x.o[0] + lt) * g.H + (x.o[1] + lh)) * g.W + (x.o[2] + lw);
-      val = *reinterpret_cast<const uint4*>((t ? vh + tok * V.sl : kh + tok * K.sl) + c * 8);
+      const long long tok = (static_cast<long long>(x.o[0] + lt) * g.H + (x.o[1] + lh)) * g.W + (x.o[2] + lw);
+      val[k] = __ldg(reinterpret_cast<const uint4*>((t ? vh + tok * V.sl : kh + tok * K.sl) + c * 8));
     }
-    *reinterpret_cast<uint4*>(dst + t * (BT * D * 2) + (c >> 3) * (BT * 128) + sw128_off(r, c & 7)) = val;
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int v = threadIdx.x + 256 * k;
+    const int t = v / CHUNKS, w = v % CHUNKS;
+    const int r = w / CPR, c = w % CPR;
+    *reinterpret_cast<uint4*>(dst + t * (BT * D * 2) + (c >> 3) * (BT * 128) + sw128_off(r, c & 7)) = val[k];
   }
 }
 
