@@ -208,7 +208,8 @@ int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int3
  * Kernel ids reported by bsa_timing_read / counted by bsa_launch_count. */
 enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
-  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT, BSA_K_COUNT
+  BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT,
+  BSA_K_GROUP, BSA_K_COUNT
 };
 /* Total kernels launched through libbsa by this process (always counted; cheap). */
 int64_t bsa_launch_count(void);

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -147,15 +148,30 @@ SelKvWs selkv_ws(const bsa::Geo& g, size_t BH, int d) {
   return w;
 }
 
-// Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL).
+// Forward tiles grouped by KV-list similarity (group.cu): opt-in with BSA_FWD_GROUPING=1 in the environment.
+// Measured at 32k: attn_fwd 0.866 -> 0.752 ms with grouped tiles, but the grouping kernels
+// cost 0.147 ms, so consecutive query blocks per tile stay the default.
+bool fwd_grouping() {
+  static const bool on = [] {
+    const char* e = std::getenv("BSA_FWD_GROUPING");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL) + the tile
+// grouping's scratch and tile table (G >= 2).
 struct FwdWs {
-  size_t kv, qs, total;
+  size_t kv, qs, grp, perm, total;
 };
-FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d) {
+FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   FwdWs w;
+  const int G = 128 / SR;
   w.kv = 0;
   w.qs = w.kv + align256(BH * g.N * 2 * static_cast<size_t>(g.BT) * d * 2);
-  w.total = w.qs + align256(BH * Lq * d * 2);
+  w.grp = w.qs + align256(BH * Lq * d * 2);
+  w.perm = w.grp + align256(G >= 2 ? bsa::group_ws_bytes(g.N, static_cast<int>(BH)) : 0);
+  w.total = w.perm + align256(G >= 2 ? BH * static_cast<size_t>(bsa::group_ntiles(g.N, G)) * G * 4 : 0);
   return w;
 }
 
@@ -261,7 +277,7 @@ int bsa_workspace_bytes(int op, const bsa_geom* g, double r, int32_t B, int32_t 
   int lq = 0, mk = 0;
   host_sizes(G, r, &lq, &mk);
   if (op == BSA_OP_ATTN_FWD) {
-    *bytes = fwd_ws(G, BH, lq, d).total;
+    *bytes = fwd_ws(G, BH, lq, d, bsa::slot_rows(mk)).total;
     return BSA_OK;
   }
   if (op == BSA_OP_ATTN_BWD) {
@@ -388,7 +404,7 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   CHECK(check_attn_geom(G, r, &Lq, &SR));
   size_t BH = static_cast<size_t>(B) * Hh;
   const bsa::bf16* Qs = static_cast<const bsa::bf16*>(q_packed);
-  FwdWs w = fwd_ws(G, BH, Lq, d);
+  FwdWs w = fwd_ws(G, BH, Lq, d, SR);
   if (!ws || ws_bytes < w.total)
     return fail(BSA_ERR_SELECTION_MISMATCH, "workspace %zu < required %zu bytes", ws_bytes, w.total);
   CHECK(check_device());
@@ -423,6 +439,17 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.O = Ov;
   a.lse = lse;
   a.kv_img = kv_img;
+  a.perm = nullptr;
+  a.ntiles = 0;
+  const int Gt = 128 / SR;
+  if (e == cudaSuccess && Gt >= 2 && fwd_grouping()) {
+    int* perm = reinterpret_cast<int*>(base + w.perm);
+    e = timed(BSA_K_GROUP, 3, st, [&] {
+      return bsa::launch_group(G.N, static_cast<int>(BH), Gt, q2k_num, q2k_idx, base + w.grp, perm, st);
+    });
+    a.perm = perm;
+    a.ntiles = bsa::group_ntiles(G.N, Gt);
+  }
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_FILL, 1, st, [&] { return bsa::launch_fill(a.BH, G.L, d, donor, a.O, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_fwd");

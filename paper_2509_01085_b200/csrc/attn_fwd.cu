@@ -57,6 +57,8 @@ struct FwdParams {
   const int* kept_tok;
   const int* q2k_num;
   const int* q2k_idx;
+  const int* perm;   // [BH][ntiles][G] query block of each tile slot (-1 = empty), or NULL: tile t = blocks t G ..
+  int ntiles;
   float scale_log2;  // scale * log2(e)
   Rows O;            // raster output, strided
   float* lse;
@@ -154,11 +156,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   constexpr int W_ALLOC = 8, W_PROD = 9, W_PV = 10, W_QK = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
+  // query block of tile slot k (grouped tiles: group.cu; else consecutive blocks)
+  auto slot_qb = [&](int k) {
+    if (p.perm) return p.perm[(static_cast<size_t>(bh) * p.ntiles + tile) * G + k];
+    const int qb = tile * G + k;
+    return qb < g.N ? qb : -1;
+  };
   if (tid < G) {
-    int qb = tile * G + tid;
-    s_qb[tid] = qb < g.N ? qb : -1;
-    s_nk[tid] = qb < g.N ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
-    s_koff[tid] = qb < g.N ? p.kept_off[qb] : 0;
+    const int qb = slot_qb(tid);
+    s_qb[tid] = qb;
+    s_nk[tid] = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
+    s_koff[tid] = qb >= 0 ? p.kept_off[qb] : 0;
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
   if (tid < 8) s_clsmask[tid] = p.clsmask[tid];
@@ -182,9 +190,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   // so reading past q2k_num is safe; only the first q2k_num are used below).
   constexpr int QPF = 2;  // list entries prefetched per thread
   const int per = FWD_THREADS / G, pgi = tid / per, pt = tid % per;
-  const int pqb = tile * G + pgi;
-  const size_t prow = static_cast<size_t>(bh) * g.N + (pqb < g.N ? pqb : 0);
-  const int pnum = pqb < g.N ? p.q2k_num[prow] : 0;
+  const int pqb = pgi < G ? slot_qb(pgi) : -1;
+  const size_t prow = static_cast<size_t>(bh) * g.N + (pqb >= 0 ? pqb : 0);
+  const int pnum = pqb >= 0 ? p.q2k_num[prow] : 0;
   int pj[QPF];
 #pragma unroll
   for (int e = 0; e < QPF; ++e) pj[e] = (pt + e * per < g.N) ? p.q2k_idx[prow * g.N + pt + e * per] : 0;
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   // admission bitmap of each slot (q2k lists). The G lists are read concurrently (thread group gi
   // of FWD_THREADS / G threads per slot): one dependent global round trip instead of G.
-  if (pqb < g.N) {
+  if (pqb >= 0) {
 #pragma unroll
     for (int e = 0; e < QPF; ++e)
       if (pt + e * per < pnum) atomicOr(&bits[pgi * NW + (pj[e] >> 5)], 1u << (pj[e] & 31));
@@ -640,6 +648,8 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.lse = a.lse;
   p.kv_img = a.kv_img;
   p.Qs = a.Qs;
+  p.perm = a.perm;
+  p.ntiles = a.ntiles;
   for (int cls = 0; cls < 8; ++cls) {  // key-validity mask per block-extent class (ragged last block per axis)
     const Geo& g = a.g;
     const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
@@ -652,7 +662,7 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
     }
     p.clsmask[cls] = m;
   }
-  int ntiles = (a.g.N + p.G - 1) / p.G;
+  int ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
   if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_fwd<128, 32>(p, ntiles, a.BH, st);
   if (a.d == 64 && a.g.BT == 64) return run_fwd<64, 64>(p, ntiles, a.BH, st);

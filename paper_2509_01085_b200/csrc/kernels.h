@@ -58,6 +58,8 @@ struct FwdArgs {
   Rows O;
   float* lse;
   const uint8_t* kv_img;  // workspace: K|V block images (launch_kv_image)
+  const int* perm;        // [BH][ntiles][G] query blocks of each tile (launch_group), or NULL: consecutive blocks
+  int ntiles;
 };
 cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
@@ -65,6 +67,12 @@ cudaError_t debug_trace_fwd(void* dev_buf, int cta);
 cudaError_t debug_trace_bwd(void* dev_buf, int cta);
 cudaError_t debug_progress_bwd(void* dev_ptr);
 cudaError_t launch_fill(int BH, int L, int d, const int* donor, Rows O, cudaStream_t st);
+
+// forward tiles: query blocks with similar KV lists share a tile (group.cu)
+size_t group_ws_bytes(int N, int BH);
+int group_ntiles(int N, int G);
+cudaError_t launch_group(int N, int BH, int G, const int* q2k_num, const int* q2k_idx, void* ws, int* perm,
+                         cudaStream_t st);
 
 // Ulysses sequence parallelism: row reorders around the all-to-all (sp.cu)
 cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, const void* src, void* dst,
