@@ -178,7 +178,7 @@ FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
 // Backward workspace: gathered Q^s (only when q_packed is NULL), Q^s|dO^s query-block images
 // (N * SR padded rows per head), D = rowsum(dO^s O^s), fp32 dQ accumulator.
 struct BwdWs {
-  size_t qs, img, dv, dq, total;
+  size_t qs, img, dv, dq, ctr, total;
 };
 BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   BwdWs w;
@@ -186,7 +186,8 @@ BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   w.img = w.qs + align256(BH * Lq * d * 2);
   w.dv = w.img + align256(BH * g.N * static_cast<size_t>(SR) * d * 4);
   w.dq = w.dv + align256(BH * g.N * static_cast<size_t>(SR) * 8);
-  w.total = w.dq + align256(BH * Lq * d * 4);
+  w.ctr = w.dq + align256(BH * Lq * d * 4);
+  w.total = w.ctr + align256(BH * 4);  // work counters of the main kernel (one per launch, <= B <= BH)
   return w;
 }
 
@@ -522,6 +523,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.qdo_img = base + w.img;
   a.lsed = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
+  a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
   const bool one_launch = (B == 1) || (Kv.sb == Hh * Kv.sh && Vv.sb == Hh * Vv.sh && dKv.sb == Hh * dKv.sh &&
                                        dVv.sb == Hh * dVv.sh);

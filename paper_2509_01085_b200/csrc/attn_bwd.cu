@@ -234,8 +234,10 @@ struct BwdParams {
   const int* k2q_num;
   const int* k2q_idx;
   float* dQacc;
-  int bh0;             // first (b,h) of this launch: blockIdx.y + bh0 indexes the internal buffers, blockIdx.y
-                       // is the head coordinate of the K/V/dK/dV tensor maps
+  int bh0;             // first (b,h) of this launch: hc + bh0 indexes the internal buffers, hc (item / N) is the
+                       // head coordinate of the K/V/dK/dV tensor maps
+  int items;           // work items of this launch: heads x N KV blocks, item = hc * N + j
+  int* work_ctr;       // next unclaimed item (zeroed before the launch)
   float scale_log2;
   float scale;
 };
@@ -274,15 +276,15 @@ struct BwdSmem {
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
-// A CTA handles BWD_NB (= 2; 4 / 8 / 16 measured 1.72 / 1.82 / 1.97 ms vs 1.71 at 32k: tail imbalance)
-// consecutive KV blocks of one head, one after another, with every barrier phase
-// counted across them (chunk counter c runs over all of the CTA's chunks): the dQ drain of a block's last
-// chunks, its dK/dV epilogue and the next block's K/V load overlap the next block's first chunks, and the
-// CTA prologue (barrier init, TMEM allocation, stage zeroing) is paid once per BWD_NB blocks.
-#ifndef BSA_BWD_NB
-#define BSA_BWD_NB 2
-#endif
-constexpr int BWD_NB = BSA_BWD_NB;
+// Persistent CTAs (one per SM): the producer warp claims KV blocks (items over all heads of the launch) with
+// an atomic counter and publishes them through a ring in shared memory; every role walks the same item
+// sequence with all barrier phases counted across items (chunk counter c runs over all of the CTA's chunks).
+// So the dQ drain of a block's last chunks, its dK/dV epilogue and the next block's K/V load overlap the next
+// block's first chunks, the CTA prologue (barrier init, TMEM allocation, stage zeroing) is paid once per SM,
+// and dynamic claiming bounds the tail by one block (fixed runs of 2 / 4 / 8 / 16 consecutive blocks per CTA
+// measured 1.71 / 1.72 / 1.82 / 1.97 ms at 32k: tail imbalance of static assignment).
+constexpr int ITEM_RING = 8;
+constexpr int ITEM_READERS = 10;  // S/dP issuer, gradient issuer, 4 softmax warps, 4 drain warps
 
 template <int D, int BT>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
@@ -302,48 +304,38 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   };
 
   __shared__ __align__(8) uint64_t bar_kv, bar_c_full[2], bar_c_empty[2], bar_sd_full, bar_sd_free, bar_ps_full,
-      bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc, bar_acc_free;
+      bar_ps_free, bar_dq_full[2], bar_dq_free[2], bar_acc, bar_acc_free, bar_item_full[ITEM_RING],
+      bar_item_empty[ITEM_RING];
+  __shared__ int s_item[ITEM_RING];
   __shared__ uint32_t s_tmem;
   // Chunk metadata ring (first packed row, kept count, block id of each slot; row -1 = empty slot), written
   // by the producer for chunk c into entry c & 3. Four deep: the producer rewrites an entry only after
   // the MMAs of chunk c-2 completed, by which time the softmax and drain warps are done with chunk c-4.
-  __shared__ int s_row0[4][BWD_MAX_G], s_nk[4][BWD_MAX_G], s_qb[4][BWD_MAX_G];
+  __shared__ int s_row0[4][BWD_MAX_G], s_nk[4][BWD_MAX_G];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bh = p.bh0 + static_cast<int>(blockIdx.y), hc = static_cast<int>(blockIdx.y);
   const int G = p.G, SR = p.SR;
-  const int j_first = blockIdx.x * BWD_NB, j_end = min_i(j_first + BWD_NB, g.N);
-  // per KV block of this CTA: admitting query blocks, chunks, rotation of the chunk order (concurrent CTAs
-  // start on different query blocks: no L2 hot spot)
-  auto nq_of = [&](int j) { return p.k2q_num[static_cast<size_t>(bh) * g.N + j]; };
-  auto rot_of = [&](int j, int nch) {
+  // per KV block (hc, j): admitting query blocks, rotation of the chunk order (concurrent CTAs start on
+  // different query blocks: no L2 hot spot)
+  auto nq_of = [&](int bh, int j) { return p.k2q_num[static_cast<size_t>(bh) * g.N + j]; };
+  auto rot_of = [&](int bh, int j, int nch) {
     return nch > 0 ? static_cast<int>((static_cast<unsigned>(j) * 2654435761u + bh * 40503u) % nch) : 0;
+  };
+  // item `it` of this CTA (-1: no work left); every reader hands its ring slot back after reading it
+  auto read_item = [&](int it) {
+    const int s = it % ITEM_RING;
+    bwait(&bar_item_full[s], (it / ITEM_RING) & 1);
+    const int v = s_item[s];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar_item_empty[s]);
+    return v;
   };
 
 #ifdef BSA_TRACE
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
-  // Producer: metadata of the CTA's first chunk (k2q_num -> k2q_idx -> kept_off, three dependent loads)
-  // fetched before the prologue barrier, so its latency overlaps the barrier init, TMEM allocation and
-  // stage zeroing.
-  int pf_j = -1, pf_qbl = 0, pf_nk = 0, pf_row0 = -1;
-  if (warp == 10) {  // W_PROD
-    for (int j = j_first; j < j_end; ++j) {
-      const int nq = nq_of(j), nch = (nq + G - 1) / G;
-      if (nch == 0) continue;
-      const int cc = rot_of(j, nch);
-      if (lane < min_i(G, nq - cc * G)) {
-        pf_qbl = p.k2q_idx[(static_cast<size_t>(bh) * g.N + j) * g.N + cc * G + lane];
-        const int ko = p.kept_off[pf_qbl];
-        pf_nk = p.kept_off[pf_qbl + 1] - ko;
-        pf_row0 = bh * p.Lq + ko;
-      }
-      pf_j = j;
-      break;
-    }
-  }
 #ifdef BSA_HANG_DEBUG
   if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && g_hang_rec) {
     unsigned* m = g_hang_rec + 8 + 8 * 500;
@@ -368,6 +360,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     mbar_init(&bar_ps_free, 1);
     mbar_init(&bar_acc, 1);
     mbar_init(&bar_acc_free, 128);
+    for (int s = 0; s < ITEM_RING; ++s) {
+      mbar_init(&bar_item_full[s], 1);
+      mbar_init(&bar_item_empty[s], ITEM_READERS);
+    }
     fence_mbar_init();
   }
   // Warp roles (the warp arbiter favours higher ids, so the single-thread producer and MMA roles get the
@@ -393,23 +389,29 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   if (tid == 0) CTA_STAMP(4);
 
   if (warp == W_PROD) {
-    // ============================ producer (lane 0 issues TMA; all lanes fetch metadata)
-    int c = 0, nacc = 0;  // global chunk counter; blocks with MMAs so far (bar_kv / bar_acc phases)
-    for (int j = j_first; j < j_end; ++j) {
-      const int nq = nq_of(j), nchunks = (nq + G - 1) / G, crot = rot_of(j, nchunks);
+    // ============================ producer (lane 0 claims items and issues TMA; all lanes fetch metadata)
+    int c = 0;  // global chunk counter
+    for (int it = 0;; ++it) {
+      if (lane == 0) {  // claim the next item and publish it once every reader released the slot's last use
+        const int rs = it % ITEM_RING;
+        if (it >= ITEM_RING) bwait(&bar_item_empty[rs], ((it / ITEM_RING) - 1) & 1);
+        const int v = atomicAdd(p.work_ctr, 1);
+        s_item[rs] = v < p.items ? v : -1;
+        mbar_arrive(&bar_item_full[rs]);
+      }
+      __syncwarp();
+      const int item = s_item[it % ITEM_RING];
+      if (item < 0) break;
+      const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
+      const int nq = nq_of(bh, j), nchunks = (nq + G - 1) / G, crot = rot_of(bh, j, nchunks);
       if (nchunks == 0) continue;
       const int* qlist = p.k2q_idx + (static_cast<size_t>(bh) * g.N + j) * g.N;
-      ++nacc;  // (the block's K/V tiles are loaded by the S/dP issuer, their first consumer)
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
         const int cc = (cl + crot) % nchunks;
         const int nb = min_i(G, nq - cc * G);
         int row0 = -1, nk = 0, qbl = 0;
-        if (c == 0 && j == pf_j) {  // prefetched before the prologue barrier
-          row0 = pf_row0;
-          nk = pf_nk;
-          qbl = pf_qbl;
-        } else if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
+        if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
           qbl = qlist[cc * G + lane];
           int ko = p.kept_off[qbl];
           nk = p.kept_off[qbl + 1] - ko;
@@ -422,16 +424,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (lane < G) {
           s_row0[ring][lane] = row0;
           s_nk[ring][lane] = nk;
-          s_qb[ring][lane] = qbl;
         }
         __syncwarp();
+        const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
         if (lane == 0) {
-          const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
           mbar_expect_tx(&bar_c_full[s], nb * (blk_bytes + ld_bytes));
           BWD_TRACE(0, c);
           if (c == 0) CTA_STAMP(11);
-          for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
-            const size_t qimg = static_cast<size_t>(bh) * g.N + s_qb[ring][gi];
+        }
+        for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
+          const int qb_gi = __shfl_sync(0xffffffffu, qbl, gi);
+          if (lane == 0) {
+            const size_t qimg = static_cast<size_t>(bh) * g.N + qb_gi;
             bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + qimg * blk_bytes, blk_bytes, &bar_c_full[s]);
             bulk_load(stage_ld(s) + gi * 2 * SR, p.lsed + qimg * 2 * SR, ld_bytes, &bar_c_full[s]);
           }
@@ -459,8 +463,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     const uint64_t dP = umma_desc_sw128(smem_u32(sP), 8192, 1024), dS = umma_desc_sw128(smem_u32(sdS), 8192, 1024);
     const uint64_t dSa = umma_desc_sw128(smem_u32(sdS), 16, 1024);
     int c = 0, nacc = 0;
-    for (int j = j_first; j < j_end; ++j) {
-      const int nchunks = (nq_of(j) + G - 1) / G;
+    for (int it = 0;; ++it) {
+      const int item = read_item(it);
+      if (item < 0) break;
+      const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
+      const int nchunks = (nq_of(bh, j) + G - 1) / G;
       if (nchunks == 0) continue;
       if (warp == W_SD) {
         // K/V tiles of the block: the previous block's are read until its last MMA (bar_acc)
@@ -557,19 +564,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       }
       ++nacc;
     }
-#ifdef BSA_TRACE
-  } else if (warp == W_ALLOC) {
-    // debug observer (trace builds only): when each chunk's loads land
-    if (lane == 0) {
-      int c = 0;
-      for (int j = j_first; j < j_end; ++j)
-        for (int cl = 0; cl < (nq_of(j) + G - 1) / G; ++cl, ++c) {
-          bwait(&bar_c_full[c & 1], (c >> 1) & 1);
-          BWD_TRACE(12, c);
-        }
-    }
-    __syncwarp();
-#endif
   } else if (warp < 4) {
     // ============================ gradient softmax (thread == query row == TMEM lane) + dK/dV epilogue
     const int q4 = warp;
@@ -582,8 +576,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     const uint32_t sP_u = smem_u32(sP) + row * 128, sdS_u = smem_u32(sdS) + row * 128;
     int c = 0, nacc = 0;
     bool store_pending = false;  // a dK/dV TMA store still reading sP/sdS (issued by row 0)
-    for (int j = j_first; j < j_end; ++j) {
-      const int nchunks = (nq_of(j) + G - 1) / G;
+    for (int it = 0;; ++it) {
+      const int item = read_item(it);
+      if (item < 0) break;
+      // only `item` stays live across the chunk loop (the block coordinates are re-derived for the store)
+      const int nchunks = (p.k2q_num[static_cast<size_t>(p.bh0) * g.N + item] + G - 1) / G;
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int s = c & 1;
         if (row == 0) PROG(3, c * 8 + 0);
@@ -688,6 +685,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (row == 0) {
+        const int hc = item / g.N, j = item - hc * g.N;
         const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
         for (int cb = 0; cb < NCB; ++cb) {
           tma_store_5d(&p.mdK, sP + cb * BT * 128, cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
@@ -715,8 +713,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     const int R = p.dq_rows, nsub = 32 / R, per_slot = SROWS / R;
     int slot_i = 0;
     int c = 0;
-    for (int j = j_first; j < j_end; ++j) {
-      const int nchunks = (nq_of(j) + G - 1) / G;
+    for (int it = 0;; ++it) {
+      const int item = read_item(it);
+      if (item < 0) break;
+      const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
+      const int nchunks = (nq_of(bh, j) + G - 1) / G;
       for (int cl = 0; cl < nchunks; ++cl, ++c) {
         const int qbuf = c & 1;
         if (lane == 0) PROG(4 + q4, c * 8 + 0);
@@ -804,8 +805,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     unsigned sm_id;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
-    int nch = 0;
-    for (int j = j_first; j < j_end; ++j) nch += (nq_of(j) + G - 1) / G;
+    const int nch = 0;
     e[0] = t_start;
     e[1] = t1;
     e[2] = sm_id;
@@ -862,11 +862,14 @@ __global__ void __launch_bounds__(256) k_bwd_finalize(Geo g, int Lq, float scale
 }
 
 template <int D, int BT>
-static cudaError_t run_bwd(const BwdParams& p, int heads, cudaStream_t st) {
+static cudaError_t run_bwd(const BwdParams& p, cudaStream_t st) {
   constexpr int smem = BwdSmem<D, BT>::TOTAL;
   cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_attn_bwd<D, BT><<<dim3((p.g.N + BWD_NB - 1) / BWD_NB, heads), BWD_THREADS, smem, st>>>(p);
+  int dev = 0, sms = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  k_attn_bwd<D, BT><<<dim3(static_cast<unsigned>(min_i(p.items, sms))), BWD_THREADS, smem, st>>>(p);  // persistent
   return cudaGetLastError();
 }
 
@@ -905,7 +908,12 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
                    heads_uniform(a.dV, a.B);
   const int launches = one ? 1 : a.B, heads = one ? a.BH : a.Hh;
+  // one work counter per launch, zeroed on the stream (the persistent CTAs claim items from it)
+  cudaError_t ez = cudaMemsetAsync(a.work_ctr, 0, sizeof(int) * launches, st);
+  if (ez != cudaSuccess) return ez;
+  p.items = heads * a.g.N;
   for (int b = 0; b < launches; ++b) {
+    p.work_ctr = a.work_ctr + b;
     const Rows* ts[4] = {&a.K, &a.V, &a.dK, &a.dV};
     CUtensorMap* ms[4] = {&p.mK, &p.mV, &p.mdK, &p.mdV};
     for (int t = 0; t < 4; ++t)
@@ -913,10 +921,10 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
         return cudaErrorInvalidValue;
     p.bh0 = b * a.Hh;
     cudaError_t e = cudaErrorInvalidValue;
-    if (a.d == 128 && a.g.BT == 64) e = run_bwd<128, 64>(p, heads, st);
-    else if (a.d == 128 && a.g.BT == 32) e = run_bwd<128, 32>(p, heads, st);
-    else if (a.d == 64 && a.g.BT == 64) e = run_bwd<64, 64>(p, heads, st);
-    else if (a.d == 64 && a.g.BT == 32) e = run_bwd<64, 32>(p, heads, st);
+    if (a.d == 128 && a.g.BT == 64) e = run_bwd<128, 64>(p, st);
+    else if (a.d == 128 && a.g.BT == 32) e = run_bwd<128, 32>(p, st);
+    else if (a.d == 64 && a.g.BT == 64) e = run_bwd<64, 64>(p, st);
+    else if (a.d == 64 && a.g.BT == 32) e = run_bwd<64, 32>(p, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -62,7 +62,9 @@ struct FwdParams {
   float scale_log2;  // scale * log2(e)
   Rows O;            // raster output, strided
   float* lse;
-  unsigned long long clsmask[8];  // key-validity mask of each block-extent class (host-computed, C23)
+  unsigned long long clsmask[8];  // key-validity mask of each block-extent class (host-computed, C23): the
+                                  // image holds a block's n actual tokens in its first n rows, so bits [0, n)
+  int clsn16[8];                  // key columns computed per class: n rounded up to the MMA's N step of 16
 };
 
 constexpr int FWD_THREADS = 384;
@@ -73,6 +75,7 @@ constexpr int MAX_G = 16;
 template <int D, int BT>
 struct FwdSmem {
   static constexpr int KV_BYTES = BT * D * 2;  // one K or V tile
+  static constexpr int NCB = D / 64;            // 64-channel (128-byte) column blocks
   static constexpr int OFF_K = 0;               // stage s: K tile at OFF_K + 2 s KV_BYTES, V right after
   static constexpr int OFF_BITS = OFF_K + FWD_STAGES * 2 * KV_BYTES;
   static constexpr int BITS_BYTES = MAX_G * (MAX_N / 32) * 4;
@@ -117,8 +120,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
+  __shared__ int s_clsn16[8];
   __shared__ uint32_t s_uword[MAX_N / 32];  // union bitmap words and their exclusive popcount prefix
   __shared__ int s_upre[MAX_N / 32];
+#ifdef BSA_FWD_INTERLEAVE
+  // union entries by the TMEM lane quadrant (= SM sub-partition) of their lowest admitting slot: word masks,
+  // their per-quadrant exclusive prefix and the per-quadrant totals
+  __shared__ uint32_t s_qw[4][MAX_N / 32];
+  __shared__ int s_qpre[4][MAX_N / 32];
+  __shared__ int s_qcnt[4];
+#endif
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
   // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
   // per-column index arithmetic (which, unrolled, bloated the softmax loop past the instruction cache).
@@ -169,7 +180,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     s_koff[tid] = qb >= 0 ? p.kept_off[qb] : 0;
   }
   for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
-  if (tid < 8) s_clsmask[tid] = p.clsmask[tid];
+  if (tid < 8) {
+    s_clsmask[tid] = p.clsmask[tid];
+    s_clsn16[tid] = p.clsn16[tid];
+  }
 #ifdef BSA_TRACE
 #define FWD_CSTAMP(k)                                                                   \
   do {                                                                                  \
@@ -225,6 +239,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   // ascending union list in two parallel passes: warp 0 ORs the slots' bitmaps word by word (lane-parallel)
   // and prefix-sums the word popcounts; then every warp emits whole words, lane b writing bit b's entry
   // (entry = j | extent class << 12, N <= 4096; class bit 2/1/0 = ragged last block along t/h/w, C23)
+#ifndef BSA_FWD_INTERLEAVE
   if (warp == 0) {
     int carry = 0;
     for (int w0 = 0; w0 < NW; w0 += 32) {
@@ -258,6 +273,61 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       ulist[s_upre[w] + __popc(v & ((1u << lane) - 1u))] = static_cast<uint16_t>(jj | (cls << 12));
     }
   }
+#else
+  // Interleaved union order: consecutive steps (handled by the two softmax groups, which share the four
+  // sub-partitions) go to blocks in different TMEM lane quadrants, so one sub-partition's MUFU does not take
+  // two admitted softmax steps in a row. Key of an entry = (rank within its quadrant class, quadrant).
+  if (warp == 0) {
+    int carry[4] = {0, 0, 0, 0};
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t seen = 0u, mq[4] = {0u, 0u, 0u, 0u};
+      if (w < NW)
+        for (int gi = 0; gi < G; ++gi) {
+          const uint32_t b = bits[gi * NW + w];
+          mq[(gi * 4) / G] |= b & ~seen;
+          seen |= b;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = __popc(mq[q]);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int a = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += a;
+        }
+        if (w < NW) {
+          s_qw[q][w] = mq[q];
+          s_qpre[q][w] = carry[q] + incl - c;
+        }
+        carry[q] += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == 0) {
+      for (int q = 0; q < 4; ++q) s_qcnt[q] = carry[q];
+      s_U = carry[0] + carry[1] + carry[2] + carry[3];
+    }
+  }
+  __syncthreads();
+  for (int w = warp; w < NW; w += FWD_THREADS / 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t v = s_qw[q][w];
+      if ((v >> lane) & 1u) {
+        const int jj = w * 32 + lane;
+        const int bt = jj / (g.Nh * g.Nw), bhh = (jj / g.Nw) % g.Nh, bw = jj % g.Nw;
+        const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
+                        (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
+        const int r = s_qpre[q][w] + __popc(v & ((1u << lane) - 1u));
+        int pos = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) pos += min_i(s_qcnt[q2], r + (q2 < q ? 1 : 0));
+        ulist[pos] = static_cast<uint16_t>(jj | (cls << 12));
+      }
+    }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -283,16 +353,27 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     if (lane == 0) {
       for (int u = 0; u < U; ++u) {
         int s = u % FWD_STAGES;
+        const int ent = entry_at(u);
+        // only the first n16 rows (the block's tokens, padded to the MMA's N step) of each of the image's
+        // 2 NCB column tiles are read: one request for a whole block, one per column tile for a ragged one
+        const int n16 = s_clsn16[ent >> 12];
         mbar_wait(&bar_kv_empty[s], ((u / FWD_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&bar_kv_full[s], 2 * KV_BYTES);
+        mbar_expect_tx(&bar_kv_full[s], static_cast<uint32_t>(n16) * (4 * D));
         FWD_TRACE(0, u);
 #ifndef BSA_ABLATE_FWD_HOTSET
-        const int j = kv_at(u);
+        const int j = ent & 0xFFF;
 #else
         const int j = (u & 15);
 #endif
-        bulk_load(sK + s * 2 * KV_BYTES, p.kv_img + (static_cast<size_t>(bh) * g.N + j) * (2 * KV_BYTES),
-                  2 * KV_BYTES, &bar_kv_full[s]);
+        const uint8_t* src = p.kv_img + (static_cast<size_t>(bh) * g.N + j) * (2 * KV_BYTES);
+        if (n16 == BT) {
+          bulk_load(sK + s * 2 * KV_BYTES, src, 2 * KV_BYTES, &bar_kv_full[s]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 2 * SM::NCB; ++t)
+            bulk_load(sK + s * 2 * KV_BYTES + t * BT * 128, src + t * BT * 128, static_cast<uint32_t>(n16) * 128,
+                      &bar_kv_full[s]);
+        }
       }
     }
   } else if (warp == W_QK || warp == W_PV) {
@@ -303,7 +384,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     // issuer polling both queues needs a short suspend hint, which wakes ~0.3 us late on B200.) Each
     // warp walks its schedule whole (uniform registers); one elected lane issues.
     const bool leader = elect_one();
-    constexpr uint32_t idesc_qk = umma_idesc_bf16(128, BT, 0, 0);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, D, 0, 1);
     const uint32_t tO = tbase + SM::T_O, tS = tbase + SM::T_S, tQ = tbase + SM::T_Q, tP = tbase + SM::T_P;
     // base descriptors; an operand at byte offset o from the base is base + (o >> 4)
@@ -320,6 +400,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #endif
       for (int v = 0; v < U; ++v) {
         const int s = v % FWD_STAGES, sb = v & 1;
+        const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[entry_at(v) >> 12], 0, 0);  // N = n16 keys
         mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
         if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
         tc_fence_after();
@@ -340,6 +421,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     } else {
       for (int u = 0; u < U; ++u) {
         const int pb = u & 1, s = u % FWD_STAGES;
+        const int nkk = s_clsn16[entry_at(u) >> 12] / 16;  // K = n16 keys
         mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
         FWD_TRACE(2, u);
         tc_fence_after();
@@ -347,6 +429,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk) {
+            if (kk >= nkk) break;
 #ifndef BSA_ABLATE_FWD_MMA
             umma_ts(tO + pb * D, tP + pb * (BT / 2) + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv,
                     (u > 1 || kk > 0) ? 1u : 0u);
@@ -408,6 +491,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     for (int u = group; u < U; u += 2) {
       const int ph = (u >> 1) & 1;  // phase of this group's buffers
       const int ent = entry_at(u), j = ent & 0xFFF, cls = ent >> 12;
+      // The softmax always covers all BT columns (columns past the block's n tokens are masked, so stale TMEM
+      // values of a shorter S never leak): skipping the unused 16-column chunks of ragged blocks broke the
+      // instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
+      constexpr int n16 = BT;
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
       mbar_wait(&bar_s_full[group], ph);
       if (row == 0) FWD_TRACE(4 + 8 * group, u);
@@ -421,11 +508,103 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       tc_fence_after();
       float sv[BT];
 #pragma unroll
-      for (int c = 0; c < BT; c += 16) tmem_ld16(tS + c, sv + c);
+      for (int c = 0; c < BT; c += 16) {
+        if (c < n16) {
+          tmem_ld16(tS + c, sv + c);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sv[c + e] = -INFINITY;
+        }
+      }
       tmem_wait_ld();
       if (row == 0) FWD_TRACE(6 + 8 * group, u);
       tc_fence_before();
       mbar_arrive(&bar_s_free[group]);
+#ifdef BSA_FWD_SPEC
+      // Speculative exponentials: P = 2^(s sl2 - m_run) with the running (possibly stale) max, streamed to TMEM
+      // 32 keys at a time while the step's max is formed alongside; only if that max exceeds m_run by more
+      // than 2^8 (rare after the first step) are O and l rescaled and P recomputed from the scores still in
+      // registers. The row's first admitted step takes its exact max first (m_run = -inf).
+      const bool wadmit = __any_sync(0xffffffffu, admit);
+      if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
+      if (row == 0) FWD_TRACE(7 + 8 * group, u);
+      if (wadmit) {
+        if (admit) {
+          if (cls != 0) {
+            const uint64_t km = s_clsmask[cls];
+            const uint32_t k0 = static_cast<uint32_t>(km), k1 = static_cast<uint32_t>(km >> 32);
+#pragma unroll
+            for (int c = 0; c < BT; ++c)
+              if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
+          }
+          if (m_run == -INFINITY) {
+            float mp0[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < BT; ++c) mp0[c & 3] = fmaxf(mp0[c & 3], sv[c]);
+            m_run = fmaxf(fmaxf(mp0[0], mp0[1]), fmaxf(mp0[2], mp0[3])) * sl2;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BT; ++c) sv[c] = -INFINITY;
+        }
+        const float2 sl2v = make_float2(sl2, sl2);
+        float mref = admit ? m_run : 0.f;
+        float2 sp2[4];
+        float mp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int pass = 0; pass < 2; ++pass) {
+          const float2 nm = make_float2(-mref, -mref);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sp2[e] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int c0 = 0; c0 < BT; c0 += 32) {
+            float w[16];
+#pragma unroll
+            for (int c = c0; c < c0 + 32; c += 2) {
+              if (pass == 0) {
+                mp[c & 3] = fmaxf(mp[c & 3], sv[c]);
+                mp[(c + 1) & 3] = fmaxf(mp[(c + 1) & 3], sv[c + 1]);
+              }
+              const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+              const float e0 = ex2(x.x);
+              const float e1 = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
+              sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(e0, e1));
+              w[(c - c0) >> 1] = __uint_as_float(pack_bf16(e0, e1));
+            }
+            tmem_st16(tP + (c0 >> 1), w);
+          }
+          if (pass == 1) break;
+          const float mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])) * sl2;
+          const bool grow = admit && mx > m_run + 8.f;
+          if (!__any_sync(0xffffffffu, grow)) break;
+          // rare: the max grew by more than 2^8 -- rescale O and l, recompute P with the new max
+          const float alpha = grow ? ex2(m_run - mx) : 1.f;
+          if (grow) {
+            l_run *= alpha;
+            m_run = mx;
+          }
+          mref = admit ? m_run : 0.f;
+          tmem_wait_st();
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 16) {
+            float ov[16];
+            tmem_ld16(tO + c, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ov[e] *= alpha;
+            tmem_st16(tO + c, ov);
+          }
+        }
+        if (admit)
+          l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
+      } else {
+        float w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w[e] = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < BT / 2; c0 += 16) tmem_st16(tP + c0, w);
+      }
+#else
       float alpha = 1.f;
       bool need_rescale = false;
 #ifdef BSA_ABLATE_FWD_EXP
@@ -466,11 +645,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
         float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_run, -m_run);
 #pragma unroll
-        for (int c = 0; c < BT; c += 2) {  // one column in four on the FMA pipe, the rest on the MUFU
-          const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
-          sv[c] = ex2(x.x);
-          sv[c + 1] = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
-          sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(sv[c], sv[c + 1]));
+        for (int c0 = 0; c0 < BT; c0 += 16) {
+          if (c0 < n16) {
+#pragma unroll
+            for (int c = c0; c < c0 + 16; c += 2) {  // one column in four on the FMA pipe, the rest on the MUFU
+              const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+              sv[c] = ex2(x.x);
+#ifndef BSA_POLY_MASK
+              sv[c + 1] = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
+#else
+              sv[c] = ((BSA_POLY_MASK >> (c & 7)) & 1) ? ex2_poly(x.x) : ex2(x.x);
+              sv[c + 1] = ((BSA_POLY_MASK >> ((c + 1) & 7)) & 1) ? ex2_poly(x.y) : ex2(x.y);
+#endif
+              sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(sv[c], sv[c + 1]));
+            }
+          } else {
+#pragma unroll
+            for (int c = c0; c < c0 + 16; ++c) sv[c] = 0.f;
+          }
         }
         l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
       } else {
@@ -496,11 +688,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       // P row -> TMEM (bf16 pairs, the A operand of PV)
 #pragma unroll
       for (int c0 = 0; c0 < BT / 2; c0 += 16) {
-        float w[16];
+        if (2 * c0 < n16) {  // the PV MMA reads the first n16 keys only
+          float w[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(pack_bf16(sv[2 * (c0 + e)], sv[2 * (c0 + e) + 1]));
-        tmem_st16(tP + c0, w);
+          for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(pack_bf16(sv[2 * (c0 + e)], sv[2 * (c0 + e) + 1]));
+          tmem_st16(tP + c0, w);
+        }
       }
+#endif
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar_p_full[group]);
@@ -655,12 +850,13 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
     const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
     const int eh = (cls & 2) ? g.H - (g.Nh - 1) * g.ch : g.ch;
     const int ew = (cls & 1) ? g.W - (g.Nw - 1) * g.cw : g.cw;
-    unsigned long long m = 0;
-    for (int c = 0; c < g.BT; ++c) {
-      const int lw = c % g.cw, lh = (c / g.cw) % g.ch, lt = c / (g.cw * g.ch);
-      if (lt < et && lh < eh && lw < ew) m |= 1ull << c;
-    }
-    p.clsmask[cls] = m;
+    const int n = et * eh * ew;  // the image holds the block's n tokens in rows [0, n)
+    p.clsmask[cls] = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+#ifndef BSA_FWD_FULLN
+    p.clsn16[cls] = (n + 15) / 16 * 16;
+#else
+    p.clsn16[cls] = g.BT;
+#endif
   }
   int ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
   if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
@@ -670,10 +866,12 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-// K|V block images: for every (bh, KV block j) the exact shared-memory image the forward MMAs read —
-// [K: d-half 0 as BT rows x 128 B, d-half 1 ...][V: same], 128-byte swizzled, rows in the nominal box
-// order (lt, lh, lw), out-of-grid rows of ragged blocks zero — so one KV step is ONE contiguous bulk
-// copy (small TMA boxes cost ~500 cycles each; one 32 KB request per step keeps ~128 KB in flight).
+// K|V block images: for every (bh, KV block j) the exact shared-memory image the forward MMAs read, ONE
+// contiguous bulk copy per KV step (small TMA boxes cost ~500 cycles each). Rows = keys: the block's n actual
+// tokens in ascending raster order first (compacted: a ragged edge block's rows are a prefix, C23), zero rows
+// up to n16 = n rounded up to 16 (the MMA's N step), nothing beyond (never read). Layout [K: d-half 0 as BT
+// rows x 128 B, d-half 1 ...][V: same], 128-byte swizzled (8-row groups 1 KB apart: an image of 8-row groups
+// 4 KB apart, which makes the first n16 keys one prefix, slowed the MMAs' operand reads, 0.87 -> 1.07 ms).
 template <int D, int BT>
 __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Rows V, uint8_t* __restrict__ img) {
   constexpr int CPR = D / 8;        // 16-byte chunks per row
@@ -681,6 +879,7 @@ __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Row
   constexpr int PER = 2 * CHUNKS / 256;  // chunks per thread (K and V)
   const int j = blockIdx.x, bh = blockIdx.y;
   const Box x = block_box(g, j);
+  const int n = x.e[0] * x.e[1] * x.e[2], n16 = (n + 15) & ~15;
   uint8_t* dst = img + (static_cast<size_t>(bh) * g.N + j) * (2 * BT * D * 2);
   const bf16* kh = K.head(bh);
   const bf16* vh = V.head(bh);
@@ -691,9 +890,9 @@ __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Row
     const int v = threadIdx.x + 256 * k;
     const int t = v / CHUNKS, w = v % CHUNKS;
     const int r = w / CPR, c = w % CPR;
-    const int lw = r % g.cw, lh = (r / g.cw) % g.ch, lt = r / (g.cw * g.ch);
     val[k] = make_uint4(0, 0, 0, 0);
-    if (lt < x.e[0] && lh < x.e[1] && lw < x.e[2]) {
+    if (r < n) {
+      const int lw = r % x.e[2], lh = (r / x.e[2]) % x.e[1], lt = r / (x.e[2] * x.e[1]);
       const long long tok = (static_cast<long long>(x.o[0] + lt) * g.H + (x.o[1] + lh)) * g.W + (x.o[2] + lw);
       val[k] = __ldg(reinterpret_cast<const uint4*>((t ? vh + tok * V.sl : kh + tok * K.sl) + c * 8));
     }
@@ -703,7 +902,8 @@ __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Row
     const int v = threadIdx.x + 256 * k;
     const int t = v / CHUNKS, w = v % CHUNKS;
     const int r = w / CPR, c = w % CPR;
-    *reinterpret_cast<uint4*>(dst + t * (BT * D * 2) + (c >> 3) * (BT * 128) + sw128_off(r, c & 7)) = val[k];
+    if (r < n16)
+      *reinterpret_cast<uint4*>(dst + t * (BT * D * 2) + (c >> 3) * (BT * 128) + sw128_off(r, c & 7)) = val[k];
   }
 }
 

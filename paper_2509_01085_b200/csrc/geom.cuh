@@ -18,6 +18,7 @@ struct Geo {
 
 __host__ __device__ inline int cdiv_i(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline int min_i(int a, int b) { return a < b ? a : b; }
+__host__ __device__ inline int max_i(int a, int b) { return a > b ? a : b; }
 
 inline Geo make_geo(int T, int H, int W, int ct, int ch, int cw, int ut, int uh, int uw) {
   Geo g;

@@ -96,6 +96,7 @@ struct BwdArgs {
   uint8_t* qdo_img;  // [BH, N] query-block images of Q^s|dO^s, SR*d*4 bytes each (k_bwd_prep)
   float* lsed;       // [BH, N, 2, SR]: per query block LSE*log2(e) of its SR rows, then D of its SR rows
   float* dQacc;  // [BH, Lq, d]
+  int* work_ctr;  // [B] item counters of the persistent main kernel (one per launch)
 };
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st);
