@@ -41,7 +41,7 @@ CONFIGS = {
     "long_147k": dict(grid=(41, 45, 80), block=(4, 4, 4), B=1, Hh=40, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
 }
 KERNEL_NAMES = ["partition", "select_queries", "pool", "scores", "admit", "k2q", "gather", "attn_fwd", "fill",
-                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image", "sp_relayout", "fwd_group"]
+                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image", "sp_relayout", "fwd_group", "bwd_pairs", "bwd_dq"]
 SELECTION_IDS = range(0, 7)
 
 

@@ -170,15 +170,21 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
  *   dO^s[q] = dO[q] + sum of dO over the pruned tokens whose donor is q; D = rowsum(dO^s * O^s);
  *   dV, dK accumulate over admitting query blocks; dQ[kept] = scale * dS K, dQ[pruned] = 0;
  *   tokens of KV blocks no query block admitted get dK = dV = 0.
- *   O and lse are the outputs of bsa_attn_fwd; k2q_* from bsa_select_kv_blocks.
- *   dQ, dK, dV [B,Hh,L,d] out bf16 (strided; Q.ptr may be NULL when q_packed is given). dQ accumulates in an fp32 workspace through L2 bulk tensor reduce-adds
- *   (cp.reduce.async.bulk.tensor), one per (query row block, admitted KV block): the summation order is
- *   not deterministic, so dQ may differ run to run in the last fp32 bits before the bf16 rounding. */
+ *   O and lse are the outputs of bsa_attn_fwd; q2k_* and k2q_* from bsa_select_kv_blocks (both directions of
+ *   the same selection: dK/dV walk k2q, dQ walks q2k).
+ *   dQ, dK, dV [B,Hh,L,d] out bf16 (strided; Q.ptr may be NULL when q_packed is given).
+ *   dQ is formed one of two ways, chosen on the device from the selection's number of admitted (query block,
+ *   KV block) pairs against the workspace's capacity (a pair density of 1/8, at most 24 GiB):
+ *     dS path (pairs fit): the KV-stationary kernel stores every pair's bf16 dS tile and a query-stationary
+ *       kernel forms dQ^T = sum_j K_j^T dS_ij^T in TMEM (fp32, ascending j: deterministic);
+ *     reduce path (denser selections): fp32 dQ partials, one per (query row block, admitted KV block), are
+ *       reduced in L2 (cp.reduce.async.bulk.tensor) into an fp32 workspace: the summation order is not
+ *       deterministic, so dQ may differ run to run in the last fp32 bits before the bf16 rounding. */
 int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
                  bsa_tensor V, bsa_tensor O, bsa_tensor dO, const void* q_packed, const int32_t* kept_off,
-                 const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
-                 const float* lse, float scale, bsa_tensor dQ, bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes,
-                 void* stream);
+                 const int32_t* kept_tok, const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx,
+                 const int32_t* k2q_num, const int32_t* k2q_idx, const float* lse, float scale, bsa_tensor dQ,
+                 bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- Ulysses sequence parallelism
  * (SURVEY.md §8(e) mode 2). A sequence-parallel model gives each of P ranks a contiguous
@@ -209,8 +215,12 @@ int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int3
 enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
   BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT,
-  BSA_K_GROUP, BSA_K_COUNT
+  BSA_K_GROUP, BSA_K_BWD_PAIRS, BSA_K_BWD_DQ, BSA_K_COUNT
 };
+/* Backward dQ path (process-wide, default BSA_BWD_AUTO = the device-side switch described at bsa_attn_bwd;
+ * BSA_BWD_REDUCE forces the reduce path, for tests and A/B timing). Unknown mode: BSA_ERR_CONFIG. */
+enum bsa_bwd_path { BSA_BWD_AUTO = 0, BSA_BWD_REDUCE = 1 };
+int bsa_set_bwd_path(int mode);
 /* Total kernels launched through libbsa by this process (always counted; cheap). */
 int64_t bsa_launch_count(void);
 /* When enabled (process-wide: autograd runs the backward on its own thread), every libbsa kernel launch is

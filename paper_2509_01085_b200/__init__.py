@@ -101,8 +101,8 @@ def lib() -> ctypes.CDLL:
         L.bsa_select_queries.argtypes = [gp, _D, _I, _I, _I, _T, _P, _P, _P, _P, _P, _P]
         L.bsa_select_kv_blocks.argtypes = [gp, _I, _I, _I, _T, _P, _T, _I, _D, _P, _P, _P, _P, _P, _P, _S, _P]
         L.bsa_attn_fwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _P, _P, _P, _P, _P, _P, _F, _T, _P, _P, _S, _P]
-        L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _T, _T, _P, _P, _P, _P, _P, _P, _P, _F, _T, _T,
-                                   _T, _P, _S, _P]
+        L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _T, _T, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F,
+                                   _T, _T, _T, _P, _S, _P]
         L.bsa_sp_relayout.argtypes = [_I, _I, _I, _I, _I, _I, _P, _P, _P]
         L.bsa_select_kv_blocks_ex.argtypes = [gp, _I, _I, _I, _T, _P, _T, _I, _D, _I, _P, _P, _P, _P, _P, _P, _S, _P]
         L.bsa_resolve_k.argtypes = [_D, _I, _P]
@@ -111,10 +111,11 @@ def lib() -> ctypes.CDLL:
         L.bsa_launch_count.argtypes = []
         L.bsa_timing_enable.argtypes = [_I]
         L.bsa_timing_read.argtypes = [_P, _P, _I]
+        L.bsa_set_bwd_path.argtypes = [_I]
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
-                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile"):
+                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -263,8 +264,8 @@ def bsa_attn_fwd(g: Geometry, r: float, Q, K, V, kept_off, kept_tok, donor, q2k_
     return O, lse
 
 
-def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, donor, k2q_num, k2q_idx, lse,
-                 scale=None, q_packed=None, ws=None, out=None):
+def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, donor, q2k_num, q2k_idx, k2q_num,
+                 k2q_idx, lse, scale=None, q_packed=None, ws=None, out=None):
     """a8: returns dQ, dK, dV [B,Hh,L,d] bf16 (into `out` = (dQ, dK, dV) if given; strided views allowed)."""
     B, Hh, L, d = K.shape
     N, Lq, _ = bsa_sizes(g, r)
@@ -275,6 +276,8 @@ def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, dono
     _need_i32("kept_off", kept_off, (N + 1,))
     _need_i32("kept_tok", kept_tok, (B, Hh, Lq))
     _need_i32("donor", donor, (B, Hh, L))
+    _need_i32("q2k_num", q2k_num, (B, Hh, N))
+    _need_i32("q2k_idx", q2k_idx, (B, Hh, N, N))
     _need_i32("k2q_num", k2q_num, (B, Hh, N))
     _need_i32("k2q_idx", k2q_idx, (B, Hh, N, N))
     if tuple(lse.shape) != (B, Hh, Lq) or lse.dtype != torch.float32 or not lse.is_contiguous():
@@ -287,9 +290,18 @@ def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, dono
         ws = _ws(nb, dev)
     T = tensor_desc
     _check(lib().bsa_attn_bwd(ctypes.byref(g.c()), r, B, Hh, d, T(Q), T(K), T(V), T(O), T(dO), _ptr(q_packed),
-                              _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(k2q_num), _ptr(k2q_idx), _ptr(lse),
-                              float(scale), T(dQ), T(dK), T(dV), _ptr(ws), nb, _stream(dev)), "bsa_attn_bwd")
+                              _ptr(kept_off), _ptr(kept_tok), _ptr(donor), _ptr(q2k_num), _ptr(q2k_idx),
+                              _ptr(k2q_num), _ptr(k2q_idx), _ptr(lse), float(scale), T(dQ), T(dK), T(dV), _ptr(ws), nb,
+                              _stream(dev)), "bsa_attn_bwd")
     return dQ, dK, dV
+
+
+BWD_AUTO, BWD_REDUCE = 0, 1
+
+
+def set_bwd_path(mode: int):
+    """Backward dQ path, process-wide (include/bsa.h bsa_set_bwd_path): BWD_AUTO or BWD_REDUCE."""
+    _check(lib().bsa_set_bwd_path(int(mode)), "bsa_set_bwd_path")
 
 
 SP_SEQ_TO_SEND, SP_RECV_TO_HEADS, SP_HEADS_TO_SEND, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND_T, SP_RECV_T_TO_SEQ = 0, 1, 2, 3, 4, 5

@@ -38,6 +38,7 @@ struct TimedRec {
 };
 // Process-wide (autograd runs the backward on its own worker thread, which must be counted and timed too).
 std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_bwd_path{BSA_BWD_AUTO};  // bsa_set_bwd_path
 std::atomic<bool> g_timing{false};
 std::mutex g_recs_mu;
 std::vector<TimedRec> g_recs;
@@ -177,8 +178,18 @@ FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
 
 // Backward workspace: gathered Q^s (only when q_packed is NULL), Q^s|dO^s query-block images
 // (N * SR padded rows per head), D = rowsum(dO^s O^s), fp32 dQ accumulator.
+// dS path capacity (admitted (query block, KV block) pairs whose bf16 dS tiles the workspace holds): a pair
+// density of 1/8 (the paper's settings admit ~4-8% of the pairs), at most 24 GiB of tiles. A
+// selection with more pairs takes the reduce path (fp32 dQ partials reduced in L2); the switch is on the device.
+long long ds_capacity(const bsa::Geo& g, size_t BH, int SR) {
+  const long long per_row = std::max<long long>(8, (g.N + 7) / 8);
+  const long long dens = static_cast<long long>(BH) * g.N * per_row;
+  const long long bytes_cap = (24LL << 30) / (static_cast<long long>(SR) * 128);
+  return std::min(dens, bytes_cap);
+}
 struct BwdWs {
-  size_t qs, img, dv, dq, ctr, total;
+  size_t qs, img, dv, dq, ctr, qoff, ptot, slot, ds, total;
+  long long cap;
 };
 BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   BwdWs w;
@@ -187,7 +198,12 @@ BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   w.dv = w.img + align256(BH * g.N * static_cast<size_t>(SR) * d * 4);
   w.dq = w.dv + align256(BH * g.N * static_cast<size_t>(SR) * 8);
   w.ctr = w.dq + align256(BH * Lq * d * 4);
-  w.total = w.ctr + align256(BH * 4);  // work counters of the main kernel (one per launch, <= B <= BH)
+  w.qoff = w.ctr + align256(BH * 4);  // work counters of the main kernel (one per launch, <= B <= BH)
+  w.ptot = w.qoff + align256(BH * g.N * 4);
+  w.slot = w.ptot + align256((BH + 1) * 4);  // per-head pair counts, then the total
+  w.ds = w.slot + align256(BH * g.N * static_cast<size_t>(g.N) * 4);
+  w.cap = ds_capacity(g, BH, SR);
+  w.total = w.ds + align256(static_cast<size_t>(w.cap) * SR * 128);
   return w;
 }
 
@@ -459,9 +475,9 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
 
 int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
                  bsa_tensor V, bsa_tensor O, bsa_tensor dO, const void* q_packed, const int32_t* kept_off,
-                 const int32_t* kept_tok, const int32_t* donor, const int32_t* k2q_num, const int32_t* k2q_idx,
-                 const float* lse, float scale, bsa_tensor dQ, bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes,
-                 void* stream) {
+                 const int32_t* kept_tok, const int32_t* donor, const int32_t* q2k_num, const int32_t* q2k_idx,
+                 const int32_t* k2q_num, const int32_t* k2q_idx, const float* lse, float scale, bsa_tensor dQ,
+                 bsa_tensor dK, bsa_tensor dV, void* ws, size_t ws_bytes, void* stream) {
   bsa::Geo G;
   CHECK(check_geom(g, &G));
   CHECK(check_r(r));
@@ -476,7 +492,7 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   CHECK(check_tensor(dQ, "dQ", Hh, d, true, &dQv));
   CHECK(check_tensor(dK, "dK", Hh, d, true, &dKv));
   CHECK(check_tensor(dV, "dV", Hh, d, true, &dVv));
-  if (!kept_off || !kept_tok || !donor || !k2q_num || !k2q_idx || !lse)
+  if (!kept_off || !kept_tok || !donor || !q2k_num || !q2k_idx || !k2q_num || !k2q_idx || !lse)
     return fail(BSA_ERR_SELECTION_MISMATCH, "missing required pointer");
   if (q_packed && !aligned16(q_packed)) return fail(BSA_ERR_INVALID_SHAPE, "misaligned q_packed");
   int Lq = 0, SR = 0;
@@ -524,13 +540,31 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.lsed = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
   a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
+  a.q2k_num = q2k_num;
+  a.q2k_idx = q2k_idx;
+  a.q2k_off = reinterpret_cast<int*>(base + w.qoff);
+  a.pair_tot = reinterpret_cast<int*>(base + w.ptot);
+  a.pair_total = a.pair_tot + BH;
+  a.k2q_slot = reinterpret_cast<int*>(base + w.slot);
+  a.ds_buf = base + w.ds;
+  a.ds_cap = g_bwd_path.load() == BSA_BWD_REDUCE ? -1 : w.cap;  // (pair_total >= 0 > -1: reduce path)
+  if (e == cudaSuccess) e = timed(BSA_K_BWD_PAIRS, 2, st, [&] { return bsa::launch_bwd_pairs(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
   const bool one_launch = (B == 1) || (Kv.sb == Hh * Kv.sh && Vv.sb == Hh * Vv.sh && dKv.sb == Hh * dKv.sh &&
                                        dVv.sb == Hh * dVv.sh);
   if (e == cudaSuccess)
-    e = timed(BSA_K_ATTN_BWD, one_launch ? 1 : B, st, [&] { return bsa::launch_bwd_main(a, st); });
+    e = timed(BSA_K_ATTN_BWD, 2 * (one_launch ? 1 : B), st, [&] { return bsa::launch_bwd_main(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 1, st, [&] { return bsa::launch_bwd_finalize(a, st); });
+  const bool k_uniform = (B == 1) || Kv.sb == Hh * Kv.sh;
+  if (e == cudaSuccess)
+    e = timed(BSA_K_BWD_DQ, k_uniform ? 1 : B, st, [&] { return bsa::launch_bwd_dq(a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_bwd");
+  return BSA_OK;
+}
+
+int bsa_set_bwd_path(int mode) {
+  if (mode != BSA_BWD_AUTO && mode != BSA_BWD_REDUCE) return fail(BSA_ERR_CONFIG, "unknown backward path %d", mode);
+  g_bwd_path.store(mode);
   return BSA_OK;
 }
 

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
                                                   const bf16* __restrict__ Qs, const Rows dO, const Rows O,
                                                   const float* __restrict__ lse,
                                                   uint8_t* __restrict__ qdo_img, float* __restrict__ lsed,
-                                                  float* __restrict__ dQacc) {
+                                                  float* __restrict__ dQacc, const int* __restrict__ pair_total,
+                                                  long long ds_cap, const Rows dQ) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
   constexpr int NCB = D / 64;
   constexpr int MAXT = 128;    // tokens per block (checked by the API)
@@ -103,9 +104,13 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
     s_don[i] = donor[head + t];
   }
   __syncthreads();
+  const bool ds = *pair_total <= ds_cap;  // dS path: no fp32 dQ accumulator to clear
+  bf16* dqh = dQ.head(bh);
   for (int v = threadIdx.x; v < n * (D / 8); v += blockDim.x) {
     const int i = v / (D / 8), c = (v % (D / 8)) * 8;
     *reinterpret_cast<uint4*>(s_do + i * D + c) = *reinterpret_cast<const uint4*>(doh + s_tok[i] * dO.sl + c);
+    if (s_don[i] != s_tok[i])  // dQ of a pruned token is 0 (reading C10)
+      *reinterpret_cast<uint4*>(dqh + s_tok[i] * dQ.sl + c) = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
   const int ch0 = lane * PER;
@@ -171,9 +176,11 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
       ld[0] = lse[prow] * 1.4426950408889634f;
       ld[SR] = dsum;
     }
-    float* dq = dQacc + prow * D + ch0;
-    if (PER == 4) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
-    else *reinterpret_cast<float2*>(dq) = make_float2(0.f, 0.f);
+    if (!ds) {
+      float* dq = dQacc + prow * D + ch0;
+      if (PER == 4) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+      else *reinterpret_cast<float2*>(dq) = make_float2(0.f, 0.f);
+    }
   }
 }
 
@@ -240,6 +247,14 @@ struct BwdParams {
   int* work_ctr;       // next unclaimed item (zeroed before the launch)
   float scale_log2;
   float scale;
+  // dS path (DESIGN.md §5 "Backward"): when the selection's admitted (query block, KV block) pairs fit the
+  // workspace (*pair_total <= ds_cap), the main kernel stores each pair's bf16 dS tile (SR rows x 128 B, the
+  // swizzled shared-memory image) at ds_buf + k2q_slot[..] * SR * 128 and k_bwd_dq forms dQ from them; else the
+  // main kernel reduces fp32 dQ partials into dQacc (reduce path) and k_bwd_finalize converts them.
+  const int* pair_total;
+  long long ds_cap;
+  const int* k2q_slot;  // [BH][N][N]: pair slot of k2q entry (j, p) (k_pair_slot)
+  uint8_t* ds_buf;
 };
 
 // dQ staging: 2 slots of 32 rows per drain warp (one 4 KB reduce box per 32-column slice when SR >= 32): half the
@@ -253,7 +268,7 @@ struct BwdParams {
 constexpr int BWD_THREADS = 384;
 constexpr int BWD_MAX_G = 16;
 
-template <int D, int BT>
+template <int D, int BT, bool DS = false>
 struct BwdSmem {
   static constexpr int NCB = D / 64;
   static constexpr int KV_BYTES = BT * D * 2;
@@ -272,7 +287,9 @@ struct BwdSmem {
   static constexpr int DQ_SLOT_BYTES = DQ_SROWS * 128;
   static constexpr int OFF_DQS = OFF_ZERO + (D == 64 ? 16384 : 0);
   // the dynamic region is declared 1024-byte aligned (checked at run time), so no alignment slack is added
-  static constexpr int TOTAL = OFF_DQS + 4 * DQ_SLOTS * DQ_SLOT_BYTES;
+  // dS path: no dQ staging; the chunk ring's pair slots sit there instead
+  static constexpr int OFF_SLOT = OFF_DQS;
+  static constexpr int TOTAL = OFF_DQS + (DS ? 4 * 16 * 4 : 4 * DQ_SLOTS * DQ_SLOT_BYTES);
   static constexpr int TMEM_COLS = (4 * BT + 2 * D) <= 256 ? 256 : 512;
 };
 
@@ -284,11 +301,15 @@ struct BwdSmem {
 // and dynamic claiming bounds the tail by one block (fixed runs of 2 / 4 / 8 / 16 consecutive blocks per CTA
 // measured 1.71 / 1.72 / 1.82 / 1.97 ms at 32k: tail imbalance of static assignment).
 constexpr int ITEM_RING = 8;
-constexpr int ITEM_READERS = 10;  // S/dP issuer, gradient issuer, 4 softmax warps, 4 drain warps
+// readers of the item ring: S/dP issuer, gradient issuer, 4 softmax warps (+ 4 dQ drain warps on the reduce path)
+template <bool DS>
+__host__ __device__ constexpr int item_readers() { return DS ? 6 : 10; }
 
-template <int D, int BT>
+template <int D, int BT, bool DS>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
-  using SM = BwdSmem<D, BT>;
+  using SM = BwdSmem<D, BT, DS>;
+  // one of the two instantiations runs: the dS path when the pairs fit, else the reduce path (uniform exit)
+  if (DS != (*p.pair_total <= p.ds_cap)) return;
   constexpr int NCB = SM::NCB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
@@ -362,7 +383,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     mbar_init(&bar_acc_free, 128);
     for (int s = 0; s < ITEM_RING; ++s) {
       mbar_init(&bar_item_full[s], 1);
-      mbar_init(&bar_item_empty[s], ITEM_READERS);
+      mbar_init(&bar_item_empty[s], item_readers<DS>());
     }
     fence_mbar_init();
   }
@@ -410,9 +431,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         const int s = c & 1;
         const int cc = (cl + crot) % nchunks;
         const int nb = min_i(G, nq - cc * G);
-        int row0 = -1, nk = 0, qbl = 0;
+        int row0 = -1, nk = 0, qbl = 0, slot = -1;
         if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
           qbl = qlist[cc * G + lane];
+          if (DS) slot = p.k2q_slot[(static_cast<size_t>(bh) * g.N + j) * g.N + cc * G + lane];
           int ko = p.kept_off[qbl];
           nk = p.kept_off[qbl + 1] - ko;
           row0 = bh * p.Lq + ko;
@@ -424,6 +446,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (lane < G) {
           s_row0[ring][lane] = row0;
           s_nk[ring][lane] = nk;
+          if (DS) reinterpret_cast<int*>(sm + SM::OFF_SLOT)[ring * 16 + lane] = slot;
         }
         __syncwarp();
         const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
@@ -524,7 +547,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           if (lane == 0) PROG(2, c * 4 + 0);
           bwait(&bar_ps_full, c & 1);
           if (lane == 0) PROG(2, c * 4 + 1);
-          if (c >= 2) bwait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
+          if (!DS && c >= 2) bwait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
           if (lane == 0) PROG(2, c * 4 + 2);
           tc_fence_after();
           BWD_TRACE(2, c);
@@ -547,13 +570,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 #endif
             }
             umma_commit(&bar_c_empty[s]);  // the stage is free once dV/dK have read it
+            if (!DS) {
 #pragma unroll
-            for (int kk = 0; kk < BT / 16; ++kk) {
+              for (int kk = 0; kk < BT / 16; ++kk) {
 #ifndef BSA_ABLATE_BWD_MMA
-              umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
+                umma_ss(tdQ + qbuf * D, dSa + ((kk * 32) >> 4), dKt + ((kk * 2048) >> 4), idesc_q, kk > 0);
 #endif
+              }
+              umma_commit(&bar_dq_full[qbuf]);
             }
-            umma_commit(&bar_dq_full[qbuf]);
             umma_commit(&bar_ps_free);
           }
           __syncwarp();
@@ -616,6 +641,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (row == 0) BWD_TRACE(9, c);
         if (row == 0) PROG(3, c * 8 + 3);
         if (c >= 1) bwait(&bar_ps_free, (c - 1) & 1);  // MMAs of chunk c-1 done with sP/sdS
+        if (DS) {  // this warp's dS store of chunk c-1 has read its sdS rows
+          if (lane == 0) bulk_wait_group_read<0>();
+          __syncwarp();
+        }
         if (row == 0) PROG(3, c * 8 + 4);
         if (store_pending) {  // the previous block's dK/dV store must have read sP/sdS
           if (row == 0) bulk_wait_group_read<0>();
@@ -635,6 +664,23 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bar_ps_full);
+        if (DS) {
+          // this warp's 32 dS rows -> the pair slots of the query blocks they belong to (bulk copies of the
+          // swizzled rows; k_bwd_dq loads them back as MMA operands). Rows past a block's kept count are 0.
+          __syncwarp();
+          if (lane == 0) {
+            const int* slots = reinterpret_cast<const int*>(sm + SM::OFF_SLOT) + (c & 3) * 16;
+            const int w0 = q4 * 32;
+            for (int gi = w0 / SR; gi < G && gi * SR < w0 + 32; ++gi) {
+              const int sl = slots[gi];
+              if (sl < 0 || s_nk[c & 3][gi] == 0) continue;
+              const int r0 = max_i(gi * SR, w0), r1 = min_i((gi + 1) * SR, w0 + 32);
+              bulk_store(p.ds_buf + (static_cast<size_t>(sl) * SR + (r0 - gi * SR)) * 128, sdS + r0 * 128,
+                         static_cast<uint32_t>(r1 - r0) * 128);
+            }
+            bulk_commit_group();
+          }
+        }
         if (row == 0) BWD_TRACE(5, c);
       }
       if (row == 0) CTA_STAMP(5);
@@ -651,8 +697,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         tc_fence_after();
       }
       if (row == 0) PROG(11, 2000 + nacc);
-      if (store_pending) {  // (a block with no chunks right after another block's store)
-        if (row == 0) bulk_wait_group_read<0>();
+      if (store_pending || DS) {  // (a block with no chunks right after another block's store; dS stores)
+        if (DS ? lane == 0 : row == 0) bulk_wait_group_read<0>();
         named_bar_sync(1, 128);
         store_pending = false;
       }
@@ -697,7 +743,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       if (row == 0) CTA_STAMP(6);
     }
     if (row == 0) bulk_wait_group<0>();  // the last stores are complete before the CTA exits
-  } else if (warp < 8) {
+  } else if (warp < 8 && !DS) {
     // ============================ dQ drain: TMEM dQ partial -> smem slices -> TMA bulk reduce-add
     // Each warp owns TMEM lane quadrant q4 (chunk rows 32 q4 .. +32), split into 32/R sub-boxes of R =
     // min(SR, 16) rows that each belong to one query block and map to R consecutive packed dQacc rows.
@@ -814,6 +860,245 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 #endif
 }
 
+
+// ------------------------------------------------------------------------------------ dS path: pair slots
+// The dS tiles of query block i are stored contiguously in q2k order: pair (i, t-th admitted KV block) at slot
+// base(bh) + q2k_off[bh][i] + t. k_pair_off: per head the exclusive scan of q2k_num and its total.
+__global__ void __launch_bounds__(1024) k_pair_off(int N, const int* __restrict__ q2k_num, int* __restrict__ q2k_off,
+                                                   int* __restrict__ tot) {
+  __shared__ int s_w[32];
+  __shared__ int s_chunk;
+  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int* num = q2k_num + static_cast<size_t>(bh) * N;
+  int carry = 0;
+  for (int b0 = 0; b0 < N; b0 += 1024) {
+    const int i = b0 + tid;
+    const int v = i < N ? num[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int w = s_w[lane];
+      int wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += a;
+      }
+      s_w[lane] = wi - w;  // exclusive prefix of the warp totals
+      if (lane == 31) s_chunk = wi;
+    }
+    __syncthreads();
+    if (i < N) q2k_off[static_cast<size_t>(bh) * N + i] = carry + s_w[warp] + incl - v;
+    carry += s_chunk;
+    __syncthreads();
+  }
+  if (tid == 0) tot[bh] = carry;
+}
+
+// k_pair_slot: slot of every k2q entry (KV block j, p-th admitting query block i) = base(bh) + q2k_off[i] + rank
+// of j in q2k[i] (binary search in the ascending list; k2q is its exact transpose). One warp per KV block.
+// The last head's first CTA also writes the total number of pairs (the path switch).
+__global__ void __launch_bounds__(256) k_pair_slot(int N, int BH, const int* __restrict__ q2k_num,
+                                                   const int* __restrict__ q2k_idx, const int* __restrict__ k2q_num,
+                                                   const int* __restrict__ k2q_idx, const int* __restrict__ q2k_off,
+                                                   const int* __restrict__ tot, int* __restrict__ k2q_slot,
+                                                   int* __restrict__ pair_total) {
+  __shared__ int s_part[8];
+  const int bh = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int b = 0;
+  for (int h = threadIdx.x; h < bh; h += 256) b += tot[h];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  if (lane == 0) s_part[warp] = b;
+  __syncthreads();
+  const int base = s_part[0] + s_part[1] + s_part[2] + s_part[3] + s_part[4] + s_part[5] + s_part[6] + s_part[7];
+  if (bh == BH - 1 && blockIdx.x == 0 && threadIdx.x == 0) *pair_total = base + tot[bh];
+  const int j = blockIdx.x * 8 + warp;
+  if (j >= N) return;
+  const size_t hN = static_cast<size_t>(bh) * N;
+  const int nq = k2q_num[hN + j];
+  for (int pp = lane; pp < nq; pp += 32) {
+    const int i = k2q_idx[(hN + j) * N + pp];
+    const int* row = q2k_idx + (hN + i) * N;
+    int lo = 0, hi = q2k_num[hN + i];  // first position with row[pos] >= j
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (row[mid] < j) lo = mid + 1;
+      else hi = mid;
+    }
+    k2q_slot[(hN + j) * N + pp] = base + q2k_off[hN + i] + lo;
+  }
+}
+
+// ------------------------------------------------------------------------------------ dS path: dQ
+// dQ[kept rows of block i] = scale * sum over its admitted KV blocks j of dS_ij K_j, formed transposed so the
+// tensor-core M is the channel dimension: dQ_i^T (d x SR) += K_j^T (d x BT, MN-major) dS_ij^T (BT x SR, K-major),
+// one TMEM accumulator per query block of the CTA's tile (fp32, deterministic order: ascending j).
+// Warps 0-3: epilogue (thread = channel = TMEM lane), warp 4: producer (K_j by the 5D block box, dS tile by one
+// bulk copy), warp 5: TMEM allocator + MMA issuer.
+constexpr int DQ_STAGES = 4;
+constexpr int DQ_THREADS = 192;
+template <int D, int BT>
+struct DqSmem {
+  static constexpr int NCB = D / 64;
+  static constexpr int K_BYTES = BT * D * 2;
+  static constexpr int DS_BYTES = 64 * 128;  // up to 64 rows of 128 B (SR <= 64; N >= 16 rows read)
+  static constexpr int STAGE = K_BYTES + DS_BYTES;
+  static constexpr int OFF_ZERO = DQ_STAGES * STAGE;  // d = 64: zero channels 64..127 of the M = 128 operand
+  static constexpr int TOTAL = OFF_ZERO + (D == 64 ? BT * 128 : 0);
+};
+
+struct DqParams {
+  CUtensorMap mK;
+  Geo g;
+  int Lq, SR, N16, Gq, bh0;
+  const int* kept_off;
+  const int* kept_tok;
+  const int* q2k_num;
+  const int* q2k_idx;
+  const int* q2k_off;
+  const int* tot;
+  const int* pair_total;
+  long long ds_cap;
+  const uint8_t* ds_buf;
+  float scale;
+  Rows dQ;
+};
+
+template <int D, int BT>
+__global__ void __launch_bounds__(DQ_THREADS) k_bwd_dq(const __grid_constant__ DqParams p) {
+  using SM = DqSmem<D, BT>;
+  if (!(*p.pair_total <= p.ds_cap)) return;  // reduce path
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  __shared__ __align__(8) uint64_t bar_full[DQ_STAGES], bar_empty[DQ_STAGES], bar_acc[16];
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_base;
+  const Geo& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int hc = blockIdx.y, bh = p.bh0 + hc;
+  const int Gq = p.Gq, N16 = p.N16, SR = p.SR;
+  const int i0 = blockIdx.x * Gq;
+  const int nblk = min_i(Gq, g.N - i0);
+  const size_t hN = static_cast<size_t>(bh) * g.N;
+  if (tid == 0) {
+    for (int s = 0; s < DQ_STAGES; ++s) { mbar_init(&bar_full[s], 1); mbar_init(&bar_empty[s], 1); }
+    for (int k = 0; k < 16; ++k) mbar_init(&bar_acc[k], 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(&s_tmem, Gq * N16 <= 32 ? 32 : Gq * N16 <= 64 ? 64 : Gq * N16 <= 128 ? 128 : 256);
+  if (warp == 4) {  // pair base of this head
+    int b = 0;
+    for (int h = lane; h < bh; h += 32) b += p.tot[h];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) s_base = b;
+  }
+  if (D == 64)
+    for (int o = tid * 16; o < BT * 128; o += DQ_THREADS * 16)
+      *reinterpret_cast<uint4*>(sm + SM::OFF_ZERO + o) = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tacc = s_tmem;
+  const int base = s_base;
+
+  if (warp == 4) {
+    // ============================ producer: every admitted pair of the tile's blocks, block by block
+    int n = 0;
+    for (int gi = 0; gi < nblk; ++gi) {
+      const int i = i0 + gi;
+      const int num = p.q2k_num[hN + i];
+      const size_t off = static_cast<size_t>(base) + p.q2k_off[hN + i];
+      const int* list = p.q2k_idx + (hN + i) * g.N;
+      for (int t0 = 0; t0 < num; t0 += 32) {
+        const int jl = t0 + lane < num ? list[t0 + lane] : 0;  // 32 list entries fetched at once
+        const int cnt = min_i(32, num - t0);
+        for (int e = 0; e < cnt; ++e, ++n) {
+          const int j = __shfl_sync(0xffffffffu, jl, e);
+          const int s = n % DQ_STAGES;
+          if (lane == 0) {
+            mbar_wait(&bar_empty[s], ((n / DQ_STAGES) & 1) ^ 1);
+            mbar_expect_tx(&bar_full[s], SM::K_BYTES + SR * 128);
+            uint8_t* st = sm + s * SM::STAGE;
+            const int bt = j / (g.Nh * g.Nw), bhh = (j / g.Nw) % g.Nh, bw = j % g.Nw;
+            for (int cb = 0; cb < SM::NCB; ++cb)
+              tma_load_5d(st + cb * BT * 128, &p.mK, &bar_full[s], cb * 64, bw * g.cw, bhh * g.ch, bt * g.ct, hc);
+            bulk_load(st + SM::K_BYTES, p.ds_buf + (off + t0 + e) * static_cast<size_t>(SR) * 128, SR * 128,
+                      &bar_full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ============================ MMA issuer: dQ_i^T += K_j^T dS_ij^T (M = 128 channels, N = N16 rows, K = BT)
+    const bool leader = elect_one();
+    const uint32_t idesc = umma_idesc_bf16(128, N16, 1, 0);
+    const uint32_t zero = smem_u32(sm + SM::OFF_ZERO);
+    int n = 0;
+    for (int gi = 0; gi < nblk; ++gi) {
+      const int num = p.q2k_num[hN + i0 + gi];
+      for (int t = 0; t < num; ++t, ++n) {
+        const int s = n % DQ_STAGES;
+        mbar_wait(&bar_full[s], (n / DQ_STAGES) & 1);
+        tc_fence_after();
+        if (leader) {
+          const uint32_t ka = smem_u32(sm + s * SM::STAGE), da = ka + SM::K_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BT / 16; ++kk) {
+            // A: K_j^T, MN-major over channels (64-channel chunks BT * 128 B apart; d = 64 reads the zero block)
+            const uint64_t adesc = umma_desc_sw128(ka + kk * 2048, D == 128 ? BT * 128 : zero - ka, 1024);
+            const uint64_t bdesc = umma_desc_sw128(da + kk * 32, 16, 1024);  // B: dS rows, K-major over keys
+            umma_ss(tacc + gi * N16, adesc, bdesc, idesc, (t > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&bar_empty[s]);
+          if (t == num - 1) umma_commit(&bar_acc[gi]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 4) {
+    // ============================ epilogue: thread = channel (TMEM lane), columns = the block's rows
+    const int ch = warp * 32 + lane;
+    const uint32_t trow = tacc + (static_cast<uint32_t>(warp * 32) << 16);
+    for (int gi = 0; gi < nblk; ++gi) {
+      const int i = i0 + gi;
+      const int num = p.q2k_num[hN + i];
+      const int ko = p.kept_off[i], nk = p.kept_off[i + 1] - ko;
+      if (num > 0) {
+        mbar_wait(&bar_acc[gi], 0);
+        tc_fence_after();
+      }
+      for (int c0 = 0; c0 < nk; c0 += 16) {
+        float v[16];
+        if (num > 0) {
+          tmem_ld16(trow + gi * N16 + c0, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0.f;
+        }
+        if (ch < D) {
+          const int* toks = p.kept_tok + static_cast<size_t>(bh) * p.Lq + ko;
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (c0 + e < nk) p.dQ.row(bh, toks[c0 + e])[ch] = __float2bfloat16_rn(v[e] * p.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc(tacc, Gq * N16 <= 32 ? 32 : Gq * N16 <= 64 ? 64 : Gq * N16 <= 128 ? 128 : 256);
+}
+
 // ------------------------------------------------------------------------------------ finalize
 // dQ of one (b,h, block): kept tokens (ascending) take scale * dQacc of their packed row kept_off[b] + rank,
 // pruned tokens get 0 (reading C10). One CTA per block: the block's donors decide kept / pruned, a ballot
@@ -821,7 +1106,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 template <int D>
 __global__ void __launch_bounds__(256) k_bwd_finalize(Geo g, int Lq, float scale, const int* __restrict__ kept_off,
                                                       const int* __restrict__ donor, const float* __restrict__ dQacc,
-                                                      const Rows dQ) {
+                                                      const Rows dQ, const int* __restrict__ pair_total,
+                                                      long long ds_cap) {
+  if (*pair_total <= ds_cap) return;  // dS path: k_bwd_dq wrote dQ
   constexpr int MAXT = 128, VPR = D / 8;
   __shared__ int s_tok[MAXT], s_prow[MAXT], s_wk[8];
   const int blk = blockIdx.x, bh = blockIdx.y;
@@ -861,30 +1148,90 @@ __global__ void __launch_bounds__(256) k_bwd_finalize(Geo g, int Lq, float scale
   }
 }
 
-template <int D, int BT>
-static cudaError_t run_bwd(const BwdParams& p, cudaStream_t st) {
-  constexpr int smem = BwdSmem<D, BT>::TOTAL;
-  cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  k_attn_bwd<D, BT><<<dim3(static_cast<unsigned>(min_i(p.items, sms))), BWD_THREADS, smem, st>>>(p);  // persistent
-  return cudaGetLastError();
-}
-
 // The K/V/dK/dV tensor maps index heads with one stride: one launch over all B*Hh heads when the batch stride
 // continues the head stride (sb == Hh sh, e.g. contiguous [B, Hh, L, d], or B == 1), else one launch per batch.
 static bool heads_uniform(const Rows& x, int B) { return B == 1 || x.sb == x.Hh * x.sh; }
+
+template <int D, int BT, bool DS>
+static cudaError_t run_bwd1(const BwdParams& p, int sms, cudaStream_t st) {
+  constexpr int smem = BwdSmem<D, BT, DS>::TOTAL;
+  cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<D, BT, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_attn_bwd<D, BT, DS><<<dim3(static_cast<unsigned>(min_i(p.items, sms))), BWD_THREADS, smem, st>>>(p);  // persistent
+  return cudaGetLastError();
+}
+// both instantiations are launched; the one whose path the device-side pair count does not select exits at once
+template <int D, int BT>
+static cudaError_t run_bwd(const BwdParams& p, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = run_bwd1<D, BT, true>(p, sms, st);
+  if (e == cudaSuccess) e = run_bwd1<D, BT, false>(p, sms, st);
+  return e;
+}
+
+// slot of every admitted pair for the dS path (k_pair_off, k_pair_slot) and the path switch *pair_total
+cudaError_t launch_bwd_pairs(const BwdArgs& a, cudaStream_t st) {
+  k_pair_off<<<a.BH, 1024, 0, st>>>(a.g.N, a.q2k_num, a.q2k_off, a.pair_tot);
+  k_pair_slot<<<dim3((a.g.N + 7) / 8, a.BH), 256, 0, st>>>(a.g.N, a.BH, a.q2k_num, a.q2k_idx, a.k2q_num, a.k2q_idx,
+                                                            a.q2k_off, a.pair_tot, a.k2q_slot, a.pair_total);
+  return cudaGetLastError();
+}
+
+template <int D, int BT>
+static cudaError_t run_dq(const DqParams& p, int heads, cudaStream_t st) {
+  constexpr int smem = DqSmem<D, BT>::TOTAL;
+  cudaError_t e = cudaFuncSetAttribute(k_bwd_dq<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_bwd_dq<D, BT><<<dim3((p.g.N + p.Gq - 1) / p.Gq, heads), DQ_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+// dS path: dQ of the kept rows from the stored dS tiles (exits at once on the reduce path)
+cudaError_t launch_bwd_dq(const BwdArgs& a, cudaStream_t st) {
+  DqParams p;
+  memset(&p, 0, sizeof(p));
+  p.g = a.g;
+  p.Lq = a.Lq;
+  p.SR = a.SR;
+  p.N16 = a.SR < 16 ? 16 : a.SR;
+  p.Gq = 128 / p.N16;
+  p.kept_off = a.kept_off;
+  p.kept_tok = a.kept_tok;
+  p.q2k_num = a.q2k_num;
+  p.q2k_idx = a.q2k_idx;
+  p.q2k_off = a.q2k_off;
+  p.tot = a.pair_tot;
+  p.pair_total = a.pair_total;
+  p.ds_cap = a.ds_cap;
+  p.ds_buf = a.ds_buf;
+  p.scale = a.scale;
+  p.dQ = a.dQ;
+  const bool one = heads_uniform(a.K, a.B);
+  const int launches = one ? 1 : a.B, heads = one ? a.BH : a.Hh;
+  for (int b = 0; b < launches; ++b) {
+    if (!make_map_5d(&p.mK, a.K.p + b * a.K.sb, a.g, a.d, heads, a.K.sl, a.K.sh)) return cudaErrorInvalidValue;
+    p.bh0 = b * a.Hh;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (a.d == 128 && a.g.BT == 64) e = run_dq<128, 64>(p, heads, st);
+    else if (a.d == 128 && a.g.BT == 32) e = run_dq<128, 32>(p, heads, st);
+    else if (a.d == 64 && a.g.BT == 64) e = run_dq<64, 64>(p, heads, st);
+    else if (a.d == 64 && a.g.BT == 32) e = run_dq<64, 32>(p, heads, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
   const dim3 prep_blocks(a.g.N, a.BH);  // one CTA per (b,h, query block)
   if (a.d == 128)
     k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc);
+                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ);
   else
     k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                a.O, a.lse, a.qdo_img, a.lsed, a.dQacc);
+                                                a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ);
   return cudaGetLastError();
 }
 
@@ -903,6 +1250,10 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.scale = a.scale;
   p.qdo_img = a.qdo_img;
   p.lsed = a.lsed;
+  p.pair_total = a.pair_total;
+  p.ds_cap = a.ds_cap;
+  p.k2q_slot = a.k2q_slot;
+  p.ds_buf = a.ds_buf;
   p.dq_rows = a.SR < BSA_DQ_SLOT_ROWS ? a.SR : BSA_DQ_SLOT_ROWS;
   if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
   const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
@@ -933,9 +1284,11 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
 cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st) {
   const dim3 grid(a.g.N, a.BH);
   if (a.d == 128)
-    k_bwd_finalize<128><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ);
+    k_bwd_finalize<128><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ, a.pair_total,
+                                              a.ds_cap);
   else
-    k_bwd_finalize<64><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ);
+    k_bwd_finalize<64><<<grid, 256, 0, st>>>(a.g, a.Lq, a.scale, a.kept_off, a.donor, a.dQacc, a.dQ, a.pair_total,
+                                             a.ds_cap);
   return cudaGetLastError();
 }
 

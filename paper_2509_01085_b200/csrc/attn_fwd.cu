@@ -84,8 +84,14 @@ struct FwdSmem {
   static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
   // TMEM columns: O of the even / odd steps [0, 2D), S double buffer, Q^s (packed bf16 pairs), P double
   // buffer (packed). Buffer b = step parity = softmax group.
+#ifndef BSA_FWD_PALIAS
   static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 2 * BT, T_P = T_Q + D / 2;
   static constexpr int TMEM_COLS = (T_P + BT) <= 256 ? 256 : 512;
+#else
+  // three S buffers; P(u) is written over the first BT / 2 columns of S(u) (no separate P buffers)
+  static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 3 * BT, T_P = T_S;
+  static constexpr int TMEM_COLS = (T_Q + D / 2) <= 256 ? 256 : 512;
+#endif
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -115,8 +121,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   uint32_t* bits = reinterpret_cast<uint32_t*>(sm + SM::OFF_BITS);
   uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
 
-  __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
-      bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o_final;
+#ifndef BSA_FWD_PALIAS
+  constexpr int NSB = 2;
+#else
+  constexpr int NSB = 3;  // S/P buffers in flight: step u uses buffer u % 3
+#endif
+  __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[NSB],
+      bar_s_free[NSB], bar_p_full[NSB], bar_p_free[2], bar_o_final;
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
@@ -157,10 +168,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     mbar_init(&bar_qt, 128);
     for (int s = 0; s < FWD_STAGES; ++s) { mbar_init(&bar_kv_full[s], 1); mbar_init(&bar_kv_empty[s], 1); }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_s_full[b], 1);
-      mbar_init(&bar_s_free[b], 128);
-      mbar_init(&bar_p_full[b], 128);
       mbar_init(&bar_p_free[b], 1);
+    }
+    for (int b = 0; b < NSB; ++b) {
+      mbar_init(&bar_s_full[b], 1);
+#ifndef BSA_FWD_PALIAS
+      mbar_init(&bar_s_free[b], 128);
+#else
+      mbar_init(&bar_s_free[b], 1);  // PV(u) done: buffer u % 3 (S, then P over it) free
+#endif
+      mbar_init(&bar_p_full[b], 128);
     }
     mbar_init(&bar_o_final, 1);
     fence_mbar_init();
@@ -399,10 +416,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
 #endif
       for (int v = 0; v < U; ++v) {
+#ifndef BSA_FWD_PALIAS
         const int s = v % FWD_STAGES, sb = v & 1;
+#else
+        const int s = v % FWD_STAGES, sb = v % 3;
+#endif
         const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[entry_at(v) >> 12], 0, 0);  // N = n16 keys
         mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
+#ifndef BSA_FWD_PALIAS
         if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
+#else
+        if (v >= 3) mbar_wait(&bar_s_free[sb], ((v / 3) - 1) & 1);  // PV(v - 3) done
+#endif
         tc_fence_after();
         const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
         if (leader) {
@@ -422,7 +447,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       for (int u = 0; u < U; ++u) {
         const int pb = u & 1, s = u % FWD_STAGES;
         const int nkk = s_clsn16[entry_at(u) >> 12] / 16;  // K = n16 keys
+#ifndef BSA_FWD_PALIAS
+        const uint32_t tPu = tP + pb * (BT / 2);
         mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
+#else
+        const int b3 = u % 3;
+        const uint32_t tPu = tS + b3 * BT;
+        mbar_wait(&bar_p_full[b3], (u / 3) & 1);
+#endif
         FWD_TRACE(2, u);
         tc_fence_after();
         const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
@@ -431,7 +463,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           for (int kk = 0; kk < BT / 16; ++kk) {
             if (kk >= nkk) break;
 #ifndef BSA_ABLATE_FWD_MMA
-            umma_ts(tO + pb * D, tP + pb * (BT / 2) + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv,
+            umma_ts(tO + pb * D, tPu + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv,
                     (u > 1 || kk > 0) ? 1u : 0u);
 #endif
           }
@@ -439,6 +471,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           // read of the stage
           umma_commit(&bar_kv_empty[s]);
           umma_commit(&bar_p_free[pb]);
+#ifdef BSA_FWD_PALIAS
+          umma_commit(&bar_s_free[b3]);
+#endif
         }
         __syncwarp();
         FWD_TRACE(3, u);
@@ -485,7 +520,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       mbar_arrive(&bar_qt);
     }
     const float sl2 = p.scale_log2;
-    const uint32_t tS = trow + SM::T_S + group * BT, tP = trow + SM::T_P + group * (BT / 2);
+#ifndef BSA_FWD_PALIAS
+    const uint32_t tS0 = trow + SM::T_S + group * BT, tP0 = trow + SM::T_P + group * (BT / 2);
+#endif
     const uint32_t tO = trow + SM::T_O + group * D;
     float m_run = -INFINITY, l_run = 0.f;
     for (int u = group; u < U; u += 2) {
@@ -496,7 +533,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       // instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
       constexpr int n16 = BT;
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
+#ifndef BSA_FWD_PALIAS
+      const uint32_t tS = tS0, tP = tP0;
       mbar_wait(&bar_s_full[group], ph);
+#else
+      const int b3 = u % 3;
+      const uint32_t tS = trow + SM::T_S + b3 * BT, tP = tS;  // P(u) over S(u)
+      mbar_wait(&bar_s_full[b3], (u / 3) & 1);
+#endif
       if (row == 0) FWD_TRACE(4 + 8 * group, u);
 #ifdef BSA_TRACE
       if (u == 0 && row == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
@@ -518,93 +562,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       tmem_wait_ld();
       if (row == 0) FWD_TRACE(6 + 8 * group, u);
+#ifndef BSA_FWD_PALIAS
       tc_fence_before();
       mbar_arrive(&bar_s_free[group]);
-#ifdef BSA_FWD_SPEC
-      // Speculative exponentials: P = 2^(s sl2 - m_run) with the running (possibly stale) max, streamed to TMEM
-      // 32 keys at a time while the step's max is formed alongside; only if that max exceeds m_run by more
-      // than 2^8 (rare after the first step) are O and l rescaled and P recomputed from the scores still in
-      // registers. The row's first admitted step takes its exact max first (m_run = -inf).
-      const bool wadmit = __any_sync(0xffffffffu, admit);
-      if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
-      if (row == 0) FWD_TRACE(7 + 8 * group, u);
-      if (wadmit) {
-        if (admit) {
-          if (cls != 0) {
-            const uint64_t km = s_clsmask[cls];
-            const uint32_t k0 = static_cast<uint32_t>(km), k1 = static_cast<uint32_t>(km >> 32);
-#pragma unroll
-            for (int c = 0; c < BT; ++c)
-              if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
-          }
-          if (m_run == -INFINITY) {
-            float mp0[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-            for (int c = 0; c < BT; ++c) mp0[c & 3] = fmaxf(mp0[c & 3], sv[c]);
-            m_run = fmaxf(fmaxf(mp0[0], mp0[1]), fmaxf(mp0[2], mp0[3])) * sl2;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < BT; ++c) sv[c] = -INFINITY;
-        }
-        const float2 sl2v = make_float2(sl2, sl2);
-        float mref = admit ? m_run : 0.f;
-        float2 sp2[4];
-        float mp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        for (int pass = 0; pass < 2; ++pass) {
-          const float2 nm = make_float2(-mref, -mref);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sp2[e] = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int c0 = 0; c0 < BT; c0 += 32) {
-            float w[16];
-#pragma unroll
-            for (int c = c0; c < c0 + 32; c += 2) {
-              if (pass == 0) {
-                mp[c & 3] = fmaxf(mp[c & 3], sv[c]);
-                mp[(c + 1) & 3] = fmaxf(mp[(c + 1) & 3], sv[c + 1]);
-              }
-              const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
-              const float e0 = ex2(x.x);
-              const float e1 = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
-              sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(e0, e1));
-              w[(c - c0) >> 1] = __uint_as_float(pack_bf16(e0, e1));
-            }
-            tmem_st16(tP + (c0 >> 1), w);
-          }
-          if (pass == 1) break;
-          const float mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])) * sl2;
-          const bool grow = admit && mx > m_run + 8.f;
-          if (!__any_sync(0xffffffffu, grow)) break;
-          // rare: the max grew by more than 2^8 -- rescale O and l, recompute P with the new max
-          const float alpha = grow ? ex2(m_run - mx) : 1.f;
-          if (grow) {
-            l_run *= alpha;
-            m_run = mx;
-          }
-          mref = admit ? m_run : 0.f;
-          tmem_wait_st();
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D; c += 16) {
-            float ov[16];
-            tmem_ld16(tO + c, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) ov[e] *= alpha;
-            tmem_st16(tO + c, ov);
-          }
-        }
-        if (admit)
-          l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
-      } else {
-        float w[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) w[e] = 0.f;
-#pragma unroll
-        for (int c0 = 0; c0 < BT / 2; c0 += 16) tmem_st16(tP + c0, w);
-      }
-#else
+#endif
       float alpha = 1.f;
       bool need_rescale = false;
 #ifdef BSA_ABLATE_FWD_EXP
@@ -669,8 +630,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll
         for (int c = 0; c < BT; ++c) sv[c] = 0.f;
       }
-      // P buffer and O accumulator of this group are free once PV(u-2) (its previous step) completed
+      // P buffer and O accumulator of this group are free once PV(u-2) (its previous step) completed (with
+      // P over S, only an O rescale needs that)
+#ifndef BSA_FWD_PALIAS
       if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
+#else
+      if (u >= 2 && __any_sync(0xffffffffu, need_rescale)) mbar_wait(&bar_p_free[group], ph ^ 1);
+#endif
       if (row == 0) FWD_TRACE(7 + 8 * group, u);
       // O rescale in TMEM; warp-collective access
       if (__any_sync(0xffffffffu, need_rescale)) {
@@ -695,10 +661,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           tmem_st16(tP + c0, w);
         }
       }
-#endif
       tmem_wait_st();
       tc_fence_before();
+#ifndef BSA_FWD_PALIAS
       mbar_arrive(&bar_p_full[group]);
+#else
+      mbar_arrive(&bar_p_full[b3]);
+#endif
       if (row == 0) FWD_TRACE(5 + 8 * group, u);
     }
     // epilogue: merge the two groups' (m, l, O), O^s = O / l scattered to the kept token's raster row,

@@ -97,7 +97,18 @@ struct BwdArgs {
   float* lsed;       // [BH, N, 2, SR]: per query block LSE*log2(e) of its SR rows, then D of its SR rows
   float* dQacc;  // [BH, Lq, d]
   int* work_ctr;  // [B] item counters of the persistent main kernel (one per launch)
+  // dS path (attn_bwd.cu): selection lists, pair slots, the path switch and the dS tile store
+  const int* q2k_num;
+  const int* q2k_idx;
+  int* q2k_off;      // [BH, N] head-local exclusive scan of q2k_num
+  int* pair_tot;     // [BH] pairs per head
+  int* pair_total;   // [1] all pairs (dS path iff <= ds_cap)
+  int* k2q_slot;     // [BH, N, N]
+  uint8_t* ds_buf;   // ds_cap tiles of SR x 128 B
+  long long ds_cap;
 };
+cudaError_t launch_bwd_pairs(const BwdArgs& a, cudaStream_t st);
+cudaError_t launch_bwd_dq(const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_finalize(const BwdArgs& a, cudaStream_t st);

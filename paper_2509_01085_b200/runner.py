@@ -163,7 +163,8 @@ class BSAAttention:
         T = tensor_desc
         _check(lib().bsa_attn_bwd(ctypes.byref(self._g), self.r, self.B, self.Hh, self.d, T(None), T(K), T(V), T(O),
                                   T(dO), _ptr(self.q_packed), _ptr(self.kept_off), _ptr(self.kept_tok),
-                                  _ptr(self.donor), _ptr(self.k2q_num), _ptr(self.k2q_idx), _ptr(self.lse),
+                                  _ptr(self.donor), _ptr(self.q2k_num), _ptr(self.q2k_idx), _ptr(self.k2q_num),
+                                  _ptr(self.k2q_idx), _ptr(self.lse),
                                   ctypes.c_float(self.scale), T(dQ), T(dK), T(dV), _ptr(self.ws), self.ws.numel(),
                                   self._stream()), "bsa_attn_bwd")
         return dQ, dK, dV

@@ -86,8 +86,16 @@ def test_selection_parity(case):
             assert np.array_equal(kidx[h, j, :knum[h, j]], np.nonzero(adm[:, j])[0])
 
 
+@pytest.fixture(params=["auto", "reduce"])
+def bwd_path(request):
+    """Both dQ paths of bsa_attn_bwd: auto (the dS path at these densities) and the forced L2-reduce path."""
+    bsa.set_bwd_path(bsa.BWD_REDUCE if request.param == "reduce" else bsa.BWD_AUTO)
+    yield request.param
+    bsa.set_bwd_path(bsa.BWD_AUTO)
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_attention_parity(case):
+def test_attention_parity(case, bwd_path):
     og, g, host, dev, k, sel = _run(case, seed=1)
     name, grid, block, unit, Hh, d, r, f, tau, kind = case
     Q, K, V = dev
@@ -114,14 +122,15 @@ def test_attention_parity(case):
     assert lse_err < 2e-2
     # backward
     dO = bsa_gen.grad_output(1, (1, Hh, og.L, d)).cuda()
-    dQ, dK, dV = bsa.bsa_attn_bwd(g, r, Q, K, V, O, dO, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.k2q_num,
-                                  sel.k2q_idx, lse, scale=scale, q_packed=sel.q_packed)
+    dQ, dK, dV = bsa.bsa_attn_bwd(g, r, Q, K, V, O, dO, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num,
+                                  sel.q2k_idx, sel.k2q_num, sel.k2q_idx, lse, scale=scale, q_packed=sel.q_packed)
     torch.cuda.synchronize()
     dQr, dKr, dVr = orc.attn_bwd(og, r, host[0][0], host[1][0], host[2][0], dO.cpu()[0], kt, dn, qn, qi,
                                  float(np.float32(scale)))
-    assert_close("dV", dV[0], dVr, case=name)
-    assert_close("dK", dK[0], dKr, case=name)
-    assert_close("dQ", dQ[0], dQr, case=name)
+    tag = name if bwd_path == "auto" else name + "/reduce"
+    assert_close("dV", dV[0], dVr, case=tag)
+    assert_close("dK", dK[0], dKr, case=tag)
+    assert_close("dQ", dQ[0], dQr, case=tag)
     # exact structural properties: pruned dQ rows are 0; unadmitted key blocks get 0
     pruned = dn != np.arange(og.L)[None, :]
     assert torch.count_nonzero(dQ[0].cpu()[torch.from_numpy(pruned)]) == 0

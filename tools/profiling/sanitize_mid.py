@@ -19,7 +19,7 @@ sel = bsa.select(g, r, k, tau, Q, K)
 O, lse = bsa.bsa_attn_fwd(g, r, Q, K, V, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num, sel.q2k_idx,
                           q_packed=sel.q_packed)
 dO = bsa_gen.grad_output(0, (1, Hh, g.L, d)).cuda()
-dQ, dK, dV = bsa.bsa_attn_bwd(g, r, Q, K, V, O, dO, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.k2q_num,
-                              sel.k2q_idx, lse, q_packed=sel.q_packed)
+dQ, dK, dV = bsa.bsa_attn_bwd(g, r, Q, K, V, O, dO, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num,
+                              sel.q2k_idx, sel.k2q_num, sel.k2q_idx, lse, q_packed=sel.q_packed)
 torch.cuda.synchronize()
 print("mid ok", float(O.float().abs().sum()), float(dQ.float().abs().sum()))
