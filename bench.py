@@ -348,15 +348,31 @@ def main():
     phases = {
         "selection_ms": sum(kms[i] for i in SELECTION_IDS) / args.steps,
         "fwd_ms": (kms[7] + kms[8] + kms[12] + kms[14]) / args.steps,
-        "bwd_ms": (kms[9] + kms[10] + kms[11]) / args.steps,
+        "bwd_ms": (kms[9] + kms[10] + kms[11] + kms[15] + kms[16]) / args.steps,
         "sp_relayout_ms": kms[13] / args.steps,
     }
 
     # ---------------------------------------------------------------- roofline (dominant kernel)
+    # The backward's dQ path (include/bsa.h bsa_attn_bwd): the dS path when the admitted (query block, KV block)
+    # pairs fit the workspace -- attn_bwd then executes S, dP, dV, dK (8 d P flops) and bwd_dq dQ (2 d P) --
+    # else the reduce path, where attn_bwd executes all five contractions (10 d P).
     peaks = read_peaks()
-    dom = "attn_bwd" if kms[10] >= kms[7] else "attn_fwd"
-    dom_ms = kms[10 if dom == "attn_bwd" else 7] / max(1, kcnt[10 if dom == "attn_bwd" else 7])
-    dom_flops = fl["bwd"] if dom == "attn_bwd" else fl["fwd"]
+    n_pairs = int(layer.q2k_num.to(torch.int64).sum().item())
+    cap = bsa.bwd_ds_capacity(g, layer.r, B, layer.Hh, d)
+    ds_path = 0 <= n_pairs <= cap
+    P = fl["pairs"]
+    per_kernel = {"attn_fwd": (7, fl["fwd"]), "attn_bwd": (10, (8 if ds_path else 10) * d * P)}
+    if ds_path:
+        per_kernel["bwd_dq"] = (16, 2 * d * P)
+    kernels_roof = {}
+    for kname, (kid, kfl) in per_kernel.items():
+        kms_avg = kms[kid] / max(1, kcnt[kid])
+        kernels_roof[kname] = {"avg_launch_ms": kms_avg, "algorithmic_flops_per_launch": kfl,
+                               "achieved_tflops": kfl / (kms_avg * 1e-3) / 1e12 if kms_avg > 0 else None,
+                               "frac": kfl / (kms_avg * 1e-3) / 1e12 / peaks["bf16"] if kms_avg > 0 else None}
+    dom = max(("attn_fwd", "attn_bwd"), key=lambda k: kms[per_kernel[k][0]])
+    dom_ms = kernels_roof[dom]["avg_launch_ms"]
+    dom_flops = per_kernel[dom][1]
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -367,16 +383,27 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16"], "traffic": traffic, "peak_source": f"{peaks['source']} bf16 burst",
-                "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_ms}
-    # Secondary bound of the backward: every admitted (query row, KV block) sends one fp32 dQ
-    # partial row of d values to the L2 reduce units; measured ceiling of that path 6.2 TB/s
-    # (tools/microbench/red_rate.cu, 128-byte-row tensor reduce boxes, all SMs).
-    dq_bytes = layer.admitted_block_rows() * d * 4
-    bwd_ms = kms[10] / max(1, kcnt[10])
-    roofline["secondary"] = {"bound": "l2_reduce", "kernel": "attn_bwd", "bytes_per_launch": dq_bytes,
-                             "achieved_tbs": dq_bytes / (bwd_ms * 1e-3) / 1e12, "peak_tbs": 6.2,
-                             "frac": dq_bytes / (bwd_ms * 1e-3) / 1e12 / 6.2,
-                             "peak_source": "measured, tools/microbench/red_rate.cu (profiles/r01_microbench.md)"}
+                "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_ms,
+                "bwd_dq_path": "ds" if ds_path else "reduce", "admitted_pairs": n_pairs, "ds_capacity": cap,
+                "kernels": kernels_roof}
+    if ds_path:
+        # bwd_dq streams one K tile (BT d 2 B, L2) and one dS tile (SR rows x 128 B, HBM) per admitted pair
+        tile_b = layer.g.BT * d * 2 + layer.SR * 128
+        dq_ms = kernels_roof["bwd_dq"]["avg_launch_ms"]
+        roofline["secondary"] = {"bound": "l2_copy", "kernel": "bwd_dq", "bytes_per_launch": n_pairs * tile_b,
+                                 "achieved_tbs": n_pairs * tile_b / (dq_ms * 1e-3) / 1e12 if dq_ms > 0 else None,
+                                 "peak_tbs": 19.0,
+                                 "peak_source": "measured L2 -> smem bulk copies, tools/microbench/bulk_bench.cu "
+                                                "(profiles/r01_microbench.md)"}
+    else:
+        # every admitted (query row, KV block) sends one fp32 dQ partial row of d values to the L2 reduce units;
+        # measured ceiling of that path 6.2 TB/s (tools/microbench/red_rate.cu, 128-byte-row tensor reduce boxes)
+        dq_bytes = layer.admitted_block_rows() * d * 4
+        bwd_ms = kms[10] / max(1, kcnt[10])
+        roofline["secondary"] = {"bound": "l2_reduce", "kernel": "attn_bwd", "bytes_per_launch": dq_bytes,
+                                 "achieved_tbs": dq_bytes / (bwd_ms * 1e-3) / 1e12, "peak_tbs": 6.2,
+                                 "frac": dq_bytes / (bwd_ms * 1e-3) / 1e12 / 6.2,
+                                 "peak_source": "measured, tools/microbench/red_rate.cu (profiles/r01_microbench.md)"}
     # selection kernels against HBM (algorithmic bytes), per (b,h): read Q and K once (4 L d B);
     # write kept_tok + donor (4 Lq + 4 L B); q2k and its transpose k2q, counts and the admitted block ids
     # (2 x 4 N (1 + avg|S_i|) B, blocks not tokens); the pooled Q_c (8 N d B) and Q^s (2 Lq d B) outputs

@@ -175,9 +175,9 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
  *   dQ, dK, dV [B,Hh,L,d] out bf16 (strided; Q.ptr may be NULL when q_packed is given).
  *   dQ is formed one of two ways, chosen on the device from the selection's number of admitted (query block,
  *   KV block) pairs against the workspace's capacity (a pair density of 1/8, at most 24 GiB):
- *     dS path (pairs fit): the KV-stationary kernel stores every pair's bf16 dS tile and a query-stationary
+ *     dS path (BSA_BWD_DS set and the pairs fit): the KV-stationary kernel stores every pair's bf16 dS tile and a query-stationary
  *       kernel forms dQ^T = sum_j K_j^T dS_ij^T in TMEM (fp32, ascending j: deterministic);
- *     reduce path (denser selections): fp32 dQ partials, one per (query row block, admitted KV block), are
+ *     reduce path (default; denser selections under BSA_BWD_DS): fp32 dQ partials, one per (query row block, admitted KV block), are
  *       reduced in L2 (cp.reduce.async.bulk.tensor) into an fp32 workspace: the summation order is not
  *       deterministic, so dQ may differ run to run in the last fp32 bits before the bf16 rounding. */
 int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, bsa_tensor Q, bsa_tensor K,
@@ -217,10 +217,16 @@ enum bsa_kernel_id {
   BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT,
   BSA_K_GROUP, BSA_K_BWD_PAIRS, BSA_K_BWD_DQ, BSA_K_COUNT
 };
-/* Backward dQ path (process-wide, default BSA_BWD_AUTO = the device-side switch described at bsa_attn_bwd;
- * BSA_BWD_REDUCE forces the reduce path, for tests and A/B timing). Unknown mode: BSA_ERR_CONFIG. */
-enum bsa_bwd_path { BSA_BWD_AUTO = 0, BSA_BWD_REDUCE = 1 };
+/* Backward dQ path (process-wide): BSA_BWD_REDUCE (default) always takes the reduce path; BSA_BWD_DS takes the
+ * dS path whenever the selection's pairs fit (the device-side switch described at bsa_attn_bwd). The default is
+ * the reduce path because it measured faster on the BASELINE workloads. Unknown mode:
+ * BSA_ERR_CONFIG. */
+enum bsa_bwd_path { BSA_BWD_REDUCE = 0, BSA_BWD_DS = 1 };
 int bsa_set_bwd_path(int mode);
+/* Capacity of the backward's dS path in admitted (query block, KV block) pairs for this geometry (-1 unless
+ * BSA_BWD_DS is set): bsa_attn_bwd takes the dS path iff sum(q2k_num) <= *pairs. Errors as
+ * bsa_workspace_bytes. */
+int bsa_bwd_ds_capacity(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, int64_t* pairs);
 /* Total kernels launched through libbsa by this process (always counted; cheap). */
 int64_t bsa_launch_count(void);
 /* When enabled (process-wide: autograd runs the backward on its own thread), every libbsa kernel launch is

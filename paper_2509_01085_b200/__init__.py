@@ -112,10 +112,11 @@ def lib() -> ctypes.CDLL:
         L.bsa_timing_enable.argtypes = [_I]
         L.bsa_timing_read.argtypes = [_P, _P, _I]
         L.bsa_set_bwd_path.argtypes = [_I]
+        L.bsa_bwd_ds_capacity.argtypes = [gp, _D, _I, _I, _I, _P]
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
-                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path"):
+                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path", "bsa_bwd_ds_capacity"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -296,11 +297,18 @@ def bsa_attn_bwd(g: Geometry, r: float, Q, K, V, O, dO, kept_off, kept_tok, dono
     return dQ, dK, dV
 
 
-BWD_AUTO, BWD_REDUCE = 0, 1
+BWD_REDUCE, BWD_DS = 0, 1
+
+
+def bwd_ds_capacity(g: Geometry, r: float, B: int, Hh: int, d: int) -> int:
+    """Admitted-pair capacity of the backward's dS path (-1 unless BWD_DS is set); include/bsa.h."""
+    out = ctypes.c_int64(0)
+    _check(lib().bsa_bwd_ds_capacity(ctypes.byref(g.c()), r, B, Hh, d, ctypes.byref(out)), "bsa_bwd_ds_capacity")
+    return int(out.value)
 
 
 def set_bwd_path(mode: int):
-    """Backward dQ path, process-wide (include/bsa.h bsa_set_bwd_path): BWD_AUTO or BWD_REDUCE."""
+    """Backward dQ path, process-wide (include/bsa.h bsa_set_bwd_path): BWD_REDUCE (default) or BWD_DS."""
     _check(lib().bsa_set_bwd_path(int(mode)), "bsa_set_bwd_path")
 
 

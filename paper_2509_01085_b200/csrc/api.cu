@@ -38,7 +38,7 @@ struct TimedRec {
 };
 // Process-wide (autograd runs the backward on its own worker thread, which must be counted and timed too).
 std::atomic<int64_t> g_launches{0};
-std::atomic<int> g_bwd_path{BSA_BWD_AUTO};  // bsa_set_bwd_path
+std::atomic<int> g_bwd_path{BSA_BWD_REDUCE};  // bsa_set_bwd_path
 std::atomic<bool> g_timing{false};
 std::mutex g_recs_mu;
 std::vector<TimedRec> g_recs;
@@ -304,6 +304,18 @@ int bsa_workspace_bytes(int op, const bsa_geom* g, double r, int32_t B, int32_t 
   return fail(BSA_ERR_CONFIG, "unknown op %d", op);
 }
 
+int bsa_bwd_ds_capacity(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, int64_t* pairs) {
+  bsa::Geo G;
+  CHECK(check_geom(g, &G));
+  CHECK(check_dims(B, Hh, d));
+  CHECK(check_r(r));
+  if (!pairs) return fail(BSA_ERR_SELECTION_MISMATCH, "pairs is NULL");
+  int lq = 0, mk = 0;
+  host_sizes(G, r, &lq, &mk);
+  *pairs = g_bwd_path.load() != BSA_BWD_DS ? -1 : bwd_ws(G, static_cast<size_t>(B) * Hh, lq, bsa::slot_rows(mk), d).cap;
+  return BSA_OK;
+}
+
 int bsa_block_partition(const bsa_geom* g, double r, int32_t* block_off, int32_t* block_tok, int32_t* block_ext,
                         int32_t* kept_off, void* stream) {
   bsa::Geo G;
@@ -544,26 +556,27 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.q2k_idx = q2k_idx;
   a.q2k_off = reinterpret_cast<int*>(base + w.qoff);
   a.pair_tot = reinterpret_cast<int*>(base + w.ptot);
-  a.pair_total = a.pair_tot + BH;
+  const bool ds_mode = g_bwd_path.load() == BSA_BWD_DS;
+  a.pair_total = ds_mode ? a.pair_tot + BH : nullptr;  // NULL: reduce path, nothing for the device to decide
   a.k2q_slot = reinterpret_cast<int*>(base + w.slot);
   a.ds_buf = base + w.ds;
-  a.ds_cap = g_bwd_path.load() == BSA_BWD_REDUCE ? -1 : w.cap;  // (pair_total >= 0 > -1: reduce path)
-  if (e == cudaSuccess) e = timed(BSA_K_BWD_PAIRS, 2, st, [&] { return bsa::launch_bwd_pairs(a, st); });
+  a.ds_cap = w.cap;
+  if (e == cudaSuccess && ds_mode) e = timed(BSA_K_BWD_PAIRS, 2, st, [&] { return bsa::launch_bwd_pairs(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_BWD_PREP, 1, st, [&] { return bsa::launch_bwd_prep(a, st); });
   const bool one_launch = (B == 1) || (Kv.sb == Hh * Kv.sh && Vv.sb == Hh * Vv.sh && dKv.sb == Hh * dKv.sh &&
                                        dVv.sb == Hh * dVv.sh);
   if (e == cudaSuccess)
-    e = timed(BSA_K_ATTN_BWD, 2 * (one_launch ? 1 : B), st, [&] { return bsa::launch_bwd_main(a, st); });
+    e = timed(BSA_K_ATTN_BWD, (ds_mode ? 2 : 1) * (one_launch ? 1 : B), st, [&] { return bsa::launch_bwd_main(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_BWD_FINAL, 1, st, [&] { return bsa::launch_bwd_finalize(a, st); });
   const bool k_uniform = (B == 1) || Kv.sb == Hh * Kv.sh;
-  if (e == cudaSuccess)
+  if (e == cudaSuccess && ds_mode)
     e = timed(BSA_K_BWD_DQ, k_uniform ? 1 : B, st, [&] { return bsa::launch_bwd_dq(a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_bwd");
   return BSA_OK;
 }
 
 int bsa_set_bwd_path(int mode) {
-  if (mode != BSA_BWD_AUTO && mode != BSA_BWD_REDUCE) return fail(BSA_ERR_CONFIG, "unknown backward path %d", mode);
+  if (mode != BSA_BWD_REDUCE && mode != BSA_BWD_DS) return fail(BSA_ERR_CONFIG, "unknown backward path %d", mode);
   g_bwd_path.store(mode);
   return BSA_OK;
 }

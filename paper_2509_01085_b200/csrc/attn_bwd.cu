@@ -104,12 +104,14 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
     s_don[i] = donor[head + t];
   }
   __syncthreads();
-  const bool ds = *pair_total <= ds_cap;  // dS path: no fp32 dQ accumulator to clear
+  // dS path (pair_total == NULL: reduce path chosen on the host): no fp32 dQ accumulator to clear, and the
+  // pruned rows of dQ are zeroed here (on the reduce path k_bwd_finalize writes every row)
+  const bool ds = pair_total != nullptr && *pair_total <= ds_cap;
   bf16* dqh = dQ.head(bh);
   for (int v = threadIdx.x; v < n * (D / 8); v += blockDim.x) {
     const int i = v / (D / 8), c = (v % (D / 8)) * 8;
     *reinterpret_cast<uint4*>(s_do + i * D + c) = *reinterpret_cast<const uint4*>(doh + s_tok[i] * dO.sl + c);
-    if (s_don[i] != s_tok[i])  // dQ of a pruned token is 0 (reading C10)
+    if (ds && s_don[i] != s_tok[i])  // dQ of a pruned token is 0 (reading C10)
       *reinterpret_cast<uint4*>(dqh + s_tok[i] * dQ.sl + c) = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
@@ -309,7 +311,7 @@ template <int D, int BT, bool DS>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
   using SM = BwdSmem<D, BT, DS>;
   // one of the two instantiations runs: the dS path when the pairs fit, else the reduce path (uniform exit)
-  if (DS != (*p.pair_total <= p.ds_cap)) return;
+  if (DS != (p.pair_total != nullptr && *p.pair_total <= p.ds_cap)) return;
   constexpr int NCB = SM::NCB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
@@ -787,6 +789,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         (void)any;
         continue;
 #endif
+#ifdef BSA_DQ_EARLY_RELEASE
+        // the whole partial row (D fp32) goes to registers first, so the TMEM buffer is handed back to the
+        // next dQ MMA at once; staging and reduce-adds then run from registers
+        float vall[D];
+#pragma unroll
+        for (int cs = 0; cs < D; cs += 16)
+          tmem_ld16(tdQ + qbuf * D + (static_cast<uint32_t>(q4 * 32) << 16) + cs, vall + cs);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bar_dq_free[qbuf]);
+#pragma unroll
+        for (int cs = 0; cs < D; cs += 32) {
+          const float* v = vall + cs;
+#else
 #pragma unroll 1
         for (int cs = 0; cs < D; cs += 32) {
           float v[32];
@@ -798,6 +814,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             tc_fence_before();
             mbar_arrive(&bar_dq_free[qbuf]);
           }
+#endif
           if (any) {
             const int s_first = slot_i;
             slot_i = (slot_i + SPS) % NSL;
@@ -1108,7 +1125,7 @@ __global__ void __launch_bounds__(256) k_bwd_finalize(Geo g, int Lq, float scale
                                                       const int* __restrict__ donor, const float* __restrict__ dQacc,
                                                       const Rows dQ, const int* __restrict__ pair_total,
                                                       long long ds_cap) {
-  if (*pair_total <= ds_cap) return;  // dS path: k_bwd_dq wrote dQ
+  if (pair_total != nullptr && *pair_total <= ds_cap) return;  // dS path: k_bwd_dq wrote dQ
   constexpr int MAXT = 128, VPR = D / 8;
   __shared__ int s_tok[MAXT], s_prow[MAXT], s_wk[8];
   const int blk = blockIdx.x, bh = blockIdx.y;
@@ -1160,13 +1177,14 @@ static cudaError_t run_bwd1(const BwdParams& p, int sms, cudaStream_t st) {
   k_attn_bwd<D, BT, DS><<<dim3(static_cast<unsigned>(min_i(p.items, sms))), BWD_THREADS, smem, st>>>(p);  // persistent
   return cudaGetLastError();
 }
-// both instantiations are launched; the one whose path the device-side pair count does not select exits at once
+// dS mode: both instantiations are launched and the one the device-side pair count does not select exits at once;
+// reduce mode (pair_total == NULL): only the reduce instantiation
 template <int D, int BT>
 static cudaError_t run_bwd(const BwdParams& p, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = run_bwd1<D, BT, true>(p, sms, st);
+  if (e == cudaSuccess && p.pair_total != nullptr) e = run_bwd1<D, BT, true>(p, sms, st);
   if (e == cudaSuccess) e = run_bwd1<D, BT, false>(p, sms, st);
   return e;
 }

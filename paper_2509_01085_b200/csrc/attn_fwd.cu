@@ -84,14 +84,8 @@ struct FwdSmem {
   static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
   // TMEM columns: O of the even / odd steps [0, 2D), S double buffer, Q^s (packed bf16 pairs), P double
   // buffer (packed). Buffer b = step parity = softmax group.
-#ifndef BSA_FWD_PALIAS
   static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 2 * BT, T_P = T_Q + D / 2;
   static constexpr int TMEM_COLS = (T_P + BT) <= 256 ? 256 : 512;
-#else
-  // three S buffers; P(u) is written over the first BT / 2 columns of S(u) (no separate P buffers)
-  static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 3 * BT, T_P = T_S;
-  static constexpr int TMEM_COLS = (T_Q + D / 2) <= 256 ? 256 : 512;
-#endif
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -121,11 +115,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   uint32_t* bits = reinterpret_cast<uint32_t*>(sm + SM::OFF_BITS);
   uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
 
-#ifndef BSA_FWD_PALIAS
   constexpr int NSB = 2;
-#else
-  constexpr int NSB = 3;  // S/P buffers in flight: step u uses buffer u % 3
-#endif
   __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[NSB],
       bar_s_free[NSB], bar_p_full[NSB], bar_p_free[2], bar_o_final;
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
@@ -172,11 +162,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     }
     for (int b = 0; b < NSB; ++b) {
       mbar_init(&bar_s_full[b], 1);
-#ifndef BSA_FWD_PALIAS
       mbar_init(&bar_s_free[b], 128);
-#else
-      mbar_init(&bar_s_free[b], 1);  // PV(u) done: buffer u % 3 (S, then P over it) free
-#endif
       mbar_init(&bar_p_full[b], 128);
     }
     mbar_init(&bar_o_final, 1);
@@ -416,18 +402,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
 #endif
       for (int v = 0; v < U; ++v) {
-#ifndef BSA_FWD_PALIAS
         const int s = v % FWD_STAGES, sb = v & 1;
-#else
-        const int s = v % FWD_STAGES, sb = v % 3;
-#endif
         const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[entry_at(v) >> 12], 0, 0);  // N = n16 keys
         mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
-#ifndef BSA_FWD_PALIAS
         if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
-#else
-        if (v >= 3) mbar_wait(&bar_s_free[sb], ((v / 3) - 1) & 1);  // PV(v - 3) done
-#endif
         tc_fence_after();
         const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
         if (leader) {
@@ -447,14 +425,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       for (int u = 0; u < U; ++u) {
         const int pb = u & 1, s = u % FWD_STAGES;
         const int nkk = s_clsn16[entry_at(u) >> 12] / 16;  // K = n16 keys
-#ifndef BSA_FWD_PALIAS
         const uint32_t tPu = tP + pb * (BT / 2);
         mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
-#else
-        const int b3 = u % 3;
-        const uint32_t tPu = tS + b3 * BT;
-        mbar_wait(&bar_p_full[b3], (u / 3) & 1);
-#endif
         FWD_TRACE(2, u);
         tc_fence_after();
         const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
@@ -471,9 +443,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
           // read of the stage
           umma_commit(&bar_kv_empty[s]);
           umma_commit(&bar_p_free[pb]);
-#ifdef BSA_FWD_PALIAS
-          umma_commit(&bar_s_free[b3]);
-#endif
         }
         __syncwarp();
         FWD_TRACE(3, u);
@@ -520,9 +489,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       mbar_arrive(&bar_qt);
     }
     const float sl2 = p.scale_log2;
-#ifndef BSA_FWD_PALIAS
     const uint32_t tS0 = trow + SM::T_S + group * BT, tP0 = trow + SM::T_P + group * (BT / 2);
-#endif
     const uint32_t tO = trow + SM::T_O + group * D;
     float m_run = -INFINITY, l_run = 0.f;
     for (int u = group; u < U; u += 2) {
@@ -533,14 +500,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       // instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
       constexpr int n16 = BT;
       const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
-#ifndef BSA_FWD_PALIAS
       const uint32_t tS = tS0, tP = tP0;
       mbar_wait(&bar_s_full[group], ph);
-#else
-      const int b3 = u % 3;
-      const uint32_t tS = trow + SM::T_S + b3 * BT, tP = tS;  // P(u) over S(u)
-      mbar_wait(&bar_s_full[b3], (u / 3) & 1);
-#endif
       if (row == 0) FWD_TRACE(4 + 8 * group, u);
 #ifdef BSA_TRACE
       if (u == 0 && row == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
@@ -562,10 +523,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       tmem_wait_ld();
       if (row == 0) FWD_TRACE(6 + 8 * group, u);
-#ifndef BSA_FWD_PALIAS
       tc_fence_before();
       mbar_arrive(&bar_s_free[group]);
-#endif
       float alpha = 1.f;
       bool need_rescale = false;
 #ifdef BSA_ABLATE_FWD_EXP
@@ -632,11 +591,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       // P buffer and O accumulator of this group are free once PV(u-2) (its previous step) completed (with
       // P over S, only an O rescale needs that)
-#ifndef BSA_FWD_PALIAS
       if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
-#else
-      if (u >= 2 && __any_sync(0xffffffffu, need_rescale)) mbar_wait(&bar_p_free[group], ph ^ 1);
-#endif
       if (row == 0) FWD_TRACE(7 + 8 * group, u);
       // O rescale in TMEM; warp-collective access
       if (__any_sync(0xffffffffu, need_rescale)) {
@@ -663,11 +618,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       }
       tmem_wait_st();
       tc_fence_before();
-#ifndef BSA_FWD_PALIAS
       mbar_arrive(&bar_p_full[group]);
-#else
-      mbar_arrive(&bar_p_full[b3]);
-#endif
       if (row == 0) FWD_TRACE(5 + 8 * group, u);
     }
     // epilogue: merge the two groups' (m, l, O), O^s = O / l scattered to the kept token's raster row,

@@ -32,6 +32,7 @@ class BSAAttention:
         self.g, self.r = geom, float(r)
         self.B, self.Hh, self.d = B, Hh, d
         self.N, self.Lq, self.max_kept = bsa_sizes(geom, r)
+        self.SR = max(8, 1 << max(0, self.max_kept - 1).bit_length())  # query-block slot rows (kernels.h slot_rows)
         self.set_knobs(f, tau)
         self.scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
         self.device = torch.device(device)

@@ -86,12 +86,12 @@ def test_selection_parity(case):
             assert np.array_equal(kidx[h, j, :knum[h, j]], np.nonzero(adm[:, j])[0])
 
 
-@pytest.fixture(params=["auto", "reduce"])
+@pytest.fixture(params=["reduce", "ds"])
 def bwd_path(request):
-    """Both dQ paths of bsa_attn_bwd: auto (the dS path at these densities) and the forced L2-reduce path."""
-    bsa.set_bwd_path(bsa.BWD_REDUCE if request.param == "reduce" else bsa.BWD_AUTO)
+    """Both dQ paths of bsa_attn_bwd: the default L2-reduce path and the dS path (which these sizes fit)."""
+    bsa.set_bwd_path(bsa.BWD_DS if request.param == "ds" else bsa.BWD_REDUCE)
     yield request.param
-    bsa.set_bwd_path(bsa.BWD_AUTO)
+    bsa.set_bwd_path(bsa.BWD_REDUCE)
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -127,7 +127,7 @@ def test_attention_parity(case, bwd_path):
     torch.cuda.synchronize()
     dQr, dKr, dVr = orc.attn_bwd(og, r, host[0][0], host[1][0], host[2][0], dO.cpu()[0], kt, dn, qn, qi,
                                  float(np.float32(scale)))
-    tag = name if bwd_path == "auto" else name + "/reduce"
+    tag = name if bwd_path == "reduce" else name + "/ds"
     assert_close("dV", dV[0], dVr, case=tag)
     assert_close("dK", dK[0], dKr, case=tag)
     assert_close("dQ", dQ[0], dQr, case=tag)
