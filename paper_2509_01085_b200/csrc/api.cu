@@ -201,8 +201,11 @@ BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   w.qoff = w.ctr + align256(BH * 4);  // work counters of the main kernel (one per launch, <= B <= BH)
   w.ptot = w.qoff + align256(BH * g.N * 4);
   w.slot = w.ptot + align256((BH + 1) * 4);  // per-head pair counts, then the total
-  w.ds = w.slot + align256(BH * g.N * static_cast<size_t>(g.N) * 4);
-  w.cap = ds_capacity(g, BH, SR);
+  const bool ds = g_bwd_path.load() == BSA_BWD_DS;
+  w.ds = w.slot + (ds ? align256(BH * g.N * static_cast<size_t>(g.N) * 4) : 0);
+  // the dS region only under BSA_BWD_DS (24 GiB at the 147k workload otherwise allocated for nothing): a layer
+  // must be built after bsa_set_bwd_path; a too-small workspace is rejected by bsa_attn_bwd
+  w.cap = ds ? ds_capacity(g, BH, SR) : 0;
   w.total = w.ds + align256(static_cast<size_t>(w.cap) * SR * 128);
   return w;
 }

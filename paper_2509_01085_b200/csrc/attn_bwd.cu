@@ -789,20 +789,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         (void)any;
         continue;
 #endif
-#ifdef BSA_DQ_EARLY_RELEASE
-        // the whole partial row (D fp32) goes to registers first, so the TMEM buffer is handed back to the
-        // next dQ MMA at once; staging and reduce-adds then run from registers
-        float vall[D];
-#pragma unroll
-        for (int cs = 0; cs < D; cs += 16)
-          tmem_ld16(tdQ + qbuf * D + (static_cast<uint32_t>(q4 * 32) << 16) + cs, vall + cs);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&bar_dq_free[qbuf]);
-#pragma unroll
-        for (int cs = 0; cs < D; cs += 32) {
-          const float* v = vall + cs;
-#else
 #pragma unroll 1
         for (int cs = 0; cs < D; cs += 32) {
           float v[32];
@@ -814,7 +800,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             tc_fence_before();
             mbar_arrive(&bar_dq_free[qbuf]);
           }
-#endif
           if (any) {
             const int s_first = slot_i;
             slot_i = (slot_i + SPS) % NSL;
