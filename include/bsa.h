@@ -209,6 +209,15 @@ enum bsa_sp_mode {
 };
 int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int32_t P, const void* src, void* dst,
                     void* stream);
+/* Head-group variant of the token-major exchange (B = 1), used to pipeline the exchange of head group g+1 with
+ * the attention of group g: each rank's chunk carries heads [p Hp + hoff, p Hp + hoff + Hs) of its destination p
+ * (Hp = Hh/P, 0 <= hoff, hoff + Hs <= Hp):
+ *   BSA_SP_GROUP_SEND  src [Ls][Hh][d]                      -> dst [P][Ls][Hs][d]
+ *   BSA_SP_GROUP_RECV  src [P][Ls][Hs][d]                   -> dst [Ls][Hh][d], only those heads written
+ * Errors as bsa_sp_relayout; a group outside [0, Hp) is BSA_ERR_CONFIG. */
+enum bsa_sp_group_mode { BSA_SP_GROUP_SEND = 0, BSA_SP_GROUP_RECV = 1 };
+int bsa_sp_relayout_group(int mode, int32_t Ls, int32_t Hh, int32_t d, int32_t P, int32_t hoff, int32_t Hs,
+                          const void* src, void* dst, void* stream);
 
 /* ---------------------------------------------------------------- instrumentation (off the hot path)
  * Kernel ids reported by bsa_timing_read / counted by bsa_launch_count. */

@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         L.bsa_attn_bwd.argtypes = [gp, _D, _I, _I, _I, _T, _T, _T, _T, _T, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F,
                                    _T, _T, _T, _P, _S, _P]
         L.bsa_sp_relayout.argtypes = [_I, _I, _I, _I, _I, _I, _P, _P, _P]
+        L.bsa_sp_relayout_group.argtypes = [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P]
         L.bsa_select_kv_blocks_ex.argtypes = [gp, _I, _I, _I, _T, _P, _T, _I, _D, _I, _P, _P, _P, _P, _P, _P, _S, _P]
         L.bsa_resolve_k.argtypes = [_D, _I, _P]
         L.bsa_kv_quantile.argtypes = [_I, _I, _P]
@@ -116,7 +117,8 @@ def lib() -> ctypes.CDLL:
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
-                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path", "bsa_bwd_ds_capacity"):
+                  "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path", "bsa_bwd_ds_capacity",
+                  "bsa_sp_relayout_group"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -323,6 +325,23 @@ def bsa_sp_relayout(mode: int, src: torch.Tensor, dst: torch.Tensor, B: int, Ls:
     if src.numel() != B * Ls * Hh * d or dst.numel() != src.numel():
         raise BSAError("bsa_sp_relayout: src/dst must hold B*Ls*Hh*d elements")
     _check(lib().bsa_sp_relayout(mode, B, Ls, Hh, d, P, _ptr(src), _ptr(dst), _stream(src.device)), "bsa_sp_relayout")
+    return dst
+
+
+SP_GROUP_SEND, SP_GROUP_RECV = 0, 1
+
+
+def bsa_sp_relayout_group(mode: int, src: torch.Tensor, dst: torch.Tensor, Ls: int, Hh: int, d: int, P: int,
+                          hoff: int, Hs: int):
+    """Head-group token-major reorder (include/bsa.h, bsa_sp_relayout_group); writes dst."""
+    _need_cuda(src, dst)
+    if src.dtype != torch.bfloat16 or dst.dtype != torch.bfloat16 or not src.is_contiguous() or not dst.is_contiguous():
+        raise BSAError("bsa_sp_relayout_group: src and dst must be contiguous bf16")
+    big, small = Ls * Hh * d, P * Ls * Hs * d
+    if (src.numel(), dst.numel()) != ((big, small) if mode == SP_GROUP_SEND else (small, big)):
+        raise BSAError("bsa_sp_relayout_group: src/dst sizes do not match the mode")
+    _check(lib().bsa_sp_relayout_group(mode, Ls, Hh, d, P, hoff, Hs, _ptr(src), _ptr(dst), _stream(src.device)),
+           "bsa_sp_relayout_group")
     return dst
 
 

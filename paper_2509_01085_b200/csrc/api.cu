@@ -601,6 +601,25 @@ int bsa_sp_relayout(int mode, int32_t B, int32_t Ls, int32_t Hh, int32_t d, int3
   return BSA_OK;
 }
 
+int bsa_sp_relayout_group(int mode, int32_t Ls, int32_t Hh, int32_t d, int32_t P, int32_t hoff, int32_t Hs,
+                          const void* src, void* dst, void* stream) {
+  if (Ls < 1 || Hh < 1 || P < 1) return fail(BSA_ERR_INVALID_SHAPE, "Ls, Hh, P must be >= 1");
+  if (d < 8 || d % 8) return fail(BSA_ERR_INVALID_SHAPE, "d must be a positive multiple of 8 (got %d)", d);
+  if (Hh % P) return fail(BSA_ERR_CONFIG, "Hh = %d heads do not split over P = %d ranks", Hh, P);
+  if (hoff < 0 || Hs < 1 || hoff + Hs > Hh / P)
+    return fail(BSA_ERR_CONFIG, "head group [%d, %d) outside the %d heads of a rank", hoff, hoff + Hs, Hh / P);
+  if (mode != BSA_SP_GROUP_SEND && mode != BSA_SP_GROUP_RECV) return fail(BSA_ERR_CONFIG, "unknown mode %d", mode);
+  if (!src || !dst || !aligned16(src) || !aligned16(dst))
+    return fail(BSA_ERR_INVALID_SHAPE, "src/dst must be non-NULL and 16-byte aligned");
+  CHECK(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = timed(BSA_K_SP_RELAYOUT, 1, st, [&] {
+    return bsa::launch_sp_group(mode == BSA_SP_GROUP_SEND ? 0 : 1, Ls, Hh, d, P, hoff, Hs, src, dst, st);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "sp_relayout_group");
+  return BSA_OK;
+}
+
 // Debug aid (not in bsa.h): per-step timeline of one forward CTA, see attn_fwd.cu FWD_TRACE.
 int bsa_debug_trace_fwd(void* dev_buf, int cta) {
   cudaError_t e = bsa::debug_trace_fwd(dev_buf, cta);

@@ -75,6 +75,8 @@ cudaError_t launch_group(int N, int BH, int G, const int* q2k_num, const int* q2
                          cudaStream_t st);
 
 // Ulysses sequence parallelism: row reorders around the all-to-all (sp.cu)
+cudaError_t launch_sp_group(int mode, int Ls, int Hh, int d, int P, int hoff, int Hs, const void* src, void* dst,
+                            cudaStream_t st);
 cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, const void* src, void* dst,
                                cudaStream_t st);
 

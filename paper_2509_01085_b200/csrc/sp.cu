@@ -74,6 +74,40 @@ __global__ void __launch_bounds__(256) k_sp_relayout(int B, int Ls, int Hh, int 
   dst[row * vpr + c] = src[srow * vpr + c];
 }
 
+// Head-group token-major exchange (B = 1 pipelining, ulysses.py head_groups): each rank's chunk carries only
+// heads [p Hp + hoff, p Hp + hoff + Hs) of head group p, so a sub-group can be exchanged and attended while the
+// next one is in flight.
+//   GROUP_SEND (0)  dst [P][Ls][Hs][d]  <-  src [Ls][Hh][d] heads p Hp + hoff + h
+//   GROUP_RECV (1)  dst [Ls][Hh][d] heads p Hp + hoff + h  <-  src [P][Ls][Hs][d]   (other heads untouched)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_sp_group(int Ls, int Hh, int P, int hoff, int Hs, int vpr,
+                                                  const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                  size_t total) {
+  const size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= total) return;
+  const size_t row = v / vpr;  // enumerates [P][Ls][Hs]
+  const int c = static_cast<int>(v % vpr);
+  const int h = static_cast<int>(row % Hs);
+  const size_t t = row / Hs;
+  const int l = static_cast<int>(t % Ls), p = static_cast<int>(t / Ls);
+  const size_t mrow = static_cast<size_t>(l) * Hh + static_cast<size_t>(p) * (Hh / P) + hoff + h;  // [Ls][Hh]
+  if (MODE == 0) dst[row * vpr + c] = src[mrow * vpr + c];
+  else dst[mrow * vpr + c] = src[row * vpr + c];
+}
+
+cudaError_t launch_sp_group(int mode, int Ls, int Hh, int d, int P, int hoff, int Hs, const void* src, void* dst,
+                            cudaStream_t st) {
+  const int vpr = d / 8;
+  const size_t total = static_cast<size_t>(P) * Ls * Hs * vpr;
+  if (total == 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+  const uint4* s = static_cast<const uint4*>(src);
+  uint4* o = static_cast<uint4*>(dst);
+  if (mode == 0) k_sp_group<0><<<blocks, 256, 0, st>>>(Ls, Hh, P, hoff, Hs, vpr, s, o, total);
+  else k_sp_group<1><<<blocks, 256, 0, st>>>(Ls, Hh, P, hoff, Hs, vpr, s, o, total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sp_relayout(int mode, int B, int Ls, int Hh, int d, int P, const void* src, void* dst,
                                cudaStream_t st) {
   const int vpr = d / 8;  // 16-byte vectors per row of d bf16

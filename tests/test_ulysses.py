@@ -19,8 +19,9 @@ import torch.multiprocessing as mp
 
 import bsa_gen
 import oracle as orc
-from paper_2509_01085_b200 import (SP_HEADS_TO_SEND, SP_RECV_T_TO_SEQ, SP_RECV_TO_HEADS, SP_RECV_TO_SEQ,
-                                   SP_SEQ_TO_SEND, SP_SEQ_TO_SEND_T, Geometry, resolve_k)
+from paper_2509_01085_b200 import (SP_GROUP_RECV, SP_GROUP_SEND, SP_HEADS_TO_SEND, SP_RECV_T_TO_SEQ,
+                                   SP_RECV_TO_HEADS, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND, SP_SEQ_TO_SEND_T, Geometry,
+                                   resolve_k)
 
 
 def ref_relayout(mode, src, dst, B, Ls, Hh, d, P):
@@ -145,15 +146,28 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def ref_relayout_group(mode, src, dst, Ls, Hh, d, P, hoff, Hs):
+    """Independent statement of include/bsa.h's bsa_sp_relayout_group (token-major head sub-group)."""
+    Hp = Hh // P
+    if mode == SP_GROUP_SEND:  # [Ls][Hh][d] heads p Hp + hoff + h -> [P][Ls][Hs][d]
+        dst.view(-1).copy_(src.reshape(Ls, P, Hp, d)[:, :, hoff:hoff + Hs].permute(1, 0, 2, 3).reshape(-1))
+    else:                      # [P][Ls][Hs][d] -> those heads of [Ls][Hh][d]
+        dst.view(Ls, P, Hp, d)[:, :, hoff:hoff + Hs] = src.reshape(P, Ls, Hs, d).permute(1, 0, 2, 3)
+    return dst
+
+
+def _worker(rank, world, port, out, head_groups=1):
     from paper_2509_01085_b200.ulysses import UlyssesBSA
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         og = orc.Geom(*GRID, *BLOCK)
         N = orc.sizes(og, R)[0]
         layer = OracleLayer(og, R, resolve_k(F, N), TAU, D)
-        u = UlyssesBSA(Geometry(*GRID, *BLOCK), R, F, TAU, 1, HH, D, device="cpu", attention=layer,
-                       relayout=ref_relayout, dtype=torch.float64)
+        make = lambda n: OracleLayer(og, R, resolve_k(F, N), TAU, D)  # noqa: E731
+        u = UlyssesBSA(Geometry(*GRID, *BLOCK), R, F, TAU, 1, HH, D, device="cpu",
+                       attention=None if head_groups > 1 else layer, relayout=ref_relayout, dtype=torch.float64,
+                       head_groups=head_groups, make_attention=make, group_relayout=ref_relayout_group)
+        assert (len(u.groups) == min(head_groups, HH // world)) if head_groups > 1 else not u.groups
         Q, K, V, dO = _inputs()
         L = Q.shape[2]
         Ls = L // world
@@ -165,12 +179,15 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_ulysses_gloo_two_ranks_equals_single_process_oracle():
+@pytest.mark.parametrize("head_groups", [1, 2])
+def test_ulysses_gloo_two_ranks_equals_single_process_oracle(head_groups):
+    """Two gloo ranks, plain (one exchange per tensor) and head-group pipelined (two sub-groups of one head per
+    rank, exchanged, attended and returned one after another), against the single-process oracle."""
     world = 2
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, out, head_groups), nprocs=world, join=True)
         res = dict(out)
     Q, K, V, dO = _inputs()
     og = orc.Geom(*GRID, *BLOCK)
@@ -248,3 +265,23 @@ def test_ulysses_emulated_ranks_match_single_layer(P):
         got = torch.cat(seq, dim=1).permute(0, 2, 1, 3)  # [B, Hh, L, d]
         torch.cuda.synchronize()
         assert_close(name, got[0], ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Ls,Hh,d,P,hoff,Hs", [(96, 8, 128, 2, 0, 2), (96, 8, 128, 2, 2, 2), (33, 15, 64, 3, 1, 3),
+                                               (40, 40, 128, 8, 3, 2)])
+def test_sp_relayout_group_kernels_match_reference(Ls, Hh, d, P, hoff, Hs):
+    import paper_2509_01085_b200 as bsa
+    g = torch.Generator().manual_seed(7)
+    x = torch.randn(Ls, Hh, d, generator=g).to(torch.bfloat16).cuda()
+    got = torch.full((P * Ls * Hs * d,), float("nan"), dtype=torch.bfloat16, device="cuda")
+    bsa.bsa_sp_relayout_group(SP_GROUP_SEND, x, got, Ls, Hh, d, P, hoff, Hs)
+    want = torch.empty_like(got)
+    ref_relayout_group(SP_GROUP_SEND, x, want, Ls, Hh, d, P, hoff, Hs)
+    assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+    back = torch.zeros(Ls * Hh * d, dtype=torch.bfloat16, device="cuda")
+    bsa.bsa_sp_relayout_group(SP_GROUP_RECV, got, back, Ls, Hh, d, P, hoff, Hs)
+    ref = torch.zeros_like(back)
+    ref_relayout_group(SP_GROUP_RECV, want, ref, Ls, Hh, d, P, hoff, Hs)
+    torch.cuda.synchronize()
+    assert torch.equal(back.view(torch.int16), ref.view(torch.int16))
