@@ -870,6 +870,33 @@ __device__ __forceinline__ void warp_bitonic(double* cs, int* cj, int lane) {
     cj[e * 32 + lane] = j[e];
   }
 }
+// The same sort over the warp's shared slice (P = 256, 512): a lane-strided compare-exchange loop per stage.
+// Fully unrolled register versions of these sizes (45 stages x 16 elements at P = 512) made the kernel's code
+// larger than the instruction cache (ncu at 147k: 64% of the stall samples "no instruction", 8.1 ms).
+__device__ __forceinline__ void smem_bitonic(double* cs, int* cj, int P, int lane) {
+#pragma unroll 1
+  for (int sz = 2; sz <= P; sz <<= 1) {
+#pragma unroll 1
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+#pragma unroll 4
+      for (int t = lane; t < P; t += 32) {
+        const int u = t ^ st;
+        if (u > t) {
+          const double a = cs[t], b = cs[u];
+          const int ja = cj[t], jb = cj[u];
+          const bool up = (t & sz) == 0;
+          if (up ? before(b, jb, a, ja) : before(a, ja, b, jb)) {
+            cs[t] = b;
+            cs[u] = a;
+            cj[t] = jb;
+            cj[u] = ja;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
 constexpr int ADMIT_WARPS = 8;
 
 __device__ __forceinline__ double warp_sum_bcast(double v) {
@@ -967,8 +994,7 @@ __global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const
         case 32: warp_bitonic<1>(cs, cj, lane); break;
         case 64: warp_bitonic<2>(cs, cj, lane); break;
         case 128: warp_bitonic<4>(cs, cj, lane); break;
-        case 256: warp_bitonic<8>(cs, cj, lane); break;
-        default: warp_bitonic<16>(cs, cj, lane); break;
+        default: smem_bitonic(cs, cj, P, lane); break;
       }
       __syncwarp();
       const double m = cs[0];
