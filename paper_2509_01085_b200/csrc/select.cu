@@ -946,20 +946,29 @@ __global__ void __launch_bounds__(256) k_admit_warp(int N, int rows_total, const
     }
     const double sigma = sqrt(warp_sum_bcast((a0 + a1) + (a2 + a3)) / (double)N);
     const double p = mu + sigma * z;
-    // compaction (ascending j)
+    // compaction (ascending j); four 32-wide chunks per iteration with their loads issued together (the loop
+    // was a chain of dependent L2 round trips at N = 2640)
     int nc = 0;
     bool over = false;
-    for (int j0 = 0; j0 < N; j0 += 32) {
-      const int j = j0 + lane;
-      const double v = j < N ? __ldg(srow + j) : 0.0;
-      const bool c = j < N && v >= p;
-      const unsigned m = __ballot_sync(0xffffffffu, c);
-      const int pos = nc + __popc(m & ((1u << lane) - 1u));
-      if (c && pos < ADMIT_CAP) {
-        cs[pos] = v;
-        cj[pos] = j;
+    for (int j0 = 0; j0 < N; j0 += 128) {
+      double vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + 32 * q + lane;
+        vv[q] = j < N ? __ldg(srow + j) : 0.0;
       }
-      nc += __popc(m);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + 32 * q + lane;
+        const bool c = j < N && vv[q] >= p;
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        const int pos = nc + __popc(m & ((1u << lane) - 1u));
+        if (c && pos < ADMIT_CAP) {
+          cs[pos] = vv[q];
+          cj[pos] = j;
+        }
+        nc += __popc(m);
+      }
     }
     if (nc > ADMIT_CAP) over = true;
     if (over) {  // leave this row to the CTA fallback

@@ -208,3 +208,39 @@ def test_selection_rejects_more_than_4096_blocks():
         args += [ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, None, ctypes.c_void_p(16), 1 << 40, None]
         rc = getattr(L, fn)(*args)
         assert rc == 1 and b"4096" in L.bsa_last_error(), fn
+
+
+def test_bwd_path_switch_and_ds_capacity():
+    """bsa_set_bwd_path / bsa_bwd_ds_capacity (include/bsa.h): the reduce path is the default (capacity -1);
+    BSA_BWD_DS gives the dS capacity (a pair density of 1/8, at most 24 GiB of SR x 128-byte tiles) and a larger
+    backward workspace; an unknown mode is BSA_ERR_CONFIG."""
+    L = bsa.lib()
+    g = bsa.Geometry(21, 30, 52)
+    assert bsa.bwd_ds_capacity(g, 0.5, 1, 12, 128) == -1
+    ws_reduce = bsa.bsa_workspace_bytes(bsa.OP_ATTN_BWD, g, 0.5, 1, 12, 128)
+    try:
+        bsa.set_bwd_path(bsa.BWD_DS)
+        cap = bsa.bwd_ds_capacity(g, 0.5, 1, 12, 128)
+        N = 624
+        assert cap == 12 * N * ((N + 7) // 8)  # 1/8 density, far below the 24 GiB bound
+        ws_ds = bsa.bsa_workspace_bytes(bsa.OP_ATTN_BWD, g, 0.5, 1, 12, 128)
+        assert ws_ds >= ws_reduce + cap * 32 * 128 + 12 * N * N * 4  # dS tiles (SR = 32) + the pair-slot table
+        big = bsa.Geometry(41, 45, 80)  # 147k: capped by the 24 GiB bound
+        assert bsa.bwd_ds_capacity(big, 0.5, 1, 40, 128) == (24 << 30) // (32 * 128)
+    finally:
+        bsa.set_bwd_path(bsa.BWD_REDUCE)
+    assert L.bsa_set_bwd_path(7) == 2 and b"backward path" in L.bsa_last_error()
+
+
+def test_sp_relayout_group_validation():
+    """bsa_sp_relayout_group: a head group outside [0, Hh/P) or an unknown mode -> BSA_ERR_CONFIG, d not a
+    multiple of 8 or a misaligned buffer -> BSA_ERR_INVALID_SHAPE, all before any device access."""
+    L = bsa.lib()
+    a, b = ctypes.c_void_p(256), ctypes.c_void_p(512)
+    assert L.bsa_sp_relayout_group(0, 16, 8, 128, 2, 3, 2, a, b, None) == 2  # [3, 5) outside Hp = 4
+    assert b"head group" in L.bsa_last_error()
+    assert L.bsa_sp_relayout_group(0, 16, 8, 128, 2, 0, 0, a, b, None) == 2
+    assert L.bsa_sp_relayout_group(5, 16, 8, 128, 2, 0, 2, a, b, None) == 2
+    assert L.bsa_sp_relayout_group(0, 16, 8, 12, 2, 0, 2, a, b, None) == 1
+    assert L.bsa_sp_relayout_group(1, 16, 8, 128, 2, 0, 2, ctypes.c_void_p(258), b, None) == 1
+    assert L.bsa_sp_relayout_group(0, 16, 6, 128, 4, 0, 1, a, b, None) == 2  # heads do not split over P
