@@ -41,7 +41,8 @@ CONFIGS = {
     "long_147k": dict(grid=(41, 45, 80), block=(4, 4, 4), B=1, Hh=40, d=128, r=0.5, f=0.1, tau=0.9, kind="video"),
 }
 KERNEL_NAMES = ["partition", "select_queries", "pool", "scores", "admit", "k2q", "gather", "attn_fwd", "fill",
-                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image", "sp_relayout", "fwd_group", "bwd_pairs", "bwd_dq"]
+                "bwd_prep", "attn_bwd", "bwd_finalize", "kv_image", "sp_relayout", "fwd_group", "bwd_pairs", "bwd_dq",
+                "fwd_union"]
 SELECTION_IDS = range(0, 7)
 
 
@@ -347,7 +348,7 @@ def main():
     kernel_ms = {KERNEL_NAMES[i]: kms[i] / max(1, args.steps) for i in range(nk) if kcnt[i]}
     phases = {
         "selection_ms": sum(kms[i] for i in SELECTION_IDS) / args.steps,
-        "fwd_ms": (kms[7] + kms[8] + kms[12] + kms[14]) / args.steps,
+        "fwd_ms": (kms[7] + kms[8] + kms[12] + kms[14] + kms[17]) / args.steps,
         "bwd_ms": (kms[9] + kms[10] + kms[11] + kms[15] + kms[16]) / args.steps,
         "sp_relayout_ms": kms[13] / args.steps,
     }

@@ -224,7 +224,7 @@ int bsa_sp_relayout_group(int mode, int32_t Ls, int32_t Hh, int32_t d, int32_t P
 enum bsa_kernel_id {
   BSA_K_PARTITION = 0, BSA_K_SELECT_Q, BSA_K_POOL, BSA_K_SCORES, BSA_K_ADMIT, BSA_K_K2Q, BSA_K_GATHER,
   BSA_K_ATTN_FWD, BSA_K_FILL, BSA_K_BWD_PREP, BSA_K_ATTN_BWD, BSA_K_BWD_FINAL, BSA_K_KV_IMAGE, BSA_K_SP_RELAYOUT,
-  BSA_K_GROUP, BSA_K_BWD_PAIRS, BSA_K_BWD_DQ, BSA_K_COUNT
+  BSA_K_GROUP, BSA_K_BWD_PAIRS, BSA_K_BWD_DQ, BSA_K_FWD_UNION, BSA_K_COUNT
 };
 /* Backward dQ path (process-wide): BSA_BWD_REDUCE (default) always takes the reduce path; BSA_BWD_DS takes the
  * dS path whenever the selection's pairs fit (the device-side switch described at bsa_attn_bwd). The default is

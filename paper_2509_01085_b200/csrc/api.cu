@@ -1,6 +1,7 @@
 // api.cu — the extern "C" boundary of libbsa.so (declared and documented in include/bsa.h).
 // Validates every argument on the host, sizes workspaces, and enqueues the kernels of
 // select.cu / attn_fwd.cu / attn_bwd.cu on the caller's stream. Never allocates or synchronises.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -163,7 +164,7 @@ bool fwd_grouping() {
 // Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL) + the tile
 // grouping's scratch and tile table (G >= 2).
 struct FwdWs {
-  size_t kv, qs, grp, perm, total;
+  size_t kv, qs, grp, perm, ul, uc, total;
 };
 FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   FwdWs w;
@@ -172,7 +173,12 @@ FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   w.qs = w.kv + align256(BH * g.N * 2 * static_cast<size_t>(g.BT) * d * 2);
   w.grp = w.qs + align256(BH * Lq * d * 2);
   w.perm = w.grp + align256(G >= 2 ? bsa::group_ws_bytes(g.N, static_cast<int>(BH)) : 0);
-  w.total = w.perm + align256(G >= 2 ? BH * static_cast<size_t>(bsa::group_ntiles(g.N, G)) * G * 4 : 0);
+  w.ul = w.perm + align256(G >= 2 ? BH * static_cast<size_t>(bsa::group_ntiles(g.N, G)) * G * 4 : 0);
+  // union lists of the forward tiles (enough for the grouped tiling, which has the most tiles)
+  const size_t ntiles = G >= 2 ? std::max(static_cast<size_t>(bsa::group_ntiles(g.N, G)), static_cast<size_t>((g.N + G - 1) / G))
+                               : static_cast<size_t>(g.N);
+  w.uc = w.ul + align256(BH * ntiles * g.N * 4);
+  w.total = w.uc + align256(BH * ntiles * 4);
   return w;
 }
 
@@ -482,6 +488,10 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
     a.perm = perm;
     a.ntiles = bsa::group_ntiles(G.N, Gt);
   }
+  a.ulists = reinterpret_cast<uint32_t*>(base + w.ul);
+  a.ucount = reinterpret_cast<int*>(base + w.uc);
+  if (e == cudaSuccess)
+    e = timed(BSA_K_FWD_UNION, 1, st, [&] { return bsa::launch_fwd_union(a, a.ulists, a.ucount, st); });
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
   if (e == cudaSuccess) e = timed(BSA_K_FILL, 1, st, [&] { return bsa::launch_fill(a.BH, G.L, d, donor, a.O, st); });
   if (e != cudaSuccess) return cuda_fail(e, "attn_fwd");

@@ -59,6 +59,8 @@ struct FwdParams {
   const int* q2k_idx;
   const int* perm;   // [BH][ntiles][G] query block of each tile slot (-1 = empty), or NULL: tile t = blocks t G ..
   int ntiles;
+  const uint32_t* ulists;  // [BH][ntiles][N] union entries of each tile (k_fwd_union), ucount[BH][ntiles] of them
+  const int* ucount;
   float scale_log2;  // scale * log2(e)
   Rows O;            // raster output, strided
   float* lse;
@@ -77,10 +79,8 @@ struct FwdSmem {
   static constexpr int KV_BYTES = BT * D * 2;  // one K or V tile
   static constexpr int NCB = D / 64;            // 64-channel (128-byte) column blocks
   static constexpr int OFF_K = 0;               // stage s: K tile at OFF_K + 2 s KV_BYTES, V right after
-  static constexpr int OFF_BITS = OFF_K + FWD_STAGES * 2 * KV_BYTES;
-  static constexpr int BITS_BYTES = MAX_G * (MAX_N / 32) * 4;
-  static constexpr int OFF_ULIST = OFF_BITS + BITS_BYTES + 32 * 4;  // + union words
-  static constexpr int ULIST_BYTES = MAX_N * 2;
+  static constexpr int OFF_ULIST = OFF_K + FWD_STAGES * 2 * KV_BYTES;  // the tile's union entries (uint32)
+  static constexpr int ULIST_BYTES = MAX_N * 4;
   static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
   // TMEM columns: O of the even / odd steps [0, 2D), S double buffer, Q^s (packed bf16 pairs), P double
   // buffer (packed). Buffer b = step parity = softmax group.
@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm + SM::OFF_K;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(sm + SM::OFF_BITS);
-  uint16_t* ulist = reinterpret_cast<uint16_t*>(sm + SM::OFF_ULIST);
+  uint32_t* ulist = reinterpret_cast<uint32_t*>(sm + SM::OFF_ULIST);
 
   constexpr int NSB = 2;
   __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[NSB],
@@ -122,15 +121,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   __shared__ uint32_t s_tmem;
   __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
   __shared__ int s_clsn16[8];
-  __shared__ uint32_t s_uword[MAX_N / 32];  // union bitmap words and their exclusive popcount prefix
-  __shared__ int s_upre[MAX_N / 32];
-#ifdef BSA_FWD_INTERLEAVE
-  // union entries by the TMEM lane quadrant (= SM sub-partition) of their lowest admitting slot: word masks,
-  // their per-quadrant exclusive prefix and the per-quadrant totals
-  __shared__ uint32_t s_qw[4][MAX_N / 32];
-  __shared__ int s_qpre[4][MAX_N / 32];
-  __shared__ int s_qcnt[4];
-#endif
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
   // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
   // per-column index arithmetic (which, unrolled, bloated the softmax loop past the instruction cache).
@@ -140,7 +130,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, bh = blockIdx.y;
   const int G = p.G, SR = p.SR;
-  const int NW = (g.N + 31) >> 5;
 #ifdef BSA_TRACE
   // CTA g_fwd_trace_cta writes slots [0, 8K); with BSA_TRACE_GLOBALTIMER also CTA +1 into [8K, 16K)
   const int my_cta = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
@@ -182,7 +171,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     s_nk[tid] = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
     s_koff[tid] = qb >= 0 ? p.kept_off[qb] : 0;
   }
-  for (int w = tid; w < G * NW; w += FWD_THREADS) bits[w] = 0u;
   if (tid < 8) {
     s_clsmask[tid] = p.clsmask[tid];
     s_clsn16[tid] = p.clsn16[tid];
@@ -202,20 +190,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   } while (0)
 #endif
   FWD_CSTAMP(8);
-  // The slots' q2k lists are read now, concurrently with kept_off: thread group gi (FWD_THREADS / G
-  // threads) holds list entries t, t + per, ... of slot gi in registers (the row has N allocated entries,
-  // so reading past q2k_num is safe; only the first q2k_num are used below).
-  constexpr int QPF = 2;  // list entries prefetched per thread
-  const int per = FWD_THREADS / G, pgi = tid / per, pt = tid % per;
-  const int pqb = pgi < G ? slot_qb(pgi) : -1;
-  const size_t prow = static_cast<size_t>(bh) * g.N + (pqb >= 0 ? pqb : 0);
-  const int pnum = pqb >= 0 ? p.q2k_num[prow] : 0;
-  int pj[QPF];
-#pragma unroll
-  for (int e = 0; e < QPF; ++e) pj[e] = (pt + e * per < g.N) ? p.q2k_idx[prow * g.N + pt + e * per] : 0;
+  // The tile's union of admitted KV blocks (P:210 lists of its G query blocks) was built by k_fwd_union:
+  // entry = j | extent class << 12 (C23) | admitting-slot mask << 16. One count load, then one coalesced copy.
+  const size_t tix = static_cast<size_t>(bh) * p.ntiles + tile;
+  if (tid == 0) s_U = p.ucount[tix];
   __syncthreads();
   FWD_CSTAMP(9);
-  // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the union build;
+  // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the list copy;
   // written to TMEM after it (A operand of every S MMA)
   uint4 qrow[D / 8];
   if (warp < 4) {
@@ -225,112 +206,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #pragma unroll
     for (int e = 0; e < D / 8; ++e) qrow[e] = valid ? src[e] : make_uint4(0, 0, 0, 0);
   }
-  // admission bitmap of each slot (q2k lists). The G lists are read concurrently (thread group gi
-  // of FWD_THREADS / G threads per slot): one dependent global round trip instead of G.
-  if (pqb >= 0) {
-#pragma unroll
-    for (int e = 0; e < QPF; ++e)
-      if (pt + e * per < pnum) atomicOr(&bits[pgi * NW + (pj[e] >> 5)], 1u << (pj[e] & 31));
-    const int* idx = p.q2k_idx + prow * g.N;
-    for (int a = pt + QPF * per; a < pnum; a += per) {  // long lists (more than QPF per thread)
-      const int j = idx[a];
-      atomicOr(&bits[pgi * NW + (j >> 5)], 1u << (j & 31));
-    }
+  {
+    const uint32_t* src = p.ulists + tix * g.N;
+    for (int u = tid; u < s_U; u += FWD_THREADS) ulist[u] = __ldg(src + u);
   }
-  __syncthreads();
   FWD_CSTAMP(10);
-  // ascending union list in two parallel passes: warp 0 ORs the slots' bitmaps word by word (lane-parallel)
-  // and prefix-sums the word popcounts; then every warp emits whole words, lane b writing bit b's entry
-  // (entry = j | extent class << 12, N <= 4096; class bit 2/1/0 = ragged last block along t/h/w, C23)
-#ifndef BSA_FWD_INTERLEAVE
-  if (warp == 0) {
-    int carry = 0;
-    for (int w0 = 0; w0 < NW; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t v = 0u;
-      if (w < NW)
-        for (int gi = 0; gi < G; ++gi) v |= bits[gi * NW + w];
-      const int c = __popc(v);
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += a;
-      }
-      if (w < NW) {
-        s_uword[w] = v;
-        s_upre[w] = carry + incl - c;
-      }
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) s_U = carry;
-  }
-  __syncthreads();
-  for (int w = warp; w < NW; w += FWD_THREADS / 32) {
-    const uint32_t v = s_uword[w];
-    if ((v >> lane) & 1u) {
-      const int jj = w * 32 + lane;
-      const int bt = jj / (g.Nh * g.Nw), bhh = (jj / g.Nw) % g.Nh, bw = jj % g.Nw;
-      const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
-                      (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
-      ulist[s_upre[w] + __popc(v & ((1u << lane) - 1u))] = static_cast<uint16_t>(jj | (cls << 12));
-    }
-  }
-#else
-  // Interleaved union order: consecutive steps (handled by the two softmax groups, which share the four
-  // sub-partitions) go to blocks in different TMEM lane quadrants, so one sub-partition's MUFU does not take
-  // two admitted softmax steps in a row. Key of an entry = (rank within its quadrant class, quadrant).
-  if (warp == 0) {
-    int carry[4] = {0, 0, 0, 0};
-    for (int w0 = 0; w0 < NW; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t seen = 0u, mq[4] = {0u, 0u, 0u, 0u};
-      if (w < NW)
-        for (int gi = 0; gi < G; ++gi) {
-          const uint32_t b = bits[gi * NW + w];
-          mq[(gi * 4) / G] |= b & ~seen;
-          seen |= b;
-        }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = __popc(mq[q]);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int a = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += a;
-        }
-        if (w < NW) {
-          s_qw[q][w] = mq[q];
-          s_qpre[q][w] = carry[q] + incl - c;
-        }
-        carry[q] += __shfl_sync(0xffffffffu, incl, 31);
-      }
-    }
-    if (lane == 0) {
-      for (int q = 0; q < 4; ++q) s_qcnt[q] = carry[q];
-      s_U = carry[0] + carry[1] + carry[2] + carry[3];
-    }
-  }
-  __syncthreads();
-  for (int w = warp; w < NW; w += FWD_THREADS / 32) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t v = s_qw[q][w];
-      if ((v >> lane) & 1u) {
-        const int jj = w * 32 + lane;
-        const int bt = jj / (g.Nh * g.Nw), bhh = (jj / g.Nw) % g.Nh, bw = jj % g.Nw;
-        const int cls = (bt == g.Nt - 1 && g.T % g.ct ? 4 : 0) | (bhh == g.Nh - 1 && g.H % g.ch ? 2 : 0) |
-                        (bw == g.Nw - 1 && g.W % g.cw ? 1 : 0);
-        const int r = s_qpre[q][w] + __popc(v & ((1u << lane) - 1u));
-        int pos = 0;
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) pos += min_i(s_qcnt[q2], r + (q2 < q ? 1 : 0));
-        ulist[pos] = static_cast<uint16_t>(jj | (cls << 12));
-      }
-    }
-  }
-#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -347,7 +227,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   // instead of all streaming block 0, 1, 2, ... from the same L2 slices at once (order does not change
   // the result beyond fp32 summation order).
   const int rot = U > 0 ? static_cast<int>((static_cast<unsigned>(tile) * 2654435761u + bh * 40503u) % U) : 0;
-  auto entry_at = [&](int u) { int x = u + rot; return static_cast<int>(ulist[x >= U ? x - U : x]); };
+  auto entry_at = [&](int u) { int x = u + rot; return ulist[x >= U ? x - U : x]; };
   auto kv_at = [&](int u) { return entry_at(u) & 0xFFF; };
   constexpr uint32_t KV_BYTES = SM::KV_BYTES;
 
@@ -356,10 +236,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     if (lane == 0) {
       for (int u = 0; u < U; ++u) {
         int s = u % FWD_STAGES;
-        const int ent = entry_at(u);
+        const uint32_t ent = entry_at(u);
         // only the first n16 rows (the block's tokens, padded to the MMA's N step) of each of the image's
         // 2 NCB column tiles are read: one request for a whole block, one per column tile for a ragged one
-        const int n16 = s_clsn16[ent >> 12];
+        const int n16 = s_clsn16[(ent >> 12) & 7];
         mbar_wait(&bar_kv_empty[s], ((u / FWD_STAGES) & 1) ^ 1);
         mbar_expect_tx(&bar_kv_full[s], static_cast<uint32_t>(n16) * (4 * D));
         FWD_TRACE(0, u);
@@ -403,7 +283,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #endif
       for (int v = 0; v < U; ++v) {
         const int s = v % FWD_STAGES, sb = v & 1;
-        const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[entry_at(v) >> 12], 0, 0);  // N = n16 keys
+        const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[(entry_at(v) >> 12) & 7], 0, 0);  // N = n16 keys
         mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
         if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
         tc_fence_after();
@@ -424,7 +304,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     } else {
       for (int u = 0; u < U; ++u) {
         const int pb = u & 1, s = u % FWD_STAGES;
-        const int nkk = s_clsn16[entry_at(u) >> 12] / 16;  // K = n16 keys
+        const int nkk = s_clsn16[(entry_at(u) >> 12) & 7] / 16;  // K = n16 keys
         const uint32_t tPu = tP + pb * (BT / 2);
         mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
         FWD_TRACE(2, u);
@@ -467,7 +347,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const int gi = row / SR, lr = row % SR;
     const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
-    const uint32_t* mybits = bits + (gi < G ? gi : 0) * NW;
+    const int mybit = 16 + (gi < G ? gi : 0);  // this row's slot in an entry's admitting-slot mask
     const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0;
     if (group == 0) {
       // Q^s row (loaded in the prologue) -> TMEM (A operand of the S MMAs): bf16 pairs in memory order
@@ -494,12 +374,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     float m_run = -INFINITY, l_run = 0.f;
     for (int u = group; u < U; u += 2) {
       const int ph = (u >> 1) & 1;  // phase of this group's buffers
-      const int ent = entry_at(u), j = ent & 0xFFF, cls = ent >> 12;
+      const uint32_t ent = entry_at(u);
+      const int cls = (ent >> 12) & 7;
       // The softmax always covers all BT columns (columns past the block's n tokens are masked, so stale TMEM
       // values of a shorter S never leak): skipping the unused 16-column chunks of ragged blocks broke the
       // instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
       constexpr int n16 = BT;
-      const bool admit = valid && ((mybits[j >> 5] >> (j & 31)) & 1u);
+      const bool admit = valid && ((ent >> mybit) & 1u);
       const uint32_t tS = tS0, tP = tP0;
       mbar_wait(&bar_s_full[group], ph);
       if (row == 0) FWD_TRACE(4 + 8 * group, u);
@@ -678,6 +559,88 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 #endif
 }
 
+// Union pre-pass (one CTA per (tile, b,h)): the ascending union of the tile slots' admitted KV blocks (P:210
+// q2k lists), entry = j | extent class << 12 (bit 2/1/0: ragged last block along t/h/w, C23) | mask << 16 of the
+// slots that admitted j. Built here, in parallel for all tiles, so the attention CTA's prologue is one list copy.
+template <int MAXG>
+__global__ void __launch_bounds__(256) k_fwd_union(Geo g, int G, int ntiles, const int* __restrict__ perm,
+                                                   const int* __restrict__ q2k_num, const int* __restrict__ q2k_idx,
+                                                   uint32_t* __restrict__ ulists, int* __restrict__ ucount) {
+  extern __shared__ uint32_t ubits[];  // [G][NW] slot bitmaps
+  __shared__ int s_qb[MAXG];
+  __shared__ int s_upre[MAX_N / 32];
+  __shared__ int s_tot;
+  const int tile = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = (g.N + 31) >> 5;
+  if (tid < G) {
+    int qb;
+    if (perm) qb = perm[(static_cast<size_t>(bh) * ntiles + tile) * G + tid];
+    else qb = tile * G + tid < g.N ? tile * G + tid : -1;
+    s_qb[tid] = qb;
+  }
+  for (int w = tid; w < G * NW; w += 256) ubits[w] = 0u;
+  __syncthreads();
+  for (int gi = 0; gi < G; ++gi) {
+    const int qb = s_qb[gi];
+    if (qb < 0) continue;
+    const size_t row = static_cast<size_t>(bh) * g.N + qb;
+    const int num = q2k_num[row];
+    const int* idx = q2k_idx + row * g.N;
+    for (int a = tid; a < num; a += 256) {
+      const int j = idx[a];
+      atomicOr(&ubits[gi * NW + (j >> 5)], 1u << (j & 31));
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // word popcount prefix of the union
+    int carry = 0;
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t v = 0u;
+      if (w < NW)
+        for (int gi = 0; gi < G; ++gi) v |= ubits[gi * NW + w];
+      const int c = __popc(v);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += a;
+      }
+      if (w < NW) s_upre[w] = carry + incl - c;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_tot = carry;
+  }
+  __syncthreads();
+  const size_t tix = static_cast<size_t>(bh) * ntiles + tile;
+  uint32_t* out = ulists + tix * g.N;
+  for (int w = warp; w < NW; w += 8) {
+    uint32_t v = 0u, mask = 0u;
+    for (int gi = 0; gi < G; ++gi) {
+      const uint32_t b = ubits[gi * NW + w];
+      v |= b;
+      mask |= ((b >> lane) & 1u) << gi;
+    }
+    if ((v >> lane) & 1u) {
+      const int jj = w * 32 + lane;
+      const int bt = jj / (g.Nh * g.Nw), bhh = (jj / g.Nw) % g.Nh, bw = jj % g.Nw;
+      const uint32_t cls = (bt == g.Nt - 1 && g.T % g.ct ? 4u : 0u) | (bhh == g.Nh - 1 && g.H % g.ch ? 2u : 0u) |
+                           (bw == g.Nw - 1 && g.W % g.cw ? 1u : 0u);
+      out[s_upre[w] + __popc(v & ((1u << lane) - 1u))] = static_cast<uint32_t>(jj) | (cls << 12) | (mask << 16);
+    }
+  }
+  if (tid == 0) ucount[tix] = s_tot;
+}
+
+cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cudaStream_t st) {
+  const int G = 128 / a.SR;
+  const int ntiles = a.perm ? a.ntiles : (a.g.N + G - 1) / G;
+  const int NW = (a.g.N + 31) / 32;
+  k_fwd_union<MAX_G><<<dim3(ntiles, a.BH), 256, G * NW * 4, st>>>(a.g, G, ntiles, a.perm, a.q2k_num, a.q2k_idx,
+                                                                 ulists, ucount);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -764,7 +727,9 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.kv_img = a.kv_img;
   p.Qs = a.Qs;
   p.perm = a.perm;
-  p.ntiles = a.ntiles;
+  p.ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
+  p.ulists = a.ulists;
+  p.ucount = a.ucount;
   for (int cls = 0; cls < 8; ++cls) {  // key-validity mask per block-extent class (ragged last block per axis)
     const Geo& g = a.g;
     const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;

@@ -60,7 +60,10 @@ struct FwdArgs {
   const uint8_t* kv_img;  // workspace: K|V block images (launch_kv_image)
   const int* perm;        // [BH][ntiles][G] query blocks of each tile (launch_group), or NULL: consecutive blocks
   int ntiles;
+  uint32_t* ulists;       // workspace: [BH][ntiles][N] union entries per tile (launch_fwd_union)
+  int* ucount;            // workspace: [BH][ntiles] their counts
 };
+cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cudaStream_t st);
 cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
 cudaError_t debug_trace_fwd(void* dev_buf, int cta);

@@ -77,7 +77,7 @@ def main():
         lay = blk.attn._layer()
         fl = lay.flops()
         rec = {"step": step, "r": r, "k_frac": f, "k": lay.k, "tau": tau, "N": lay.N,
-               "selection_ms": sum(ms[i] for i in SELECTION_IDS), "fwd_ms": ms[7] + ms[8] + ms[12] + ms[14],
+               "selection_ms": sum(ms[i] for i in SELECTION_IDS), "fwd_ms": ms[7] + ms[8] + ms[12] + ms[14] + ms[17],
                "bwd_ms": ms[9] + ms[10] + ms[11] + ms[15] + ms[16], "step_ms": e0.elapsed_time(e1), "pair_density": fl["density"],
                "mean_admitted_blocks": lay.sparsity()["mean_admitted_blocks"], "loss": float(loss.item())}
         rec["attn_ms"] = rec["selection_ms"] + rec["fwd_ms"] + rec["bwd_ms"]
