@@ -164,7 +164,7 @@ bool fwd_grouping() {
 // Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL) + the tile
 // grouping's scratch and tile table (G >= 2).
 struct FwdWs {
-  size_t kv, qs, grp, perm, ul, uc, total;
+  size_t kv, qs, grp, perm, ul, uc, ctr, total;
 };
 FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   FwdWs w;
@@ -178,7 +178,8 @@ FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   const size_t ntiles = G >= 2 ? std::max(static_cast<size_t>(bsa::group_ntiles(g.N, G)), static_cast<size_t>((g.N + G - 1) / G))
                                : static_cast<size_t>(g.N);
   w.uc = w.ul + align256(BH * ntiles * g.N * 4);
-  w.total = w.uc + align256(BH * ntiles * 4);
+  w.ctr = w.uc + align256(BH * ntiles * 4);
+  w.total = w.ctr + 256;
   return w;
 }
 
@@ -490,6 +491,7 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   }
   a.ulists = reinterpret_cast<uint32_t*>(base + w.ul);
   a.ucount = reinterpret_cast<int*>(base + w.uc);
+  a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
   if (e == cudaSuccess)
     e = timed(BSA_K_FWD_UNION, 1, st, [&] { return bsa::launch_fwd_union(a, a.ulists, a.ucount, st); });
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });

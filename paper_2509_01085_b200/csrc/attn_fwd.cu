@@ -61,6 +61,8 @@ struct FwdParams {
   int ntiles;
   const uint32_t* ulists;  // [BH][ntiles][N] union entries of each tile (k_fwd_union), ucount[BH][ntiles] of them
   const int* ucount;
+  int* work_ctr;           // next unclaimed tile (zeroed before the launch; the CTAs are persistent)
+  int total_tiles;         // BH * ntiles
   float scale_log2;  // scale * log2(e)
   Rows O;            // raster output, strided
   float* lse;
@@ -70,18 +72,18 @@ struct FwdParams {
 };
 
 constexpr int FWD_THREADS = 384;
-constexpr int FWD_STAGES = 6;
+constexpr int FWD_STAGES = 6;  // K|V ring depth (5 when the two union lists of a large N need the room)
 constexpr int MAX_N = 4096;
 constexpr int MAX_G = 16;
 
-template <int D, int BT>
+template <int D, int BT, int FWD_STAGES = bsa::FWD_STAGES>
 struct FwdSmem {
   static constexpr int KV_BYTES = BT * D * 2;  // one K or V tile
   static constexpr int NCB = D / 64;            // 64-channel (128-byte) column blocks
   static constexpr int OFF_K = 0;               // stage s: K tile at OFF_K + 2 s KV_BYTES, V right after
-  static constexpr int OFF_ULIST = OFF_K + FWD_STAGES * 2 * KV_BYTES;  // the tile's union entries (uint32)
-  static constexpr int ULIST_BYTES = MAX_N * 4;
-  static constexpr int TOTAL = OFF_ULIST + ULIST_BYTES + 1024;  // + alignment slack
+  static constexpr int OFF_ULIST = OFF_K + FWD_STAGES * 2 * KV_BYTES;  // union entries (uint32) of 2 tiles
+  // dynamic shared memory for N KV blocks: the ring, two union lists of N entries, alignment slack
+  static constexpr int bytes(int N) { return OFF_ULIST + 2 * N * 4 + 1024; }
   // TMEM columns: O of the even / odd steps [0, 2D), S double buffer, Q^s (packed bf16 pairs), P double
   // buffer (packed). Buffer b = step parity = softmax group.
   static constexpr int T_O = 0, T_S = 2 * D, T_Q = 2 * D + 2 * BT, T_P = T_Q + D / 2;
@@ -106,20 +108,26 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-template <int D, int BT>
+// Persistent: one CTA per SM claims tiles (b,h, tile) from an atomic counter. Warp 8 (after the TMEM
+// allocation) prepares the NEXT tile -- slot query blocks, kept counts, its union list copied from k_fwd_union's
+// output -- into the other half of a double-buffered metadata area while the current tile runs, so a tile
+// costs its union steps plus the hand-over (Q^s of the next tile into TMEM, the epilogue of the last one),
+// not a CTA launch and prologue (round 2: 11.8 us of fixed cost per tile in the one-CTA-per-tile kernel).
+// Every role walks the same tile sequence with all barrier phases counted across tiles.
+template <int D, int BT, int FWD_STAGES>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_constant__ FwdParams p) {
-  using SM = FwdSmem<D, BT>;
+  using SM = FwdSmem<D, BT, FWD_STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm + SM::OFF_K;
-  uint32_t* ulist = reinterpret_cast<uint32_t*>(sm + SM::OFF_ULIST);
+  uint32_t* ulist0 = reinterpret_cast<uint32_t*>(sm + SM::OFF_ULIST);
 
-  constexpr int NSB = 2;
-  __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[NSB],
-      bar_s_free[NSB], bar_p_full[NSB], bar_p_free[2], bar_o_final;
+  __shared__ __align__(8) uint64_t bar_qt, bar_kv_full[FWD_STAGES], bar_kv_empty[FWD_STAGES], bar_s_full[2],
+      bar_s_free[2], bar_p_full[2], bar_p_free[2], bar_o_final, bar_o_free, bar_meta_full[2], bar_meta_free[2];
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
-  __shared__ int s_qb[MAX_G], s_nk[MAX_G], s_koff[MAX_G], s_U;
+  // per metadata buffer: claimed item (-1: no work left), slot query blocks / kept counts / kept offsets, U
+  __shared__ int s_item[2], s_U[2], s_qb[2][MAX_G], s_nk[2][MAX_G], s_koff[2][MAX_G];
   __shared__ int s_clsn16[8];
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
   // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
@@ -128,214 +136,183 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, bh = blockIdx.y;
   const int G = p.G, SR = p.SR;
-#ifdef BSA_TRACE
-  // CTA g_fwd_trace_cta writes slots [0, 8K); with BSA_TRACE_GLOBALTIMER also CTA +1 into [8K, 16K)
-  const int my_cta = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
-  unsigned long long* trace_buf = (my_cta == g_fwd_trace_cta) ? g_fwd_trace : nullptr;
-  // trace mode cta == -1: per-CTA [start, first S ready, last PV issued, end, smid, U] (globaltimer ns)
-  unsigned long long t_cta0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cta0));
-  if (g_fwd_trace_cta == -1) trace_buf = nullptr;
-#ifdef BSA_TRACE_GLOBALTIMER
-  if (my_cta == g_fwd_trace_cta + 1 && g_fwd_trace != nullptr) trace_buf = g_fwd_trace + 8 * 1024;
-#endif
-#endif
+  constexpr int W_ALLOC = 8, W_PROD = 9, W_PV = 10, W_QK = 11;
+  constexpr int META_READERS = 11;  // producer, PV issuer, QK issuer, 8 softmax warps
 
   if (tid == 0) {
     mbar_init(&bar_qt, 128);
     for (int s = 0; s < FWD_STAGES; ++s) { mbar_init(&bar_kv_full[s], 1); mbar_init(&bar_kv_empty[s], 1); }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_p_free[b], 1);
-    }
-    for (int b = 0; b < NSB; ++b) {
       mbar_init(&bar_s_full[b], 1);
       mbar_init(&bar_s_free[b], 128);
       mbar_init(&bar_p_full[b], 128);
+      mbar_init(&bar_meta_full[b], 1);
+      mbar_init(&bar_meta_free[b], META_READERS);
     }
     mbar_init(&bar_o_final, 1);
+    mbar_init(&bar_o_free, 256);
     fence_mbar_init();
   }
-  constexpr int W_ALLOC = 8, W_PROD = 9, W_PV = 10, W_QK = 11;
   if (warp == W_ALLOC) tmem_alloc(&s_tmem, SM::TMEM_COLS);
-  // query block of tile slot k (grouped tiles: group.cu; else consecutive blocks)
-  auto slot_qb = [&](int k) {
-    if (p.perm) return p.perm[(static_cast<size_t>(bh) * p.ntiles + tile) * G + k];
-    const int qb = tile * G + k;
-    return qb < g.N ? qb : -1;
-  };
-  if (tid < G) {
-    const int qb = slot_qb(tid);
-    s_qb[tid] = qb;
-    s_nk[tid] = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
-    s_koff[tid] = qb >= 0 ? p.kept_off[qb] : 0;
-  }
   if (tid < 8) {
     s_clsmask[tid] = p.clsmask[tid];
     s_clsn16[tid] = p.clsn16[tid];
   }
-#ifdef BSA_TRACE
-#define FWD_CSTAMP(k)                                                                   \
-  do {                                                                                  \
-    if (tid == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {                  \
-      unsigned long long _t;                                                            \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
-      g_fwd_trace[16 * static_cast<size_t>(my_cta) + (k)] = _t;                         \
-    }                                                                                   \
-  } while (0)
-#else
-#define FWD_CSTAMP(k) \
-  do {                \
-  } while (0)
-#endif
-  FWD_CSTAMP(8);
-  // The tile's union of admitted KV blocks (P:210 lists of its G query blocks) was built by k_fwd_union:
-  // entry = j | extent class << 12 (C23) | admitting-slot mask << 16. One count load, then one coalesced copy.
-  const size_t tix = static_cast<size_t>(bh) * p.ntiles + tile;
-  if (tid == 0) s_U = p.ucount[tix];
-  __syncthreads();
-  FWD_CSTAMP(9);
-  // Q^s rows of the softmax threads (thread == row), issued now so their latency overlaps the list copy;
-  // written to TMEM after it (A operand of every S MMA)
-  uint4 qrow[D / 8];
-  if (warp < 4) {
-    const int row = tid, gi = row / SR, lr = row % SR;
-    const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
-    const uint4* src = reinterpret_cast<const uint4*>(p.Qs + (valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0) * D);
-#pragma unroll
-    for (int e = 0; e < D / 8; ++e) qrow[e] = valid ? src[e] : make_uint4(0, 0, 0, 0);
-  }
-  {
-    const uint32_t* src = p.ulists + tix * g.N;
-    for (int u = tid; u < s_U; u += FWD_THREADS) ulist[u] = __ldg(src + u);
-  }
-  FWD_CSTAMP(10);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = s_tmem;
-  const int U = s_U;
-#ifdef BSA_TRACE
-  if (tid == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_fwd_trace[16 * static_cast<size_t>(my_cta) + 6] = t;  // union list built
-  }
-#endif
-  // Every role walks the union in the same rotated order: concurrent CTAs start at different KV blocks
-  // instead of all streaming block 0, 1, 2, ... from the same L2 slices at once (order does not change
-  // the result beyond fp32 summation order).
-  const int rot = U > 0 ? static_cast<int>((static_cast<unsigned>(tile) * 2654435761u + bh * 40503u) % U) : 0;
-  auto entry_at = [&](int u) { int x = u + rot; return ulist[x >= U ? x - U : x]; };
-  auto kv_at = [&](int u) { return entry_at(u) & 0xFFF; };
   constexpr uint32_t KV_BYTES = SM::KV_BYTES;
+  // tile `it` of this CTA: its metadata buffer, the claimed item (-1 = done) and its rotation of the union
+  // walk (concurrent CTAs start at different KV blocks instead of all streaming block 0, 1, 2, ... from the same
+  // L2 slices at once; order does not change the result beyond fp32 summation order)
+  auto wait_meta = [&](int it) {
+    mbar_wait(&bar_meta_full[it & 1], (it >> 1) & 1);
+    return s_item[it & 1];
+  };
+  auto release_meta = [&](int it) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar_meta_free[it & 1]);
+  };
+  auto rot_of = [&](int item, int U) {
+    const int bh = item / p.ntiles, tile = item - bh * p.ntiles;
+    return U > 0 ? static_cast<int>((static_cast<unsigned>(tile) * 2654435761u + bh * 40503u) % U) : 0;
+  };
 
-  if (warp == W_PROD) {
+  if (warp == W_ALLOC) {
+    // ============================ tile claimer / metadata preparation (one tile ahead)
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&bar_meta_free[b], ((it >> 1) - 1) & 1);  // every role is done with tile it - 2
+      int item = 0;
+      if (lane == 0) item = atomicAdd(p.work_ctr, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= p.total_tiles) item = -1;
+      if (item >= 0) {
+        const int bh = item / p.ntiles, tile = item - bh * p.ntiles;
+        if (lane < G) {
+          int qb;
+          if (p.perm) qb = p.perm[static_cast<size_t>(item) * G + lane];
+          else qb = tile * G + lane < g.N ? tile * G + lane : -1;
+          s_qb[b][lane] = qb;
+          s_nk[b][lane] = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
+          s_koff[b][lane] = qb >= 0 ? p.kept_off[qb] : 0;
+        }
+        const int U = p.ucount[item];
+        const uint32_t* src = p.ulists + static_cast<size_t>(item) * g.N;
+        uint32_t* dst = ulist0 + b * g.N;
+        for (int u = lane; u < U; u += 32) dst[u] = __ldg(src + u);
+        if (lane == 0) s_U[b] = U;
+        (void)bh;
+      }
+      if (lane == 0) s_item[b] = item;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_meta_full[b]);  // (release: the warp's smem writes above)
+      if (item < 0) break;
+    }
+  } else if (warp == W_PROD) {
     // ============================ bulk-copy producer
-    if (lane == 0) {
-      for (int u = 0; u < U; ++u) {
-        int s = u % FWD_STAGES;
-        const uint32_t ent = entry_at(u);
-        // only the first n16 rows (the block's tokens, padded to the MMA's N step) of each of the image's
-        // 2 NCB column tiles are read: one request for a whole block, one per column tile for a ragged one
-        const int n16 = s_clsn16[(ent >> 12) & 7];
-        mbar_wait(&bar_kv_empty[s], ((u / FWD_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&bar_kv_full[s], static_cast<uint32_t>(n16) * (4 * D));
-        FWD_TRACE(0, u);
-#ifndef BSA_ABLATE_FWD_HOTSET
-        const int j = ent & 0xFFF;
-#else
-        const int j = (u & 15);
-#endif
-        const uint8_t* src = p.kv_img + (static_cast<size_t>(bh) * g.N + j) * (2 * KV_BYTES);
-        if (n16 == BT) {
-          bulk_load(sK + s * 2 * KV_BYTES, src, 2 * KV_BYTES, &bar_kv_full[s]);
-        } else {
+    int gs = 0;  // K|V steps over all tiles (ring position and phase)
+    for (int it = 0;; ++it) {
+      const int item = wait_meta(it);
+      if (item < 0) break;
+      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / p.ntiles;
+      const uint32_t* ul = ulist0 + b * g.N;
+      if (lane == 0) {
+        for (int u = 0; u < U; ++u, ++gs) {
+          const int s = gs % FWD_STAGES;
+          const int x = u + rot;
+          const uint32_t ent = ul[x >= U ? x - U : x];
+          // only the first n16 rows (the block's tokens, padded to the MMA's N step) of each of the image's
+          // 2 NCB column tiles are read: one request for a whole block, one per column tile for a ragged one
+          const int n16 = s_clsn16[(ent >> 12) & 7];
+          mbar_wait(&bar_kv_empty[s], ((gs / FWD_STAGES) & 1) ^ 1);
+          mbar_expect_tx(&bar_kv_full[s], static_cast<uint32_t>(n16) * (4 * D));
+          const int j = ent & 0xFFF;
+          const uint8_t* src = p.kv_img + (static_cast<size_t>(bh) * g.N + j) * (2 * KV_BYTES);
+          if (n16 == BT) {
+            bulk_load(sK + s * 2 * KV_BYTES, src, 2 * KV_BYTES, &bar_kv_full[s]);
+          } else {
 #pragma unroll
-          for (int t = 0; t < 2 * SM::NCB; ++t)
-            bulk_load(sK + s * 2 * KV_BYTES + t * BT * 128, src + t * BT * 128, static_cast<uint32_t>(n16) * 128,
-                      &bar_kv_full[s]);
+            for (int t = 0; t < 2 * SM::NCB; ++t)
+              bulk_load(sK + s * 2 * KV_BYTES + t * BT * 128, src + t * BT * 128, static_cast<uint32_t>(n16) * 128,
+                        &bar_kv_full[s]);
+          }
         }
       }
+      gs = __shfl_sync(0xffffffffu, gs, 0);
+      release_meta(it);
     }
   } else if (warp == W_QK || warp == W_PV) {
     // ============================ MMA issuers. One tensor pipe, two issuing warps with plain blocking
     // (suspending) waits: W_QK issues S(v) = Q^s K_v^T as soon as its K tile landed and its S buffer is
     // free (v & 1 = softmax group), W_PV issues O_b += P(u) V_u as soon as P(u) is written. QK therefore
-    // runs ahead of PV by itself, and neither queue waits behind the other's dependencies. (A single
-    // issuer polling both queues needs a short suspend hint, which wakes ~0.3 us late on B200.) Each
-    // warp walks its schedule whole (uniform registers); one elected lane issues.
+    // runs ahead of PV by itself, and neither queue waits behind the other's dependencies. Each warp walks its
+    // schedule whole (uniform registers); one elected lane issues.
     const bool leader = elect_one();
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, D, 0, 1);
     const uint32_t tO = tbase + SM::T_O, tS = tbase + SM::T_S, tQ = tbase + SM::T_Q, tP = tbase + SM::T_P;
     // base descriptors; an operand at byte offset o from the base is base + (o >> 4)
     const uint64_t dK0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t dV0 = umma_desc_sw128(smem_u32(sK + KV_BYTES), BT * 128, 1024);
-    if (warp == W_QK) {
-      mbar_wait(&bar_qt, 0);  // Q^s is in TMEM
-#ifdef BSA_TRACE
-      if (lane == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 7] = t;  // Q^s in TMEM
-      }
-#endif
-      for (int v = 0; v < U; ++v) {
-        const int s = v % FWD_STAGES, sb = v & 1;
-        const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[(entry_at(v) >> 12) & 7], 0, 0);  // N = n16 keys
-        mbar_wait(&bar_kv_full[s], (v / FWD_STAGES) & 1);
-        if (v >= 2) mbar_wait(&bar_s_free[sb], ((v - 2) >> 1) & 1);
-        tc_fence_after();
-        const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
-        if (leader) {
+    int gs = 0;               // steps over all tiles (K|V ring position)
+    int nb[2] = {0, 0};       // uses of S buffer / P buffer b over all tiles
+    for (int it = 0;; ++it) {
+      const int item = wait_meta(it);
+      if (item < 0) break;
+      const int b = it & 1, U = s_U[b], rot = rot_of(item, U);
+      const uint32_t* ul = ulist0 + b * g.N;
+      auto entry_at = [&](int u) { int x = u + rot; return ul[x >= U ? x - U : x]; };
+      if (warp == W_QK) {
+        mbar_wait(&bar_qt, it & 1);  // Q^s of this tile is in TMEM
+        for (int v = 0; v < U; ++v, ++gs) {
+          const int s = gs % FWD_STAGES, sb = v & 1;
+          const uint32_t idesc_qk = umma_idesc_bf16(128, s_clsn16[(entry_at(v) >> 12) & 7], 0, 0);  // N = n16
+          mbar_wait(&bar_kv_full[s], (gs / FWD_STAGES) & 1);
+          if (nb[sb] > 0) mbar_wait(&bar_s_free[sb], (nb[sb] - 1) & 1);
+          tc_fence_after();
+          const uint64_t kst = dK0 + ((s * 2 * KV_BYTES) >> 4);
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const int cb = kk >> 2, ko = (kk & 3) * 32;
-#ifndef BSA_ABLATE_FWD_MMA
-            umma_ts(tS + sb * BT, tQ + kk * 8, kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
-#endif
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const int cb = kk >> 2, ko = (kk & 3) * 32;
+              umma_ts(tS + sb * BT, tQ + kk * 8, kst + ((cb * BT * 128 + ko) >> 4), idesc_qk, kk > 0);
+            }
+            umma_commit(&bar_s_full[sb]);
           }
-          umma_commit(&bar_s_full[sb]);
+          __syncwarp();
+          ++nb[sb];
         }
-        __syncwarp();
-        FWD_TRACE(1, v);
-      }
-    } else {
-      for (int u = 0; u < U; ++u) {
-        const int pb = u & 1, s = u % FWD_STAGES;
-        const int nkk = s_clsn16[(entry_at(u) >> 12) & 7] / 16;  // K = n16 keys
-        const uint32_t tPu = tP + pb * (BT / 2);
-        mbar_wait(&bar_p_full[pb], (u >> 1) & 1);
-        FWD_TRACE(2, u);
-        tc_fence_after();
-        const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
-        if (leader) {
+      } else {
+        for (int u = 0; u < U; ++u, ++gs) {
+          const int pb = u & 1, s = gs % FWD_STAGES;
+          const int nkk = s_clsn16[(entry_at(u) >> 12) & 7] / 16;  // K = n16 keys
+          const uint32_t tPu = tP + pb * (BT / 2);
+          mbar_wait(&bar_p_full[pb], nb[pb] & 1);
+          // the tile's first PV of each group overwrites O_b: the last tile's epilogue must have read it
+          if (u < 2 && it > 0) mbar_wait(&bar_o_free, (it - 1) & 1);
+          tc_fence_after();
+          const uint64_t vst = dV0 + ((s * 2 * KV_BYTES) >> 4);
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk) {
-            if (kk >= nkk) break;
-#ifndef BSA_ABLATE_FWD_MMA
-            umma_ts(tO + pb * D, tPu + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv,
-                    (u > 1 || kk > 0) ? 1u : 0u);
-#endif
+            for (int kk = 0; kk < BT / 16; ++kk) {
+              if (kk >= nkk) break;
+              umma_ts(tO + pb * D, tPu + kk * 8, vst + ((kk * 2048) >> 4), idesc_pv, (u > 1 || kk > 0) ? 1u : 0u);
+            }
+            // QK(u) (the other issuer) completed before P(u) could exist, so this commit covers every
+            // read of the stage
+            umma_commit(&bar_kv_empty[s]);
+            umma_commit(&bar_p_free[pb]);
           }
-          // QK(u) (the other issuer) completed before P(u) could exist, so this commit covers every
-          // read of the stage
-          umma_commit(&bar_kv_empty[s]);
-          umma_commit(&bar_p_free[pb]);
+          __syncwarp();
+          ++nb[pb];
         }
+        if (leader) umma_commit(&bar_o_final);  // completes once every PV of the tile has landed in TMEM
         __syncwarp();
-        FWD_TRACE(3, u);
       }
-#ifdef BSA_TRACE
-      if (leader && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 2] = t;
-      }
-#endif
-      if (leader) umma_commit(&bar_o_final);  // completes once every PV has landed in TMEM
-      __syncwarp();
+      release_meta(it);
     }
   } else if (warp < 8) {
     // ============================ softmax + epilogue: two groups of four warps. Group b = warp / 4 runs
@@ -345,218 +322,177 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     const int group = warp >> 2, q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const int gi = row / SR, lr = row % SR;
-    const bool valid = gi < G && s_qb[gi] >= 0 && lr < s_nk[gi];
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
     const int mybit = 16 + (gi < G ? gi : 0);  // this row's slot in an entry's admitting-slot mask
-    const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[gi] + lr : 0;
-    if (group == 0) {
-      // Q^s row (loaded in the prologue) -> TMEM (A operand of the S MMAs): bf16 pairs in memory order
-#pragma unroll
-      for (int c0 = 0; c0 < D / 2; c0 += 16) {
-        float w[16];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint4 v = qrow[c0 / 4 + e];
-          w[4 * e] = __uint_as_float(v.x);
-          w[4 * e + 1] = __uint_as_float(v.y);
-          w[4 * e + 2] = __uint_as_float(v.z);
-          w[4 * e + 3] = __uint_as_float(v.w);
-        }
-        tmem_st16(trow + SM::T_Q + c0, w);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bar_qt);
-    }
     const float sl2 = p.scale_log2;
-    const uint32_t tS0 = trow + SM::T_S + group * BT, tP0 = trow + SM::T_P + group * (BT / 2);
+    const uint32_t tS = trow + SM::T_S + group * BT, tP = trow + SM::T_P + group * (BT / 2);
     const uint32_t tO = trow + SM::T_O + group * D;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int u = group; u < U; u += 2) {
-      const int ph = (u >> 1) & 1;  // phase of this group's buffers
-      const uint32_t ent = entry_at(u);
-      const int cls = (ent >> 12) & 7;
-      // The softmax always covers all BT columns (columns past the block's n tokens are masked, so stale TMEM
-      // values of a shorter S never leak): skipping the unused 16-column chunks of ragged blocks broke the
-      // instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
-      constexpr int n16 = BT;
-      const bool admit = valid && ((ent >> mybit) & 1u);
-      const uint32_t tS = tS0, tP = tP0;
-      mbar_wait(&bar_s_full[group], ph);
-      if (row == 0) FWD_TRACE(4 + 8 * group, u);
-#ifdef BSA_TRACE
-      if (u == 0 && row == 0 && g_fwd_trace != nullptr && g_fwd_trace_cta == -1) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_fwd_trace[16 * static_cast<size_t>(my_cta) + 1] = t;
-      }
-#endif
-      tc_fence_after();
-      float sv[BT];
+    int ns = 0;  // this group's steps over all tiles (phases of its S / P buffers)
+    for (int it = 0;; ++it) {
+      const int item = wait_meta(it);
+      if (item < 0) break;
+      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / p.ntiles;
+      const uint32_t* ul = ulist0 + b * g.N;
+      auto entry_at = [&](int u) { int x = u + rot; return ul[x >= U ? x - U : x]; };
+      const bool valid = gi < G && s_qb[b][gi] >= 0 && lr < s_nk[b][gi];
+      const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[b][gi] + lr : 0;
+      if (group == 0) {
+        // Q^s row -> TMEM (A operand of the S MMAs): bf16 pairs in memory order. The last tile's QKs are all
+        // complete (its epilogue waited for every PV, each after its own S). (Loading the next tile's rows into
+        // registers before the epilogue spilled the softmax role: 496 bytes.)
+        uint4 qrow[D / 8];
+        const uint4* src = reinterpret_cast<const uint4*>(p.Qs + prow_idx * D);
 #pragma unroll
-      for (int c = 0; c < BT; c += 16) {
-        if (c < n16) {
-          tmem_ld16(tS + c, sv + c);
+        for (int e = 0; e < D / 8; ++e) qrow[e] = valid ? src[e] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c0 = 0; c0 < D / 2; c0 += 16) {
+          float w[16];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint4 v = qrow[c0 / 4 + e];
+            w[4 * e] = __uint_as_float(v.x);
+            w[4 * e + 1] = __uint_as_float(v.y);
+            w[4 * e + 2] = __uint_as_float(v.z);
+            w[4 * e + 3] = __uint_as_float(v.w);
+          }
+          tmem_st16(trow + SM::T_Q + c0, w);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar_qt);
+      }
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int u = group; u < U; u += 2, ++ns) {
+        const int ph = ns & 1;  // phase of this group's buffers
+        const uint32_t ent = entry_at(u);
+        const int cls = (ent >> 12) & 7;
+        // The softmax always covers all BT columns (columns past the block's n tokens are masked, so stale
+        // TMEM values of a shorter S never leak): skipping the unused 16-column chunks of ragged blocks broke
+        // the instruction scheduling of the exp loop (0.87 -> 0.99 ms); only the MMAs and copies use n16.
+        const bool admit = valid && ((ent >> mybit) & 1u);
+        mbar_wait(&bar_s_full[group], ph);
+        tc_fence_after();
+        float sv[BT];
+#pragma unroll
+        for (int c = 0; c < BT; c += 16) tmem_ld16(tS + c, sv + c);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bar_s_free[group]);
+        float alpha = 1.f;
+        bool need_rescale = false;
+        if (admit) {
+          // key validity (ragged edge blocks: only actual tokens, C23); raw scores, scale folded into ex2
+          if (cls != 0) {
+            const uint64_t km = s_clsmask[cls];
+            const uint32_t k0 = static_cast<uint32_t>(km), k1 = static_cast<uint32_t>(km >> 32);
+#pragma unroll
+            for (int c = 0; c < BT; ++c)
+              if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
+          }
+          // row max and row sum with independent partial accumulators: a single serial chain of BT dependent
+          // FMNMX/FADD would cost more than the MUFU work it waits on
+          float mp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < BT; ++c) mp[c & 3] = fmaxf(mp[c & 3], sv[c]);
+          float mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])) * sl2;
+          if (mx > m_run + 8.f) {  // conditional rescale: keep the stale max unless it grew by > 2^8
+            if (m_run != -INFINITY) { alpha = ex2(m_run - mx); need_rescale = true; }
+            l_run *= alpha;
+            m_run = mx;
+          }
+          // paired fp32 arithmetic (FFMA2 / FADD2): two columns per instruction for the scale-and-shift and
+          // the row sum (1.003 -> 0.992 ms at 32k)
+          float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_run, -m_run);
+#pragma unroll
+          for (int c = 0; c < BT; c += 2) {  // one column in four on the FMA pipe, the rest on the MUFU
+            const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+            sv[c] = ex2(x.x);
+            sv[c + 1] = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
+            sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(sv[c], sv[c + 1]));
+          }
+          l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) sv[c + e] = -INFINITY;
+          for (int c = 0; c < BT; ++c) sv[c] = 0.f;
         }
-      }
-      tmem_wait_ld();
-      if (row == 0) FWD_TRACE(6 + 8 * group, u);
-      tc_fence_before();
-      mbar_arrive(&bar_s_free[group]);
-      float alpha = 1.f;
-      bool need_rescale = false;
-#ifdef BSA_ABLATE_FWD_EXP
-      if (admit) {
+        // P buffer and O accumulator of this group are free once its previous PV completed
+        if (ns > 0) mbar_wait(&bar_p_free[group], ph ^ 1);
+        // O rescale in TMEM; warp-collective access
+        if (__any_sync(0xffffffffu, need_rescale)) {
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 16) {
+            float ov[16];
+            tmem_ld16(tO + c, ov);
+            tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < BT; ++c) sv[c] = 0.25f;
-        l_run += 1.f;
-        m_run = 0.f;
-      } else if (false) {
-#else
-      if (admit) {
-#endif
-        // key validity (ragged edge blocks: only actual tokens, C23); raw scores, scale folded into ex2
-        if (cls != 0) {
-          const uint64_t km = s_clsmask[cls];
-          const uint32_t k0 = static_cast<uint32_t>(km), k1 = static_cast<uint32_t>(km >> 32);
-#pragma unroll
-          for (int c = 0; c < BT; ++c)
-            if (!(((c < 32 ? k0 : k1) >> (c & 31)) & 1u)) sv[c] = -INFINITY;
-        }
-        // row max and row sum with independent partial accumulators: a single serial chain of BT dependent
-        // FMNMX/FADD would cost more than the MUFU work it waits on
-        float mp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < BT; ++c) mp[c & 3] = fmaxf(mp[c & 3], sv[c]);
-        float mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])) * sl2;
-#ifndef BSA_ABLATE_RESCALE
-        if (mx > m_run + 8.f) {  // conditional rescale: keep the stale max unless it grew by > 2^8
-#else
-        if (m_run == -INFINITY) {
-#endif
-          if (m_run != -INFINITY) { alpha = ex2(m_run - mx); need_rescale = true; }
-          l_run *= alpha;
-          m_run = mx;
-        }
-        // paired fp32 arithmetic (FFMA2 / FADD2): two columns per instruction for the scale-and-shift and
-        // the row sum (1.003 -> 0.992 ms at 32k)
-        float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_run, -m_run);
-#pragma unroll
-        for (int c0 = 0; c0 < BT; c0 += 16) {
-          if (c0 < n16) {
-#pragma unroll
-            for (int c = c0; c < c0 + 16; c += 2) {  // one column in four on the FMA pipe, the rest on the MUFU
-              const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
-              sv[c] = ex2(x.x);
-#ifndef BSA_POLY_MASK
-              sv[c + 1] = ((c + 1) & 3) == 3 ? ex2_poly(x.y) : ex2(x.y);
-#else
-              sv[c] = ((BSA_POLY_MASK >> (c & 7)) & 1) ? ex2_poly(x.x) : ex2(x.x);
-              sv[c + 1] = ((BSA_POLY_MASK >> ((c + 1) & 7)) & 1) ? ex2_poly(x.y) : ex2(x.y);
-#endif
-              sp2[(c >> 1) & 3] = __fadd2_rn(sp2[(c >> 1) & 3], make_float2(sv[c], sv[c + 1]));
-            }
-          } else {
-#pragma unroll
-            for (int c = c0; c < c0 + 16; ++c) sv[c] = 0.f;
+            for (int e = 0; e < 16; ++e) ov[e] *= alpha;
+            tmem_st16(tO + c, ov);
           }
         }
-        l_run += ((sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y)) + ((sp2[2].x + sp2[2].y) + (sp2[3].x + sp2[3].y));
-      } else {
+        // P row -> TMEM (bf16 pairs, the A operand of PV)
 #pragma unroll
-        for (int c = 0; c < BT; ++c) sv[c] = 0.f;
-      }
-      // P buffer and O accumulator of this group are free once PV(u-2) (its previous step) completed (with
-      // P over S, only an O rescale needs that)
-      if (u >= 2) mbar_wait(&bar_p_free[group], ph ^ 1);
-      if (row == 0) FWD_TRACE(7 + 8 * group, u);
-      // O rescale in TMEM; warp-collective access
-      if (__any_sync(0xffffffffu, need_rescale)) {
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D; c += 16) {
-          float ov[16];
-          tmem_ld16(tO + c, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) ov[e] *= alpha;
-          tmem_st16(tO + c, ov);
-        }
-      }
-      // P row -> TMEM (bf16 pairs, the A operand of PV)
-#pragma unroll
-      for (int c0 = 0; c0 < BT / 2; c0 += 16) {
-        if (2 * c0 < n16) {  // the PV MMA reads the first n16 keys only
+        for (int c0 = 0; c0 < BT / 2; c0 += 16) {
           float w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(pack_bf16(sv[2 * (c0 + e)], sv[2 * (c0 + e) + 1]));
           tmem_st16(tP + c0, w);
         }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar_p_full[group]);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bar_p_full[group]);
-      if (row == 0) FWD_TRACE(5 + 8 * group, u);
-    }
-    // epilogue: merge the two groups' (m, l, O), O^s = O / l scattered to the kept token's raster row,
-    // LSE in natural log. Group b writes output columns [b D/2, (b+1) D/2).
-    s_ml[group][0][row] = m_run;
-    s_ml[group][1][row] = l_run;
-    mbar_wait(&bar_o_final, 0);
-    tc_fence_after();
-    named_bar_sync(1, 256);
-    const float m0 = s_ml[0][0][row], l0 = s_ml[0][1][row], m1 = s_ml[1][0][row], l1 = s_ml[1][1][row];
-    const bool has1 = U > 1;  // the odd group ran at least one step (its O columns were written)
-    const float m = has1 ? fmaxf(m0, m1) : m0;
-    const float a0 = valid ? ex2(m0 - m) : 0.f, a1 = (valid && has1) ? ex2(m1 - m) : 0.f;
-    const float l = l0 * a0 + l1 * a1;
-    const float inv = valid ? 1.f / l : 0.f;
-    bf16* orow = nullptr;
-    if (valid) {
-      int tok = p.kept_tok[prow_idx];
-      orow = p.O.row(bh, tok);
-      if (group == 0) p.lse[prow_idx] = (m + log2f(l)) * 0.6931471805599453f;
-    }
-    const float s0 = a0 * inv, s1 = a1 * inv;
-#pragma unroll 1
-    for (int c = group * (D / 2); c < (group + 1) * (D / 2); c += 16) {
-      float o0[16], o1[16];
-      tmem_ld16(trow + SM::T_O + c, o0);
-      if (has1) tmem_ld16(trow + SM::T_O + D + c, o1);
-      tmem_wait_ld();
+      // group 0 issues the next tile's Q^s row loads now, so their latency overlaps this epilogue (its
+      // metadata was prepared during this tile)
+      // epilogue: merge the two groups' (m, l, O), O^s = O / l scattered to the kept token's raster row,
+      // LSE in natural log. Group b writes output columns [b D/2, (b+1) D/2).
+      s_ml[group][0][row] = m_run;
+      s_ml[group][1][row] = l_run;
+      mbar_wait(&bar_o_final, it & 1);
+      tc_fence_after();
+      named_bar_sync(1, 256);
+      const float m0 = s_ml[0][0][row], l0 = s_ml[0][1][row], m1 = s_ml[1][0][row], l1 = s_ml[1][1][row];
+      const bool has1 = U > 1;  // the odd group ran at least one step (its O columns were written)
+      const float m = has1 ? fmaxf(m0, m1) : m0;
+      const float a0 = valid ? ex2(m0 - m) : 0.f, a1 = (valid && has1) ? ex2(m1 - m) : 0.f;
+      const float l = l0 * a0 + l1 * a1;
+      const float inv = valid ? 1.f / l : 0.f;
+      bf16* orow = nullptr;
       if (valid) {
-        uint32_t w[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float x0 = has1 ? o0[2 * e] * s0 + o1[2 * e] * s1 : o0[2 * e] * s0;
-          const float x1 = has1 ? o0[2 * e + 1] * s0 + o1[2 * e + 1] * s1 : o0[2 * e + 1] * s0;
-          w[e] = pack_bf16(x0, x1);
-        }
-        *reinterpret_cast<uint4*>(orow + c) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+        const int tok = p.kept_tok[prow_idx];
+        orow = p.O.row(bh, tok);
+        if (group == 0) p.lse[prow_idx] = (m + log2f(l)) * 0.6931471805599453f;
       }
+      const float s0 = a0 * inv, s1 = a1 * inv;
+#pragma unroll 1
+      for (int c = group * (D / 2); c < (group + 1) * (D / 2); c += 16) {
+        float o0[16], o1[16];
+        tmem_ld16(trow + SM::T_O + c, o0);
+        if (has1) tmem_ld16(trow + SM::T_O + D + c, o1);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float x0 = has1 ? o0[2 * e] * s0 + o1[2 * e] * s1 : o0[2 * e] * s0;
+            const float x1 = has1 ? o0[2 * e + 1] * s0 + o1[2 * e + 1] * s1 : o0[2 * e + 1] * s0;
+            w[e] = pack_bf16(x0, x1);
+          }
+          *reinterpret_cast<uint4*>(orow + c) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_o_free);  // O read: the next tile's first PVs may overwrite it
+      named_bar_sync(1, 256);    // (s_ml is rewritten by the next tile's epilogue)
+      release_meta(it);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
-#ifdef BSA_TRACE
-  if (g_fwd_trace != nullptr && g_fwd_trace_cta == -1 && tid == 0) {
-    unsigned long long* e = g_fwd_trace + 16 * static_cast<size_t>(my_cta);
-    unsigned long long t1;
-    unsigned sm_id;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
-    e[0] = t_cta0;
-    e[3] = t1;
-    e[4] = sm_id;
-    e[5] = U;
-  }
-#endif
 }
 
 // Union pre-pass (one CTA per (tile, b,h)): the ascending union of the tile slots' admitted KV blocks (P:210
@@ -701,13 +637,25 @@ bool make_map_5d(CUtensorMap* m, const void* base, const Geo& g, int d, int head
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int D, int BT, int ST>
+static cudaError_t run_fwd_st(const FwdParams& p, int ntiles, int BH, cudaStream_t st) {
+  const int smem = FwdSmem<D, BT, ST>::bytes(p.g.N);
+  cudaError_t e = cudaFuncSetAttribute(k_attn_fwd<D, BT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p.work_ctr, 0, sizeof(int), st)) != cudaSuccess) return e;
+  const int total = ntiles * BH;
+  k_attn_fwd<D, BT, ST><<<dim3(static_cast<unsigned>(total < sms ? total : sms)), FWD_THREADS, smem, st>>>(p);  // persistent
+  return cudaGetLastError();
+}
+// six K|V stages when they fit next to the two union lists (N <= ~4000 at d = 128), else five
 template <int D, int BT>
 static cudaError_t run_fwd(const FwdParams& p, int ntiles, int BH, cudaStream_t st) {
-  constexpr int smem = FwdSmem<D, BT>::TOTAL;
-  cudaError_t e = cudaFuncSetAttribute(k_attn_fwd<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  k_attn_fwd<D, BT><<<dim3(ntiles, BH), FWD_THREADS, smem, st>>>(p);
-  return cudaGetLastError();
+  constexpr int kStatic = 4096;  // static shared memory of the kernel (< 3 KB) with margin
+  if (FwdSmem<D, BT, 6>::bytes(p.g.N) + kStatic <= 227 * 1024) return run_fwd_st<D, BT, 6>(p, ntiles, BH, st);
+  return run_fwd_st<D, BT, 5>(p, ntiles, BH, st);
 }
 
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
@@ -730,6 +678,8 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
   p.ulists = a.ulists;
   p.ucount = a.ucount;
+  p.work_ctr = a.work_ctr;
+  p.total_tiles = p.ntiles * a.BH;
   for (int cls = 0; cls < 8; ++cls) {  // key-validity mask per block-extent class (ragged last block per axis)
     const Geo& g = a.g;
     const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;

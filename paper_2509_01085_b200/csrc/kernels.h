@@ -62,6 +62,7 @@ struct FwdArgs {
   int ntiles;
   uint32_t* ulists;       // workspace: [BH][ntiles][N] union entries per tile (launch_fwd_union)
   int* ucount;            // workspace: [BH][ntiles] their counts
+  int* work_ctr;          // workspace: tile counter of the persistent forward
 };
 cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cudaStream_t st);
 cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st);
