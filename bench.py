@@ -225,7 +225,7 @@ def main():
     ap.add_argument("--unit", default=None, help="query-selection window ut,uh,uw (P:168; default = whole block)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dense-steps", type=int, default=3, help="steps of the own-dense path (0 = skip)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=16, help="e2e steps (pipelined H2D / compute / D2H; more steps amortise the pipeline fill)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="problem", choices=["problem", "heads", "ulysses"],
                     help="N>1: problem = one independent problem per rank (weak); heads = split the heads; "
