@@ -68,7 +68,7 @@ __device__ __forceinline__ float ex2b(float x) {
 // SR/8 groups of 8 rows; group q holds [Q^s d-half 0][Q^s d-half 1][dO^s d-half 0][dO^s d-half 1], each
 // 8 rows x 128 B with the 128-byte swizzle. Consecutive groups (also across the blocks stacked in a
 // chunk) are 2*NCB KB apart, so every UMMA operand over the chunk's 128 rows has a uniform stride.
-// Next to it, the block's row statistics lsed[(b,h,block)] = [LSE*log2(e) of its SR rows][D of its SR rows]
+// Next to it, the block's row statistics lsed[(b,h,block)] = [row][LSE*log2(e), D] for its SR rows
 // (one more bulk copy per block). Rows beyond the block's kept count are zero with LSE = +inf, D = 0, so
 // they contribute P = dS = 0.
 //
@@ -121,11 +121,11 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
     const uint32_t inrow = sw128_off(lr & 7, (ch0 & 63) >> 3) + (ch0 & 7) * 2;
     uint8_t* qdst = gbase + (ch0 >> 6) * 1024 + inrow;
     uint8_t* ddst = gbase + (NCB + (ch0 >> 6)) * 1024 + inrow;
-    float* ld = lsed + bi * 2 * SR + lr;
+    float* ld = lsed + bi * 2 * SR + 2 * lr;  // [row][LSE * log2 e, D]: a block prefix is one contiguous copy
     if (lr >= nk) {
       if (lane == 0) {
         ld[0] = INFINITY;
-        ld[SR] = 0.f;
+        ld[1] = 0.f;
       }
       if (PER == 4) {
         *reinterpret_cast<uint2*>(qdst) = make_uint2(0, 0);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
     for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
     if (lane == 0) {
       ld[0] = lse[prow] * 1.4426950408889634f;
-      ld[SR] = dsum;
+      ld[1] = dsum;
     }
     if (!ds) {
       float* dq = dQacc + prow * D + ch0;
@@ -233,12 +233,14 @@ struct BwdParams {
   const uint8_t* qdo_img;  // per query block Q^s|dO^s images (k_bwd_prep), SR*d*4 bytes each
   CUtensorMap mK;    // 5D block map
   CUtensorMap mV;
-  CUtensorMap mDQ;     // dQacc [BH*Lq, d] fp32, box {32, dq_rows}, 128B swizzle (bulk reduce-add target)
+  CUtensorMap mDQ;     // dQacc [BH*Lq, d] fp32, box {32 columns, 32 rows}, 128B swizzle (bulk reduce-add target)
+  CUtensorMap mDQh;    // the same with 16 and 8 rows per box (pieces of blocks that keep fewer rows)
+  CUtensorMap mDQq;
   CUtensorMap mdK;     // 5D block maps over the dK / dV outputs (TMA store of the finished block)
   CUtensorMap mdV;
   Geo g;
-  const float* lsed;   // per query block [LSE*log2e x SR][D x SR] (k_bwd_prep)
-  int Lq, SR, G, dq_rows;
+  const float* lsed;   // per query block [SR rows][LSE*log2e, D] (k_bwd_prep)
+  int Lq, SR, G;
   const int* kept_off;
   const int* k2q_num;
   const int* k2q_idx;
@@ -306,6 +308,12 @@ constexpr int ITEM_RING = 8;
 // readers of the item ring: S/dP issuer, gradient issuer, 4 softmax warps (+ 4 dQ drain warps on the reduce path)
 template <bool DS>
 __host__ __device__ constexpr int item_readers() { return DS ? 6 : 10; }
+// rows a query block with nk kept queries takes in a chunk: nk rounded up to a power of two >= 8 (<= SR)
+__device__ __forceinline__ int slot_size(int nk, int SR) {
+  int sz = 8;
+  while (sz < nk && sz < SR) sz <<= 1;
+  return sz;
+}
 
 template <int D, int BT, bool DS>
 __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_constant__ BwdParams p) {
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   uint8_t* sdS = sm + SM::OFF_DS;
   auto stage_q = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES; };  // Q^s d-half 0 of group 0
   auto stage_do = [&](int s) { return sm + SM::OFF_ST + s * SM::STAGE_BYTES + NCB * 1024; };
-  auto stage_ld = [&](int s) {  // lsed of the chunk's blocks: block gi at [gi * 2 SR, (gi + 1) * 2 SR)
+  auto stage_ld = [&](int s) {  // [LSE*log2e, D] of the chunk's 128 rows (row r at 2 r)
     return reinterpret_cast<float*>(sm + SM::OFF_ST + s * SM::STAGE_BYTES + 2 * SM::TILE_BYTES);
   };
 
@@ -334,7 +342,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
   // Chunk metadata ring (first packed row, kept count, block id of each slot; row -1 = empty slot), written
   // by the producer for chunk c into entry c & 3. Four deep: the producer rewrites an entry only after
   // the MMAs of chunk c-2 completed, by which time the softmax and drain warps are done with chunk c-4.
-  __shared__ int s_row0[4][BWD_MAX_G], s_nk[4][BWD_MAX_G];
+  // Chunk composition ring (entry c & 3 for chunk c, written by the producer): per query block e of the chunk its
+  // first packed row (dQacc row) s_row0 and kept count | chunk row offset << 8 in s_nk; s_cinfo = number of
+  // blocks | (last chunk of its KV block) << 8. Blocks are packed into the 128 rows by slot size (SR rounded
+  // down to what they keep: 32 / 16 / 8 rows at r = 0.5), first fit on 8-row-group boundaries.
+  __shared__ int s_row0[4][BWD_MAX_G], s_nk[4][BWD_MAX_G], s_cinfo[4];
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -426,44 +438,76 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int item = s_item[it % ITEM_RING];
       if (item < 0) break;
       const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
-      const int nq = nq_of(bh, j), nchunks = (nq + G - 1) / G, crot = rot_of(bh, j, nchunks);
-      if (nchunks == 0) continue;
+      const int nq = nq_of(bh, j);
+      if (nq == 0) continue;
       const int* qlist = p.k2q_idx + (static_cast<size_t>(bh) * g.N + j) * g.N;
-      for (int cl = 0; cl < nchunks; ++cl, ++c) {
-        const int s = c & 1;
-        const int cc = (cl + crot) % nchunks;
-        const int nb = min_i(G, nq - cc * G);
-        int row0 = -1, nk = 0, qbl = 0, slot = -1;
-        if (lane < nb) {  // metadata of this chunk's blocks, fetched in parallel before the stage frees
-          qbl = qlist[cc * G + lane];
-          if (DS) slot = p.k2q_slot[(static_cast<size_t>(bh) * g.N + j) * g.N + cc * G + lane];
-          int ko = p.kept_off[qbl];
-          nk = p.kept_off[qbl + 1] - ko;
-          row0 = bh * p.Lq + ko;
+      const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4);
+      // k2q[j] is consumed in order: lane l of the fetched window holds entry w0 + l (block, kept offset, count)
+      int t = 0, w0 = -64, wqb = 0, wko = 0, wnk = 0;
+      for (bool last = false; !last; ++c) {
+        const int s = c & 1, ring = c & 3;
+        // compose chunk c first (lane e holds its entry e), then wait for the stage and publish: the list reads
+        // overlap the wait
+        uint32_t used = 0u;  // 8-row groups of the chunk already taken
+        int ne = 0, e_qb = -1, e_roff = 0, e_sz = 0, e_t = 0, e_row0 = 0, e_nk = 0;
+        while (t < nq && ne < BWD_MAX_G) {
+          if (t >= w0 + 32) {  // next window of 32 list entries, fetched in parallel
+            w0 = t;
+            const int pos = t + lane;
+            if (pos < nq) {
+              wqb = qlist[pos];
+              wko = p.kept_off[wqb];
+              wnk = p.kept_off[wqb + 1] - wko;
+            }
+          }
+          const int l = t - w0;
+          const int nk = __shfl_sync(0xffffffffu, wnk, l);
+          const int sz = slot_size(nk, SR), ng = sz >> 3;
+          const uint32_t pat = (1u << ng) - 1u;
+          int o = 0;
+          while (o + ng <= 16 && (used & (pat << o))) o += ng;
+          if (o + ng > 16) break;  // no aligned room left: the chunk is full
+          used |= pat << o;
+          const int qb = __shfl_sync(0xffffffffu, wqb, l), ko = __shfl_sync(0xffffffffu, wko, l);
+          if (lane == ne) {
+            e_qb = qb;
+            e_roff = 8 * o;
+            e_sz = sz;
+            e_t = t;
+            e_row0 = bh * p.Lq + ko;
+            e_nk = nk;
+          }
+          ++ne;
+          ++t;
         }
+        last = t >= nq;
+        int e_slot = -1;
+        if (DS && e_qb >= 0) e_slot = p.k2q_slot[(static_cast<size_t>(bh) * g.N + j) * g.N + e_t];
         if (lane == 0) PROG(0, c * 4 + 0);
         bwait(&bar_c_empty[s], ((c >> 1) & 1) ^ 1);
         if (lane == 0) PROG(0, c * 4 + 1);
-        const int ring = c & 3;
-        if (lane < G) {
-          s_row0[ring][lane] = row0;
-          s_nk[ring][lane] = nk;
-          if (DS) reinterpret_cast<int*>(sm + SM::OFF_SLOT)[ring * 16 + lane] = slot;
+        if (lane < ne) {
+          s_row0[ring][lane] = e_row0;
+          s_nk[ring][lane] = e_nk | (e_roff << 8);
+          if (DS) reinterpret_cast<int*>(sm + SM::OFF_SLOT)[ring * 16 + lane] = e_slot;
         }
+        if (lane == 0) s_cinfo[ring] = ne | (last ? 256 : 0);
+        // per block: its first sz rows of the QdO image (8-row groups) and of the [LSE, D] row statistics
+        uint32_t bytes = e_qb >= 0 ? static_cast<uint32_t>(e_sz / 8) * SM::PG + 8u * e_sz : 0u;
+#pragma unroll
+        for (int x = 16; x > 0; x >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, x);
         __syncwarp();
-        const uint32_t blk_bytes = static_cast<uint32_t>(SR * D * 4), ld_bytes = static_cast<uint32_t>(SR * 8);
         if (lane == 0) {
-          mbar_expect_tx(&bar_c_full[s], nb * (blk_bytes + ld_bytes));
+          mbar_expect_tx(&bar_c_full[s], bytes);
           BWD_TRACE(0, c);
           if (c == 0) CTA_STAMP(11);
         }
-        for (int gi = 0; gi < nb; ++gi) {  // two contiguous requests per query block: image, row statistics
-          const int qb_gi = __shfl_sync(0xffffffffu, qbl, gi);
-          if (lane == 0) {
-            const size_t qimg = static_cast<size_t>(bh) * g.N + qb_gi;
-            bulk_load(stage_q(s) + gi * blk_bytes, p.qdo_img + qimg * blk_bytes, blk_bytes, &bar_c_full[s]);
-            bulk_load(stage_ld(s) + gi * 2 * SR, p.lsed + qimg * 2 * SR, ld_bytes, &bar_c_full[s]);
-          }
+        __syncwarp();
+        if (e_qb >= 0) {
+          const size_t qimg = static_cast<size_t>(bh) * g.N + e_qb;
+          bulk_load(stage_q(s) + (e_roff >> 3) * SM::PG, p.qdo_img + qimg * blk_bytes,
+                    static_cast<uint32_t>(e_sz / 8) * SM::PG, &bar_c_full[s]);
+          bulk_load(stage_ld(s) + 2 * e_roff, p.lsed + qimg * 2 * SR, 8u * e_sz, &bar_c_full[s]);
         }
         __syncwarp();
       }
@@ -492,8 +536,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int item = read_item(it);
       if (item < 0) break;
       const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
-      const int nchunks = (nq_of(bh, j) + G - 1) / G;
-      if (nchunks == 0) continue;
+      if (nq_of(bh, j) == 0) continue;
       if (warp == W_SD) {
         // K/V tiles of the block: the previous block's are read until its last MMA (bar_acc)
         if (leader) {
@@ -511,11 +554,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (lane == 0) PROG(9, 2000 + nacc);
         // S/dP(v) = Q^s K^T, dO^s V^T of chunk v, issued as soon as its stage landed and the softmax
         // warps hold S/dP(v-1) in registers (single TMEM buffer)
-        for (int cl = 0; cl < nchunks; ++cl, ++c) {
+        for (bool last = false; !last; ++c) {
           const int sv = c & 1;
           const uint32_t sov = (sv * SM::STAGE_BYTES) >> 4;  // stage offset in descriptor units
           if (lane == 0) PROG(1, c * 4 + 0);
           bwait(&bar_c_full[sv], (c >> 1) & 1);
+          last = (s_cinfo[c & 3] >> 8) & 1;
           BWD_TRACE(11, c);
           if (lane == 0) PROG(1, c * 4 + 1);
           if (c >= 1) bwait(&bar_sd_free, (c - 1) & 1);
@@ -543,11 +587,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         if (lane == 0) PROG(10, 1000 + nacc);
         if (nacc > 0) bwait(&bar_acc_free, (nacc - 1) & 1);
         if (lane == 0) PROG(10, 2000 + nacc);
-        for (int cl = 0; cl < nchunks; ++cl, ++c) {
+        int cl = 0;  // chunk of this KV block (its first gradient MMAs overwrite dV / dK)
+        for (bool last = false; !last; ++c, ++cl) {
           const int s = c & 1, qbuf = c & 1;
           const uint32_t so = (s * SM::STAGE_BYTES) >> 4;
           if (lane == 0) PROG(2, c * 4 + 0);
           bwait(&bar_ps_full, c & 1);
+          last = (s_cinfo[c & 3] >> 8) & 1;
           if (lane == 0) PROG(2, c * 4 + 1);
           if (!DS && c >= 2) bwait(&bar_dq_free[qbuf], ((c - 2) >> 1) & 1);  // drain has read dQ(c-2) from TMEM
           if (lane == 0) PROG(2, c * 4 + 2);
@@ -596,7 +642,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     const int q4 = warp;
     const int row = q4 * 32 + lane;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
-    const int gi = row / SR, lr = row % SR;
     // Key columns of a ragged block past its extent need no mask here: their K/V rows arrive as zeros
     // (TMA out-of-grid fill), so they add nothing to dQ = dS K, and their dK/dV columns are never stored.
     const float sl2 = p.scale_log2;
@@ -607,16 +652,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int item = read_item(it);
       if (item < 0) break;
       // only `item` stays live across the chunk loop (the block coordinates are re-derived for the store)
-      const int nchunks = (p.k2q_num[static_cast<size_t>(p.bh0) * g.N + item] + G - 1) / G;
-      for (int cl = 0; cl < nchunks; ++cl, ++c) {
+      const bool any_chunk = p.k2q_num[static_cast<size_t>(p.bh0) * g.N + item] > 0;
+      for (bool last = !any_chunk; any_chunk;) {
         const int s = c & 1;
         if (row == 0) PROG(3, c * 8 + 0);
         bwait(&bar_c_full[s], (c >> 1) & 1);
         if (row == 0) PROG(3, c * 8 + 1);
         if (row == 0 && c == 0) CTA_STAMP(8);
-        const bool valid = lr < s_nk[c & 3][gi];  // (slots past the chunk's last block have nk = 0)
-        const float nl = valid ? -stage_ld(s)[gi * 2 * SR + lr] : -INFINITY;  // invalid rows: P = dS = 0
-        const float Dq = valid ? stage_ld(s)[gi * 2 * SR + SR + lr] : 0.f;
+        const int cinfo = s_cinfo[c & 3], ne = cinfo & 255;
+        last = (cinfo >> 8) & 1;
+        bool valid = false;  // this row belongs to a block of the chunk and is one of its kept rows
+        for (int e = 0; e < ne; ++e) {
+          const int v = s_nk[c & 3][e], roff = v >> 8, nk = v & 255;
+          if (row >= roff && row < roff + nk) valid = true;
+        }
+        const float nl = valid ? -stage_ld(s)[2 * row] : -INFINITY;  // invalid rows: P = dS = 0
+        const float Dq = valid ? stage_ld(s)[2 * row + 1] : 0.f;
         bwait(&bar_sd_full, c & 1);
         if (row == 0) PROG(3, c * 8 + 2);
         tc_fence_after();
@@ -673,17 +724,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           if (lane == 0) {
             const int* slots = reinterpret_cast<const int*>(sm + SM::OFF_SLOT) + (c & 3) * 16;
             const int w0 = q4 * 32;
-            for (int gi = w0 / SR; gi < G && gi * SR < w0 + 32; ++gi) {
-              const int sl = slots[gi];
-              if (sl < 0 || s_nk[c & 3][gi] == 0) continue;
-              const int r0 = max_i(gi * SR, w0), r1 = min_i((gi + 1) * SR, w0 + 32);
-              bulk_store(p.ds_buf + (static_cast<size_t>(sl) * SR + (r0 - gi * SR)) * 128, sdS + r0 * 128,
+            for (int e = 0; e < ne; ++e) {
+              const int v = s_nk[c & 3][e], roff = v >> 8, nk = v & 255, sz = slot_size(nk, SR);
+              const int sl = slots[e];
+              const int r0 = max_i(roff, w0), r1 = min_i(roff + sz, w0 + 32);
+              if (sl < 0 || r0 >= r1 || r0 - roff >= nk) continue;
+              bulk_store(p.ds_buf + (static_cast<size_t>(sl) * SR + (r0 - roff)) * 128, sdS + r0 * 128,
                          static_cast<uint32_t>(r1 - r0) * 128);
             }
             bulk_commit_group();
           }
         }
         if (row == 0) BWD_TRACE(5, c);
+        ++c;
+        if (last) break;
       }
       if (row == 0) CTA_STAMP(5);
       // dK_j, dV_j: TMEM lane == channel (row of dK^T / dV^T), columns == keys of block j. Transposed into
@@ -694,7 +748,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
       const int ch_ = row;
       const uint32_t tdk = smem_u32(sP), tdv = smem_u32(sdS);
       if (row == 0) PROG(11, 1000 + nacc);
-      if (nchunks > 0) {
+      if (any_chunk) {
         bwait(&bar_acc, nacc & 1);
         tc_fence_after();
       }
@@ -707,7 +761,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
 #pragma unroll 1
       for (int cc0 = 0; cc0 < BT; cc0 += 16) {
         float kv[16], vv[16];
-        if (nchunks > 0) {
+        if (any_chunk) {
           tmem_ld16(trow + 3 * BT + cc0, kv);
           tmem_ld16(trow + 2 * BT + cc0, vv);
           tmem_wait_ld();
@@ -725,7 +779,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
           }
         }
       }
-      if (nchunks > 0) {
+      if (any_chunk) {
         tc_fence_before();
         mbar_arrive(&bar_acc_free);
         ++nacc;
@@ -757,16 +811,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
     const int q4 = warp - 4;
     const int row = q4 * 32 + lane;
     constexpr int SROWS = SM::DQ_SROWS, NSL = SM::DQ_SLOTS, SPS = 32 / SROWS;  // slots per 32-column slice
+    static_assert(SROWS == 32, "a drain slot holds the warp's 32 rows of one 32-column slice");
     uint8_t* slots = sm + SM::OFF_DQS + q4 * NSL * SM::DQ_SLOT_BYTES;
-    const int R = p.dq_rows, nsub = 32 / R, per_slot = SROWS / R;
     int slot_i = 0;
     int c = 0;
     for (int it = 0;; ++it) {
       const int item = read_item(it);
       if (item < 0) break;
       const int hc = item / g.N, j = item - hc * g.N, bh = p.bh0 + hc;
-      const int nchunks = (nq_of(bh, j) + G - 1) / G;
-      for (int cl = 0; cl < nchunks; ++cl, ++c) {
+      const bool any_chunk = nq_of(bh, j) > 0;
+      for (bool last = !any_chunk; any_chunk;) {
         const int qbuf = c & 1;
         if (lane == 0) PROG(4 + q4, c * 8 + 0);
         bwait(&bar_dq_full[qbuf], (c >> 1) & 1);
@@ -774,21 +828,32 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         tc_fence_after();
         if (row == 0) BWD_TRACE(6, c);
         const int ring = c & 3;
-        int dst = -1;  // lane k < nsub: first dQacc row of sub-box k
-        if (lane < nsub) {
-          const int r0 = q4 * 32 + lane * R, gi = r0 / SR, lr0 = r0 % SR;
-          if (gi < G && s_row0[ring][gi] >= 0 && lr0 < s_nk[ring][gi]) dst = s_row0[ring][gi] + lr0;
+        // this quadrant's pieces of the chunk's blocks (a block's rows inside [32 q4, 32 q4 + 32), 8 / 16 / 32 of
+        // them, at most four), read into registers now: the ring entry may be rewritten once dQ(c) is released
+        const int cinfo = s_cinfo[ring], ne = cinfo & 255;
+        last = (cinfo >> 8) & 1;
+        int pdst = -1, poff = 0, prows = 0;
+        if (lane < ne) {
+          const int v = s_nk[ring][lane], roff = v >> 8, nk = v & 255, sz = slot_size(nk, SR);
+          const int r0 = max_i(roff, q4 * 32), r1 = min_i(roff + sz, q4 * 32 + 32);
+          if (r0 < r1 && r0 - roff < nk) {
+            pdst = s_row0[ring][lane] + (r0 - roff);
+            poff = r0 - q4 * 32;
+            prows = r1 - r0;
+          }
         }
-        int dk[4];
+        unsigned pm = __ballot_sync(0xffffffffu, pdst >= 0);
+        const bool any = pm != 0u;
+        int dk[4], dof[4], drw[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
-        const bool any = __any_sync(0xffffffffu, dst >= 0);
-#ifdef BSA_ABLATE_DQ_DRAIN
-        tc_fence_before();
-        mbar_arrive(&bar_dq_free[qbuf]);
-        (void)any;
-        continue;
-#endif
+        for (int k = 0; k < 4; ++k) {
+          const int e = pm ? __ffs(pm) - 1 : 0;
+          dk[k] = __shfl_sync(0xffffffffu, pdst, e);
+          dof[k] = __shfl_sync(0xffffffffu, poff, e);
+          drw[k] = __shfl_sync(0xffffffffu, prows, e);
+          if (!pm) dk[k] = -1;
+          pm &= pm - 1u;
+        }
 #pragma unroll 1
         for (int cs = 0; cs < D; cs += 32) {
           float v[32];
@@ -816,24 +881,21 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
+              uint8_t* slot = slots + s_first * SM::DQ_SLOT_BYTES;
 #pragma unroll
-              for (int hf = 0; hf < SPS; ++hf) {
-                uint8_t* slot = slots + ((s_first + hf) % NSL) * SM::DQ_SLOT_BYTES;
-                for (int k = 0; k < per_slot; ++k) {
-                  const int sb = hf * per_slot + k;
-#ifndef BSA_ABLATE_DQ_RED
-                  if (dk[sb] >= 0) tma_reduce_add_2d(&p.mDQ, slot + k * R * 128, cs, dk[sb]);
-#else
-                  (void)slot;
-                  (void)sb;
-#endif
-                }
-                bulk_commit_group();
+              for (int k = 0; k < 4; ++k) {
+                if (dk[k] < 0) continue;
+                // the box covering the piece's rows (8 / 16 / 32; its rows are a prefix-aligned part of the slot)
+                const CUtensorMap* m = drw[k] == 32 ? &p.mDQ : drw[k] == 16 ? &p.mDQh : &p.mDQq;
+                tma_reduce_add_2d(m, slot + dof[k] * 128, cs, dk[k]);
               }
+              bulk_commit_group();
             }
           }
         }
         if (row == 0) BWD_TRACE(7, c);
+        ++c;
+        if (last) break;
       }
     }
     if (lane == 0) PROG(4 + q4, 999999);
@@ -1257,8 +1319,11 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
   p.ds_cap = a.ds_cap;
   p.k2q_slot = a.k2q_slot;
   p.ds_buf = a.ds_buf;
-  p.dq_rows = a.SR < BSA_DQ_SLOT_ROWS ? a.SR : BSA_DQ_SLOT_ROWS;
-  if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, static_cast<size_t>(a.BH) * a.Lq, p.dq_rows)) return cudaErrorInvalidValue;
+  const size_t dq_rows_total = static_cast<size_t>(a.BH) * a.Lq;
+  if (!make_map_rows_f32(&p.mDQ, a.dQacc, a.d, dq_rows_total, 32) ||
+      !make_map_rows_f32(&p.mDQh, a.dQacc, a.d, dq_rows_total, 16) ||
+      !make_map_rows_f32(&p.mDQq, a.dQacc, a.d, dq_rows_total, 8))
+    return cudaErrorInvalidValue;
   const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
                    heads_uniform(a.dV, a.B);
   const int launches = one ? 1 : a.B, heads = one ? a.BH : a.Hh;

@@ -100,7 +100,7 @@ struct BwdArgs {
   Rows dQ, dK, dV;
   // workspace
   uint8_t* qdo_img;  // [BH, N] query-block images of Q^s|dO^s, SR*d*4 bytes each (k_bwd_prep)
-  float* lsed;       // [BH, N, 2, SR]: per query block LSE*log2(e) of its SR rows, then D of its SR rows
+  float* lsed;       // [BH, N, SR, 2]: per query block and row, LSE*log2(e) and D
   float* dQacc;  // [BH, Lq, d]
   int* work_ctr;  // [B] item counters of the persistent main kernel (one per launch)
   // dS path (attn_bwd.cu): selection lists, pair slots, the path switch and the dS tile store
