@@ -232,6 +232,16 @@ enum bsa_kernel_id {
  * BSA_ERR_CONFIG. */
 enum bsa_bwd_path { BSA_BWD_REDUCE = 0, BSA_BWD_DS = 1 };
 int bsa_set_bwd_path(int mode);
+/* Forward query tiling (process-wide). A query block takes its kept count rounded up to a power of two rows, at
+ * least min_slot_rows and at most SR (the largest kept count rounded up); blocks of one slot size fill 128-row
+ * tiles in block order (PAPER.md P:204-210 leaves the tiling of the Q blocks to the kernel). min_slot_rows: 0 =
+ * the default (16), 8, 16, 32, 64, or 128 (>= SR: one SR-row slot per block, i.e. 128/SR consecutive blocks per
+ * tile). order: BSA_FWD_SMALL_FIRST (default: tiles of the smallest slots, which union the most KV lists, are
+ * claimed first) or BSA_FWD_LARGE_FIRST. Results do not depend on either beyond fp32 summation order (each row's
+ * softmax runs over its own admitted blocks). Other values: BSA_ERR_CONFIG. Overrides BSA_FWD_PACK /
+ * BSA_FWD_ORDER from the environment. */
+enum bsa_fwd_order { BSA_FWD_SMALL_FIRST = 0, BSA_FWD_LARGE_FIRST = 1 };
+int bsa_set_fwd_tiling(int min_slot_rows, int order);
 /* Capacity of the backward's dS path in admitted (query block, KV block) pairs for this geometry (-1 unless
  * BSA_BWD_DS is set): bsa_attn_bwd takes the dS path iff sum(q2k_num) <= *pairs. Errors as
  * bsa_workspace_bytes. */

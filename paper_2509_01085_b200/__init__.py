@@ -113,12 +113,13 @@ def lib() -> ctypes.CDLL:
         L.bsa_timing_enable.argtypes = [_I]
         L.bsa_timing_read.argtypes = [_P, _P, _I]
         L.bsa_set_bwd_path.argtypes = [_I]
+        L.bsa_set_fwd_tiling.argtypes = [_I, _I]
         L.bsa_bwd_ds_capacity.argtypes = [gp, _D, _I, _I, _I, _P]
         for f in ("bsa_timing_enable", "bsa_timing_read",
                   "bsa_sizes", "bsa_workspace_bytes", "bsa_block_partition", "bsa_select_queries",
                   "bsa_select_kv_blocks", "bsa_attn_fwd", "bsa_attn_bwd", "bsa_sp_relayout",
                   "bsa_select_kv_blocks_ex", "bsa_resolve_k", "bsa_kv_quantile", "bsa_set_bwd_path", "bsa_bwd_ds_capacity",
-                  "bsa_sp_relayout_group"):
+                  "bsa_sp_relayout_group", "bsa_set_fwd_tiling"):
             getattr(L, f).restype = _I
         _lib = L
     return _lib
@@ -312,6 +313,15 @@ def bwd_ds_capacity(g: Geometry, r: float, B: int, Hh: int, d: int) -> int:
 def set_bwd_path(mode: int):
     """Backward dQ path, process-wide (include/bsa.h bsa_set_bwd_path): BWD_REDUCE (default) or BWD_DS."""
     _check(lib().bsa_set_bwd_path(int(mode)), "bsa_set_bwd_path")
+
+
+FWD_SMALL_FIRST, FWD_LARGE_FIRST = 0, 1
+
+
+def set_fwd_tiling(min_slot_rows: int = 0, order: int = FWD_SMALL_FIRST):
+    """Forward query tiling, process-wide (include/bsa.h bsa_set_fwd_tiling): a block's slot is its kept count
+    rounded up to a power of two >= min_slot_rows (0 = default 16; >= SR = one slot per block)."""
+    _check(lib().bsa_set_fwd_tiling(int(min_slot_rows), int(order)), "bsa_set_fwd_tiling")
 
 
 SP_SEQ_TO_SEND, SP_RECV_TO_HEADS, SP_HEADS_TO_SEND, SP_RECV_TO_SEQ, SP_SEQ_TO_SEND_T, SP_RECV_T_TO_SEQ = 0, 1, 2, 3, 4, 5

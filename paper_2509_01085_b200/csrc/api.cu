@@ -40,6 +40,8 @@ struct TimedRec {
 // Process-wide (autograd runs the backward on its own worker thread, which must be counted and timed too).
 std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_bwd_path{BSA_BWD_REDUCE};  // bsa_set_bwd_path
+std::atomic<int> g_fwd_min_slot{-1};          // bsa_set_fwd_tiling (-1: not set, the environment decides)
+std::atomic<int> g_fwd_order{-1};
 std::atomic<bool> g_timing{false};
 std::mutex g_recs_mu;
 std::vector<TimedRec> g_recs;
@@ -161,10 +163,20 @@ bool fwd_grouping() {
   return on;
 }
 
+// Packed forward tiles (attn_fwd.cu k_fwd_union): a query block takes its kept count rounded up to a power of
+// two >= 16 rows, tiles of the smallest slots first. Measured (attn_fwd ms, unpacked -> packed):
+// 32k 0.814 -> 0.799, 75k 10.02 -> 9.65, 147k 31.88 -> 31.32, own dense path 9.09 -> 7.53. An 8-row minimum packs
+// 16 ragged blocks per tile, whose KV union grows as fast as the rows shrink (32k 0.826, 147k 32.00).
+// BSA_FWD_PACK=0 (one SR-row slot per block), =8 (8-row minimum), BSA_FWD_ORDER=large: the alternatives.
+int env_flag(const char* name, const char* on_value) {
+  const char* e = std::getenv(name);
+  return e && std::strcmp(e, on_value) == 0;
+}
+
 // Forward workspace: K|V block images (always) + gathered Q^s (only used when q_packed is NULL) + the tile
 // grouping's scratch and tile table (G >= 2).
 struct FwdWs {
-  size_t kv, qs, grp, perm, ul, uc, ctr, total;
+  size_t kv, qs, grp, perm, ul, uc, ctr, tab, tcount, total;
 };
 FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   FwdWs w;
@@ -175,11 +187,13 @@ FwdWs fwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int d, int SR) {
   w.perm = w.grp + align256(G >= 2 ? bsa::group_ws_bytes(g.N, static_cast<int>(BH)) : 0);
   w.ul = w.perm + align256(G >= 2 ? BH * static_cast<size_t>(bsa::group_ntiles(g.N, G)) * G * 4 : 0);
   // union lists of the forward tiles (enough for the grouped tiling, which has the most tiles)
-  const size_t ntiles = G >= 2 ? std::max(static_cast<size_t>(bsa::group_ntiles(g.N, G)), static_cast<size_t>((g.N + G - 1) / G))
-                               : static_cast<size_t>(g.N);
+  const size_t ntiles = std::max(static_cast<size_t>(G >= 2 ? bsa::group_ntiles(g.N, G) : 0),
+                                 static_cast<size_t>(bsa::fwd_max_tiles(g.N, SR)));
   w.uc = w.ul + align256(BH * ntiles * g.N * 4);
   w.ctr = w.uc + align256(BH * ntiles * 4);
-  w.total = w.ctr + 256;
+  w.tab = w.ctr + 256;  // packed tile entries, then their count
+  w.tcount = w.tab + align256(ntiles * 16 * 4);
+  w.total = w.tcount + 256;
   return w;
 }
 
@@ -492,6 +506,13 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.ulists = reinterpret_cast<uint32_t*>(base + w.ul);
   a.ucount = reinterpret_cast<int*>(base + w.uc);
   a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
+  a.tab = reinterpret_cast<int*>(base + w.tab);
+  static const int no_pack = env_flag("BSA_FWD_PACK", "0"), pack8 = env_flag("BSA_FWD_PACK", "8"),
+                   large_first = env_flag("BSA_FWD_ORDER", "large");
+  const int min_slot = g_fwd_min_slot.load() >= 0 ? g_fwd_min_slot.load() : (no_pack ? 128 : (pack8 ? 8 : 0));
+  a.pack_min = min_slot == 0 ? (SR < 16 ? SR : 16) : (min_slot < SR ? min_slot : SR);
+  a.small_first = g_fwd_order.load() >= 0 ? g_fwd_order.load() == BSA_FWD_SMALL_FIRST : !large_first;
+  a.tcount = reinterpret_cast<int*>(base + w.tcount);
   if (e == cudaSuccess)
     e = timed(BSA_K_FWD_UNION, 1, st, [&] { return bsa::launch_fwd_union(a, a.ulists, a.ucount, st); });
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });
@@ -593,6 +614,17 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
 int bsa_set_bwd_path(int mode) {
   if (mode != BSA_BWD_REDUCE && mode != BSA_BWD_DS) return fail(BSA_ERR_CONFIG, "unknown backward path %d", mode);
   g_bwd_path.store(mode);
+  return BSA_OK;
+}
+
+int bsa_set_fwd_tiling(int min_slot_rows, int order) {
+  if (min_slot_rows != 0 && min_slot_rows != 8 && min_slot_rows != 16 && min_slot_rows != 32 && min_slot_rows != 64 &&
+      min_slot_rows != 128)
+    return fail(BSA_ERR_CONFIG, "forward min slot rows must be 0, 8, 16, 32, 64 or 128 (got %d)", min_slot_rows);
+  if (order != BSA_FWD_SMALL_FIRST && order != BSA_FWD_LARGE_FIRST)
+    return fail(BSA_ERR_CONFIG, "unknown forward tile order %d", order);
+  g_fwd_min_slot.store(min_slot_rows);
+  g_fwd_order.store(order);
   return BSA_OK;
 }
 

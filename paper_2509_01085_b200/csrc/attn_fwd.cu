@@ -57,12 +57,16 @@ struct FwdParams {
   const int* kept_tok;
   const int* q2k_num;
   const int* q2k_idx;
-  const int* perm;   // [BH][ntiles][G] query block of each tile slot (-1 = empty), or NULL: tile t = blocks t G ..
+  const int* perm;   // [BH][ntiles][G] query block of each tile slot (-1 = empty, slot g = rows [g SR, (g+1) SR)), or
+                     // NULL: the packed tiles of k_fwd_union (tab / tcount)
   int ntiles;
+  const int* tab;    // [tiles][MAX_G] packed tile entries, query block | row offset << 16 (-1 = none)
+  const int* tcount; // number of packed tiles per head (device; written by k_fwd_union)
+  int BH;
+  int pack_min;      // smallest slot (8 rows; SR = one slot per block, the unpacked tiling)
   const uint32_t* ulists;  // [BH][ntiles][N] union entries of each tile (k_fwd_union), ucount[BH][ntiles] of them
   const int* ucount;
   int* work_ctr;           // next unclaimed tile (zeroed before the launch; the CTAs are persistent)
-  int total_tiles;         // BH * ntiles
   float scale_log2;  // scale * log2(e)
   Rows O;            // raster output, strided
   float* lse;
@@ -75,6 +79,12 @@ constexpr int FWD_THREADS = 384;
 constexpr int FWD_STAGES = 6;  // K|V ring depth (5 when the two union lists of a large N need the room)
 constexpr int MAX_N = 4096;
 constexpr int MAX_G = 16;
+// rows a query block with nk kept queries takes in a packed tile: nk rounded up to a power of two >= 8 (<= SR)
+__host__ __device__ __forceinline__ int fwd_slot_size(int nk, int SR, int min_sz) {
+  int sz = min_sz;
+  while (sz < nk && sz < SR) sz <<= 1;
+  return sz;
+}
 
 template <int D, int BT, int FWD_STAGES = bsa::FWD_STAGES>
 struct FwdSmem {
@@ -127,7 +137,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   __shared__ float s_ml[2][2][128];  // epilogue exchange: [group][m, l][row]
   __shared__ uint32_t s_tmem;
   // per metadata buffer: claimed item (-1: no work left), slot query blocks / kept counts / kept offsets, U
-  __shared__ int s_item[2], s_U[2], s_qb[2][MAX_G], s_nk[2][MAX_G], s_koff[2][MAX_G];
+  __shared__ int s_item[2], s_U[2], s_qb[2][MAX_G], s_nk[2][MAX_G], s_koff[2][MAX_G], s_roff[2][MAX_G];
+  __shared__ uint8_t s_rowent[2][128];  // tile row -> its entry (0xFF: no query block)
   __shared__ int s_clsn16[8];
   // Key-validity mask of each block-extent class (bit t/h/w set = the block is the ragged last one along
   // that axis, C23): 8 classes, one 64-bit row mask each, so the per-step masking is a bit test instead of
@@ -137,6 +148,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = p.G, SR = p.SR;
+  const int NT = p.perm ? p.ntiles : *p.tcount;  // tiles per head
+  const int total_tiles = NT * p.BH;
   constexpr int W_ALLOC = 8, W_PROD = 9, W_PV = 10, W_QK = 11;
   constexpr int META_READERS = 11;  // producer, PV issuer, QK issuer, 8 softmax warps
 
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     if (lane == 0) mbar_arrive(&bar_meta_free[it & 1]);
   };
   auto rot_of = [&](int item, int U) {
-    const int bh = item / p.ntiles, tile = item - bh * p.ntiles;
+    const int bh = item / NT, tile = item - bh * NT;
     return U > 0 ? static_cast<int>((static_cast<unsigned>(tile) * 2654435761u + bh * 40503u) % U) : 0;
   };
 
@@ -189,23 +202,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
       int item = 0;
       if (lane == 0) item = atomicAdd(p.work_ctr, 1);
       item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= p.total_tiles) item = -1;
+      if (item >= total_tiles) item = -1;
       if (item >= 0) {
-        const int bh = item / p.ntiles, tile = item - bh * p.ntiles;
-        if (lane < G) {
-          int qb;
-          if (p.perm) qb = p.perm[static_cast<size_t>(item) * G + lane];
-          else qb = tile * G + lane < g.N ? tile * G + lane : -1;
+        const int tile = item % NT;
+        int qb = -1, roff = 0;
+        if (p.perm) {
+          if (lane < G) { qb = p.perm[static_cast<size_t>(item) * G + lane]; roff = lane * SR; }
+        } else if (lane < MAX_G) {
+          const int e = p.tab[tile * MAX_G + lane];
+          if (e >= 0) { qb = e & 0xFFFF; roff = e >> 16; }
+        }
+        const int nk = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
+        if (lane < MAX_G) {
           s_qb[b][lane] = qb;
-          s_nk[b][lane] = qb >= 0 ? p.kept_off[qb + 1] - p.kept_off[qb] : 0;
+          s_nk[b][lane] = nk;
           s_koff[b][lane] = qb >= 0 ? p.kept_off[qb] : 0;
+          s_roff[b][lane] = roff;
+        }
+        for (int r = lane; r < 128; r += 32) s_rowent[b][r] = 0xFF;
+        __syncwarp();
+        if (qb >= 0) {
+          const int sz = p.perm ? SR : fwd_slot_size(nk, SR, p.pack_min);
+          for (int r = roff; r < roff + sz; ++r) s_rowent[b][r] = static_cast<uint8_t>(lane);
         }
         const int U = p.ucount[item];
         const uint32_t* src = p.ulists + static_cast<size_t>(item) * g.N;
         uint32_t* dst = ulist0 + b * g.N;
         for (int u = lane; u < U; u += 32) dst[u] = __ldg(src + u);
         if (lane == 0) s_U[b] = U;
-        (void)bh;
       }
       if (lane == 0) s_item[b] = item;
       __syncwarp();
@@ -218,7 +242,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     for (int it = 0;; ++it) {
       const int item = wait_meta(it);
       if (item < 0) break;
-      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / p.ntiles;
+      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / NT;
       const uint32_t* ul = ulist0 + b * g.N;
       if (lane == 0) {
         for (int u = 0; u < U; ++u, ++gs) {
@@ -321,9 +345,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     // w % 4) fill each other's latency; the two partial results are merged in the epilogue (split-K).
     const int group = warp >> 2, q4 = warp & 3;
     const int row = q4 * 32 + lane;
-    const int gi = row / SR, lr = row % SR;
     const uint32_t trow = tbase + (static_cast<uint32_t>(q4 * 32) << 16);
-    const int mybit = 16 + (gi < G ? gi : 0);  // this row's slot in an entry's admitting-slot mask
     const float sl2 = p.scale_log2;
     const uint32_t tS = trow + SM::T_S + group * BT, tP = trow + SM::T_P + group * (BT / 2);
     const uint32_t tO = trow + SM::T_O + group * D;
@@ -331,10 +353,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
     for (int it = 0;; ++it) {
       const int item = wait_meta(it);
       if (item < 0) break;
-      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / p.ntiles;
+      const int b = it & 1, U = s_U[b], rot = rot_of(item, U), bh = item / NT;
       const uint32_t* ul = ulist0 + b * g.N;
       auto entry_at = [&](int u) { int x = u + rot; return ul[x >= U ? x - U : x]; };
-      const bool valid = gi < G && s_qb[b][gi] >= 0 && lr < s_nk[b][gi];
+      const int gi = s_rowent[b][row];  // this row's entry (its bit in an union entry's admitting mask)
+      const int lr = gi != 0xFF ? row - s_roff[b][gi] : 0;
+      const bool valid = gi != 0xFF && lr < s_nk[b][gi];
+      const int mybit = 16 + (valid ? gi : 0);
       const size_t prow_idx = valid ? static_cast<size_t>(bh) * p.Lq + s_koff[b][gi] + lr : 0;
       if (group == 0) {
         // Q^s row -> TMEM (A operand of the S MMAs): bf16 pairs in memory order. The last tile's QKs are all
@@ -498,21 +523,72 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 // Union pre-pass (one CTA per (tile, b,h)): the ascending union of the tile slots' admitted KV blocks (P:210
 // q2k lists), entry = j | extent class << 12 (bit 2/1/0: ragged last block along t/h/w, C23) | mask << 16 of the
 // slots that admitted j. Built here, in parallel for all tiles, so the attention CTA's prologue is one list copy.
+//
+// Packed tiles (perm == NULL): a query block takes fwd_slot_size(nk) rows (its kept count rounded up to a power
+// of two >= 8), and the blocks of one slot size fill tiles of 128 / size of them in block order (a ragged edge
+// block's 8 or 16 kept queries no longer pad a 32- or 64-row slot). Every CTA derives the same tiling from
+// kept_off (class counts, then the stable rank of each block within its class); the (tile 0, bh 0) CTA
+// publishes the tile count and the CTAs of bh 0 their tile's entries for the attention kernel.
 template <int MAXG>
 __global__ void __launch_bounds__(256) k_fwd_union(Geo g, int G, int ntiles, const int* __restrict__ perm,
+                                                   const int* __restrict__ kept_off, int SR, int pack_min,
+                                                   int small_first,
                                                    const int* __restrict__ q2k_num, const int* __restrict__ q2k_idx,
-                                                   uint32_t* __restrict__ ulists, int* __restrict__ ucount) {
+                                                   uint32_t* __restrict__ ulists, int* __restrict__ ucount,
+                                                   int* __restrict__ tab, int* __restrict__ tcount) {
   extern __shared__ uint32_t ubits[];  // [G][NW] slot bitmaps
   __shared__ int s_qb[MAXG];
   __shared__ int s_upre[MAX_N / 32];
-  __shared__ int s_tot;
+  __shared__ int s_tot, s_cnt[4], s_wcnt[8];
   const int tile = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NW = (g.N + 31) >> 5;
-  if (tid < G) {
-    int qb;
-    if (perm) qb = perm[(static_cast<size_t>(bh) * ntiles + tile) * G + tid];
-    else qb = tile * G + tid < g.N ? tile * G + tid : -1;
-    s_qb[tid] = qb;
+  int NT = ntiles;
+  if (perm) {
+    if (tid < G) s_qb[tid] = perm[(static_cast<size_t>(bh) * ntiles + tile) * G + tid];
+  } else {
+    G = MAXG;
+    auto cls_of = [&](int j) {  // log2(slot size / 8), -1 for a block without kept queries
+      const int nk = kept_off[j + 1] - kept_off[j];
+      return nk > 0 ? 31 - __clz(fwd_slot_size(nk, SR, pack_min) >> 3) : -1;
+    };
+    if (tid < 4) s_cnt[tid] = 0;
+    if (tid < MAXG) s_qb[tid] = -1;
+    __syncthreads();
+    for (int j = tid; j < g.N; j += 256) {
+      const int c = cls_of(j);
+      if (c >= 0) atomicAdd(&s_cnt[c], 1);
+    }
+    __syncthreads();
+    // tiles of the largest slot size first (or the smallest: their longer unions start early)
+    int t0 = 0, k = -1, first = 0;
+    for (int ci = 0; ci < 4; ++ci) {
+      const int c = small_first ? ci : 3 - ci;
+      const int nt = (s_cnt[c] + (16 >> c) - 1) / (16 >> c);
+      if (k < 0 && tile < t0 + nt) { k = c; first = t0; }
+      t0 += nt;
+    }
+    NT = t0;
+    if (bh == 0 && tile == 0 && tid == 0) *tcount = NT;
+    if (tile >= NT) return;  // (uniform)
+    const int per = 16 >> k, r0 = (tile - first) * per;
+    int carry = 0;
+    for (int j0 = 0; j0 < g.N; j0 += 256) {  // stable rank of each class-k block
+      const int j = j0 + tid;
+      const bool isk = j < g.N && cls_of(j) == k;
+      const uint32_t bal = __ballot_sync(0xffffffffu, isk);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = carry;
+      for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+      const int rank = off + __popc(bal & ((1u << lane) - 1u));
+      if (isk && rank >= r0 && rank < r0 + per) s_qb[rank - r0] = j;
+      for (int w = 0; w < 8; ++w) carry += s_wcnt[w];
+      __syncthreads();
+    }
+    if (bh == 0 && tid < MAXG) {
+      const int qb = s_qb[tid];
+      tab[tile * MAXG + tid] = qb >= 0 ? qb | ((tid * (8 << k)) << 16) : -1;
+    }
   }
   for (int w = tid; w < G * NW; w += 256) ubits[w] = 0u;
   __syncthreads();
@@ -548,7 +624,7 @@ __global__ void __launch_bounds__(256) k_fwd_union(Geo g, int G, int ntiles, con
     if (lane == 0) s_tot = carry;
   }
   __syncthreads();
-  const size_t tix = static_cast<size_t>(bh) * ntiles + tile;
+  const size_t tix = static_cast<size_t>(bh) * NT + tile;
   uint32_t* out = ulists + tix * g.N;
   for (int w = warp; w < NW; w += 8) {
     uint32_t v = 0u, mask = 0u;
@@ -568,12 +644,16 @@ __global__ void __launch_bounds__(256) k_fwd_union(Geo g, int G, int ntiles, con
   if (tid == 0) ucount[tix] = s_tot;
 }
 
+int fwd_max_tiles(int N, int SR) { return (N + 128 / SR - 1) / (128 / SR) + 4; }
+
 cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cudaStream_t st) {
-  const int G = 128 / a.SR;
-  const int ntiles = a.perm ? a.ntiles : (a.g.N + G - 1) / G;
+  const int G = a.perm ? 128 / a.SR : MAX_G;
+  const int ntiles = a.perm ? a.ntiles : fwd_max_tiles(a.g.N, a.SR);  // packed: an upper bound (CTAs past it exit)
   const int NW = (a.g.N + 31) / 32;
-  k_fwd_union<MAX_G><<<dim3(ntiles, a.BH), 256, G * NW * 4, st>>>(a.g, G, ntiles, a.perm, a.q2k_num, a.q2k_idx,
-                                                                 ulists, ucount);
+  k_fwd_union<MAX_G><<<dim3(ntiles, a.BH), 256, G * NW * 4, st>>>(a.g, G, ntiles, a.perm, a.kept_off, a.SR,
+                                                                 a.pack_min, a.small_first,
+                                                                 a.q2k_num, a.q2k_idx, ulists, ucount, a.tab,
+                                                                 a.tcount);
   return cudaGetLastError();
 }
 
@@ -675,11 +755,14 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
   p.kv_img = a.kv_img;
   p.Qs = a.Qs;
   p.perm = a.perm;
-  p.ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
+  p.ntiles = a.perm ? a.ntiles : fwd_max_tiles(a.g.N, a.SR);
+  p.tab = a.tab;
+  p.tcount = a.tcount;
+  p.BH = a.BH;
+  p.pack_min = a.pack_min;
   p.ulists = a.ulists;
   p.ucount = a.ucount;
   p.work_ctr = a.work_ctr;
-  p.total_tiles = p.ntiles * a.BH;
   for (int cls = 0; cls < 8; ++cls) {  // key-validity mask per block-extent class (ragged last block per axis)
     const Geo& g = a.g;
     const int et = (cls & 4) ? g.T - (g.Nt - 1) * g.ct : g.ct;
@@ -693,7 +776,7 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
     p.clsn16[cls] = g.BT;
 #endif
   }
-  int ntiles = a.perm ? a.ntiles : (a.g.N + p.G - 1) / p.G;
+  const int ntiles = p.ntiles;  // (an upper bound for the packed tiles: surplus CTAs find no work)
   if (a.d == 128 && a.g.BT == 64) return run_fwd<128, 64>(p, ntiles, a.BH, st);
   if (a.d == 128 && a.g.BT == 32) return run_fwd<128, 32>(p, ntiles, a.BH, st);
   if (a.d == 64 && a.g.BT == 64) return run_fwd<64, 64>(p, ntiles, a.BH, st);

@@ -232,6 +232,22 @@ def test_bwd_path_switch_and_ds_capacity():
     assert L.bsa_set_bwd_path(7) == 2 and b"backward path" in L.bsa_last_error()
 
 
+def test_fwd_tiling_validation():
+    """bsa_set_fwd_tiling (include/bsa.h): min slot rows in {0, 8, 16, 32, 64, 128} and a known order, else
+    BSA_ERR_CONFIG with the setting unchanged; valid settings leave the forward workspace size unchanged."""
+    L = bsa.lib()
+    g = bsa.Geometry(21, 30, 52)
+    ws = bsa.bsa_workspace_bytes(bsa.OP_ATTN_FWD, g, 0.5, 1, 12, 128)
+    assert L.bsa_set_fwd_tiling(12, 0) == 2 and b"min slot" in L.bsa_last_error()
+    assert L.bsa_set_fwd_tiling(8, 5) == 2 and b"order" in L.bsa_last_error()
+    try:
+        for m in (0, 8, 16, 32, 64, 128):
+            bsa.set_fwd_tiling(m, bsa.FWD_LARGE_FIRST)
+            assert bsa.bsa_workspace_bytes(bsa.OP_ATTN_FWD, g, 0.5, 1, 12, 128) == ws
+    finally:
+        bsa.set_fwd_tiling(0, bsa.FWD_SMALL_FIRST)
+
+
 def test_sp_relayout_group_validation():
     """bsa_sp_relayout_group: a head group outside [0, Hh/P) or an unknown mode -> BSA_ERR_CONFIG, d not a
     multiple of 8 or a misaligned buffer -> BSA_ERR_INVALID_SHAPE, all before any device access."""

@@ -136,6 +136,41 @@ def test_attention_parity(case, bwd_path):
     assert torch.count_nonzero(dQ[0].cpu()[torch.from_numpy(pruned)]) == 0
 
 
+TILINGS = [(8, "small"), (128, "small"), (0, "large"), (32, "large")]
+
+
+@pytest.mark.parametrize("tiling", TILINGS, ids=[f"min{m}_{o}" for m, o in TILINGS])
+@pytest.mark.parametrize("case", [c for c in CASES if c[0] in ("ragged_r1", "ragged_r025", "multi_tile", "window222",
+                                                            "d128_bt32", "sparse_k1")], ids=lambda c: c[0])
+def test_fwd_tiling_parity(case, tiling):
+    """The forward's packed query tiles (bsa_set_fwd_tiling: slot = kept count rounded up to a power of two >=
+    min_slot_rows, tiles of one slot size in block order, claimed small- or large-slot first; 128 = one slot per
+    block) give the oracle's O and LSE under every tiling (the default, 16 rows small-first, runs in
+    test_attention_parity). Ragged cases put 8-, 16- and 32-row blocks next to full ones; multi_tile and
+    sparse_k1 give many tiles per head."""
+    og, g, host, dev, k, sel = _run(case, seed=2)
+    name, grid, block, unit, Hh, d, r, f, tau, kind = case
+    Q, K, V = dev
+    scale = 1.0 / np.sqrt(d)
+    try:
+        bsa.set_fwd_tiling(tiling[0], bsa.FWD_SMALL_FIRST if tiling[1] == "small" else bsa.FWD_LARGE_FIRST)
+        O, lse = bsa.bsa_attn_fwd(g, r, Q, K, V, sel.part["kept_off"], sel.kept_tok, sel.donor, sel.q2k_num,
+                                  sel.q2k_idx, scale=scale, q_packed=sel.q_packed)
+        torch.cuda.synchronize()
+    finally:
+        bsa.set_fwd_tiling(0, bsa.FWD_SMALL_FIRST)
+    kt, dn = sel.kept_tok.cpu().numpy()[0], sel.donor.cpu().numpy()[0]
+    qn, qi = sel.q2k_num.cpu().numpy()[0], sel.q2k_idx.cpu().numpy()[0]
+    N = qn.shape[1]
+    qi = np.where(np.arange(N)[None, None, :] < qn[:, :, None], qi, -1)
+    Oref, lseref = orc.attn_fwd(og, r, host[0][0], host[1][0], host[2][0], kt, dn, qn, qi, float(np.float32(scale)))
+    tag = f"{name}/tiling{tiling[0]}{tiling[1]}"
+    assert_close("O", O[0], Oref, case=tag)
+    lse_err = float(np.max(np.abs(lse.cpu().double().numpy()[0] - lseref)))
+    record(tag, kind="lse", max_abs=lse_err)
+    assert lse_err < 2e-2
+
+
 def test_dense_equivalence_d128():
     """r = 1, k = N, tau = 1: BSA == dense attention against torch SDPA in fp32."""
     grid, block, d, Hh = (4, 8, 16), (4, 4, 4), 128, 2

@@ -22,7 +22,8 @@ Q, K, V = bsa_gen.make_inputs(cfg["kind"], 0, cfg["B"], cfg["Hh"], cfg["grid"], 
 dO = bsa_gen.grad_output(0, (cfg["B"], cfg["Hh"], g.L, cfg["d"])).cuda()
 if os.environ.get("BSA_BWD_PATH") == "ds":
     bsa.set_bwd_path(bsa.BWD_DS)
-layer = BSAAttention(g, cfg["r"], cfg["f"], cfg["tau"], cfg["B"], cfg["Hh"], cfg["d"])
+dense = os.environ.get("BSA_DENSE") == "1"  # the own dense path: r = 1, k = N, tau = 1
+layer = BSAAttention(g, *((1.0, 1.0, 1.0) if dense else (cfg["r"], cfg["f"], cfg["tau"])), cfg["B"], cfg["Hh"], cfg["d"])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     layer.forward(Q, K, V)
@@ -40,5 +41,6 @@ L.bsa_timing_enable(0)
 nk = len(KERNEL_NAMES)
 ms = (ctypes.c_double * nk)()
 L.bsa_timing_read(ms, None, nk)
-print(os.path.basename(os.environ.get("BSA_LIB_PATH", "libbsa.so")), name, os.environ.get("BSA_BWD_PATH", "reduce"),
+print(os.path.basename(os.environ.get("BSA_LIB_PATH", "libbsa.so")), name + (" dense" if dense else ""),
+      os.environ.get("BSA_BWD_PATH", "reduce"),
       {n: round(ms[i] / steps, 4) for i, n in enumerate(KERNEL_NAMES) if ms[i] > 0})
