@@ -464,8 +464,19 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* kv_img = base + w.kv;
+  static const int no_pack = env_flag("BSA_FWD_PACK", "0"), pack8 = env_flag("BSA_FWD_PACK", "8"),
+                   large_first = env_flag("BSA_FWD_ORDER", "large");
+  const int min_slot = g_fwd_min_slot.load() >= 0 ? g_fwd_min_slot.load() : (no_pack ? 128 : (pack8 ? 8 : 0));
+  bsa::FwdTiling tl;
+  tl.kept_off = kept_off;
+  tl.SR = SR;
+  tl.pack_min = min_slot == 0 ? (SR < 16 ? SR : 16) : (min_slot < SR ? min_slot : SR);
+  tl.small_first = g_fwd_order.load() >= 0 ? g_fwd_order.load() == BSA_FWD_SMALL_FIRST : !large_first;
+  tl.max_tiles = bsa::fwd_max_tiles(G.N, SR);
+  tl.tab = reinterpret_cast<int*>(base + w.tab);
+  tl.tcount = reinterpret_cast<int*>(base + w.tcount);
   cudaError_t e = timed(BSA_K_KV_IMAGE, 1, st, [&] {
-    return bsa::launch_kv_image(G, static_cast<int>(BH), d, Kv, Vv, kv_img, st);
+    return bsa::launch_kv_image(G, static_cast<int>(BH), d, Kv, Vv, kv_img, tl, st);
   });
   if (e == cudaSuccess && !Qs) {
     bsa::bf16* dst = reinterpret_cast<bsa::bf16*>(base + w.qs);
@@ -506,13 +517,9 @@ int bsa_attn_fwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.ulists = reinterpret_cast<uint32_t*>(base + w.ul);
   a.ucount = reinterpret_cast<int*>(base + w.uc);
   a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
-  a.tab = reinterpret_cast<int*>(base + w.tab);
-  static const int no_pack = env_flag("BSA_FWD_PACK", "0"), pack8 = env_flag("BSA_FWD_PACK", "8"),
-                   large_first = env_flag("BSA_FWD_ORDER", "large");
-  const int min_slot = g_fwd_min_slot.load() >= 0 ? g_fwd_min_slot.load() : (no_pack ? 128 : (pack8 ? 8 : 0));
-  a.pack_min = min_slot == 0 ? (SR < 16 ? SR : 16) : (min_slot < SR ? min_slot : SR);
-  a.small_first = g_fwd_order.load() >= 0 ? g_fwd_order.load() == BSA_FWD_SMALL_FIRST : !large_first;
-  a.tcount = reinterpret_cast<int*>(base + w.tcount);
+  a.tab = tl.tab;
+  a.tcount = tl.tcount;
+  a.pack_min = tl.pack_min;
   if (e == cudaSuccess)
     e = timed(BSA_K_FWD_UNION, 1, st, [&] { return bsa::launch_fwd_union(a, a.ulists, a.ucount, st); });
   if (e == cudaSuccess) e = timed(BSA_K_ATTN_FWD, 1, st, [&] { return bsa::launch_attn_fwd(a, st); });

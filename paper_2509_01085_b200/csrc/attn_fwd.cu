@@ -3,8 +3,9 @@
 // with q2k_num and q2k_index"), followed by the fill that restores length L.
 //
 // B200 design:
-//  * One CTA per query tile = G consecutive query blocks, each in its own slot of SR = 128/G rows of
-//    the packed Q^s (kept queries, block-major). The softmax threads copy their Q^s row straight from
+//  * Query tiles of 128 rows of the packed Q^s (kept queries, block-major): each query block in a slot of its
+//    kept count rounded up to a power of two (>= 16 rows), blocks of one slot size per tile (k_fwd_union
+//    derives the tiling; persistent CTAs claim tiles). The softmax threads copy their Q^s row straight from
 //    global memory into TMEM (packed bf16 pairs): Q is the A operand of every S MMA and is never
 //    re-read from shared memory.
 //  * The CTA walks the UNION of its blocks' KV lists (rotated start). KV block j arrives as ONE bulk
@@ -63,7 +64,7 @@ struct FwdParams {
   const int* tab;    // [tiles][MAX_G] packed tile entries, query block | row offset << 16 (-1 = none)
   const int* tcount; // number of packed tiles per head (device; written by k_fwd_union)
   int BH;
-  int pack_min;      // smallest slot (8 rows; SR = one slot per block, the unpacked tiling)
+  int pack_min;      // smallest slot rows (16 by default; SR = one slot per block, the unpacked tiling)
   const uint32_t* ulists;  // [BH][ntiles][N] union entries of each tile (k_fwd_union), ucount[BH][ntiles] of them
   const int* ucount;
   int* work_ctr;           // next unclaimed tile (zeroed before the launch; the CTAs are persistent)
@@ -524,70 +525,28 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 // q2k lists), entry = j | extent class << 12 (bit 2/1/0: ragged last block along t/h/w, C23) | mask << 16 of the
 // slots that admitted j. Built here, in parallel for all tiles, so the attention CTA's prologue is one list copy.
 //
-// Packed tiles (perm == NULL): a query block takes fwd_slot_size(nk) rows (its kept count rounded up to a power
-// of two >= 8), and the blocks of one slot size fill tiles of 128 / size of them in block order (a ragged edge
-// block's 8 or 16 kept queries no longer pad a 32- or 64-row slot). Every CTA derives the same tiling from
-// kept_off (class counts, then the stable rank of each block within its class); the (tile 0, bh 0) CTA
-// publishes the tile count and the CTAs of bh 0 their tile's entries for the attention kernel.
+// Packed tiles (perm == NULL): the tiles of build_fwd_tiling (tab / tcount).
 template <int MAXG>
 __global__ void __launch_bounds__(256) k_fwd_union(Geo g, int G, int ntiles, const int* __restrict__ perm,
-                                                   const int* __restrict__ kept_off, int SR, int pack_min,
-                                                   int small_first,
                                                    const int* __restrict__ q2k_num, const int* __restrict__ q2k_idx,
                                                    uint32_t* __restrict__ ulists, int* __restrict__ ucount,
-                                                   int* __restrict__ tab, int* __restrict__ tcount) {
+                                                   const int* __restrict__ tab, const int* __restrict__ tcount) {
   extern __shared__ uint32_t ubits[];  // [G][NW] slot bitmaps
   __shared__ int s_qb[MAXG];
   __shared__ int s_upre[MAX_N / 32];
-  __shared__ int s_tot, s_cnt[4], s_wcnt[8];
+  __shared__ int s_tot;
   const int tile = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NW = (g.N + 31) >> 5;
   int NT = ntiles;
   if (perm) {
     if (tid < G) s_qb[tid] = perm[(static_cast<size_t>(bh) * ntiles + tile) * G + tid];
-  } else {
+  } else {  // packed tiles (k_kv_image's tiling CTA wrote tab / tcount)
     G = MAXG;
-    auto cls_of = [&](int j) {  // log2(slot size / 8), -1 for a block without kept queries
-      const int nk = kept_off[j + 1] - kept_off[j];
-      return nk > 0 ? 31 - __clz(fwd_slot_size(nk, SR, pack_min) >> 3) : -1;
-    };
-    if (tid < 4) s_cnt[tid] = 0;
-    if (tid < MAXG) s_qb[tid] = -1;
-    __syncthreads();
-    for (int j = tid; j < g.N; j += 256) {
-      const int c = cls_of(j);
-      if (c >= 0) atomicAdd(&s_cnt[c], 1);
-    }
-    __syncthreads();
-    // tiles of the largest slot size first (or the smallest: their longer unions start early)
-    int t0 = 0, k = -1, first = 0;
-    for (int ci = 0; ci < 4; ++ci) {
-      const int c = small_first ? ci : 3 - ci;
-      const int nt = (s_cnt[c] + (16 >> c) - 1) / (16 >> c);
-      if (k < 0 && tile < t0 + nt) { k = c; first = t0; }
-      t0 += nt;
-    }
-    NT = t0;
-    if (bh == 0 && tile == 0 && tid == 0) *tcount = NT;
+    NT = *tcount;
     if (tile >= NT) return;  // (uniform)
-    const int per = 16 >> k, r0 = (tile - first) * per;
-    int carry = 0;
-    for (int j0 = 0; j0 < g.N; j0 += 256) {  // stable rank of each class-k block
-      const int j = j0 + tid;
-      const bool isk = j < g.N && cls_of(j) == k;
-      const uint32_t bal = __ballot_sync(0xffffffffu, isk);
-      if (lane == 0) s_wcnt[warp] = __popc(bal);
-      __syncthreads();
-      int off = carry;
-      for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-      const int rank = off + __popc(bal & ((1u << lane) - 1u));
-      if (isk && rank >= r0 && rank < r0 + per) s_qb[rank - r0] = j;
-      for (int w = 0; w < 8; ++w) carry += s_wcnt[w];
-      __syncthreads();
-    }
-    if (bh == 0 && tid < MAXG) {
-      const int qb = s_qb[tid];
-      tab[tile * MAXG + tid] = qb >= 0 ? qb | ((tid * (8 << k)) << 16) : -1;
+    if (tid < MAXG) {
+      const int e = tab[tile * MAXG + tid];
+      s_qb[tid] = e >= 0 ? e & 0xFFFF : -1;
     }
   }
   for (int w = tid; w < G * NW; w += 256) ubits[w] = 0u;
@@ -650,9 +609,7 @@ cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cu
   const int G = a.perm ? 128 / a.SR : MAX_G;
   const int ntiles = a.perm ? a.ntiles : fwd_max_tiles(a.g.N, a.SR);  // packed: an upper bound (CTAs past it exit)
   const int NW = (a.g.N + 31) / 32;
-  k_fwd_union<MAX_G><<<dim3(ntiles, a.BH), 256, G * NW * 4, st>>>(a.g, G, ntiles, a.perm, a.kept_off, a.SR,
-                                                                 a.pack_min, a.small_first,
-                                                                 a.q2k_num, a.q2k_idx, ulists, ucount, a.tab,
+  k_fwd_union<MAX_G><<<dim3(ntiles, a.BH), 256, G * NW * 4, st>>>(a.g, G, ntiles, a.perm, a.q2k_num, a.q2k_idx, ulists, ucount, a.tab,
                                                                  a.tcount);
   return cudaGetLastError();
 }
@@ -790,8 +747,67 @@ cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st) {
 // up to n16 = n rounded up to 16 (the MMA's N step), nothing beyond (never read). Layout [K: d-half 0 as BT
 // rows x 128 B, d-half 1 ...][V: same], 128-byte swizzled (8-row groups 1 KB apart: an image of 8-row groups
 // 4 KB apart, which makes the first n16 keys one prefix, slowed the MMAs' operand reads, 0.87 -> 1.07 ms).
+//
+// Packed forward tiles, built by one extra CTA of this launch (so they cost no launch of their own): a query
+// block takes fwd_slot_size(nk) rows (its kept count rounded up to a power of two >= pack_min, at most SR), and
+// the blocks of one slot size fill tiles of 128 / size of them in block order (a ragged edge block's 8 or 16
+// kept queries no longer pad a 32- or 64-row slot); the classes' tiles follow each other, smallest slots first
+// by default. tab[tile][e] = query block | row offset << 16 (-1: empty), *tcount = tiles per head.
+__device__ void build_fwd_tiling(const Geo& g, const FwdTiling& tl) {
+  __shared__ int s_cnt[4], s_first[4], s_carry[4], s_w[8][4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < tl.max_tiles * MAX_G; i += 256) tl.tab[i] = -1;
+  if (tid < 4) { s_cnt[tid] = 0; s_carry[tid] = 0; }
+  __syncthreads();
+  auto cls_of = [&](int j) {  // log2(slot size / 8), -1 for a block without kept queries
+    const int nk = tl.kept_off[j + 1] - tl.kept_off[j];
+    return nk > 0 ? 31 - __clz(fwd_slot_size(nk, tl.SR, tl.pack_min) >> 3) : -1;
+  };
+  for (int j = tid; j < g.N; j += 256) {
+    const int c = cls_of(j);
+    if (c >= 0) atomicAdd(&s_cnt[c], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int t0 = 0;
+    for (int ci = 0; ci < 4; ++ci) {
+      const int c = tl.small_first ? ci : 3 - ci;
+      s_first[c] = t0;
+      t0 += (s_cnt[c] + (16 >> c) - 1) / (16 >> c);
+    }
+    *tl.tcount = t0;
+  }
+  __syncthreads();
+  for (int j0 = 0; j0 < g.N; j0 += 256) {  // stable rank of each block within its class
+    const int j = j0 + tid;
+    const int c = j < g.N ? cls_of(j) : -1;
+    unsigned bal[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bal[k] = __ballot_sync(0xffffffffu, c == k);
+      if (lane == 0) s_w[warp][k] = __popc(bal[k]);
+    }
+    __syncthreads();
+    if (c >= 0) {
+      int rank = s_carry[c] + __popc(bal[c] & ((1u << lane) - 1u));
+      for (int w = 0; w < warp; ++w) rank += s_w[w][c];
+      const int per = 16 >> c, tile = s_first[c] + rank / per, slot = rank % per;
+      tl.tab[tile * MAX_G + slot] = j | ((slot * (8 << c)) << 16);
+    }
+    __syncthreads();
+    if (tid < 4)
+      for (int w = 0; w < 8; ++w) s_carry[tid] += s_w[w][tid];
+    __syncthreads();
+  }
+}
+
 template <int D, int BT>
-__global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Rows V, uint8_t* __restrict__ img) {
+__global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Rows V, uint8_t* __restrict__ img,
+                                                  const FwdTiling tl) {
+  if (blockIdx.x == g.N) {  // the extra CTA of head 0 builds the forward tiling
+    if (blockIdx.y == 0) build_fwd_tiling(g, tl);
+    return;
+  }
   constexpr int CPR = D / 8;        // 16-byte chunks per row
   constexpr int CHUNKS = BT * CPR;  // per tensor
   constexpr int PER = 2 * CHUNKS / 256;  // chunks per thread (K and V)
@@ -825,29 +841,48 @@ __global__ void __launch_bounds__(256) k_kv_image(Geo g, const Rows K, const Row
   }
 }
 
-cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st) {
-  dim3 grid(g.N, BH);
-  if (d == 128 && g.BT == 64) k_kv_image<128, 64><<<grid, 256, 0, st>>>(g, K, V, img);
-  else if (d == 128 && g.BT == 32) k_kv_image<128, 32><<<grid, 256, 0, st>>>(g, K, V, img);
-  else if (d == 64 && g.BT == 64) k_kv_image<64, 64><<<grid, 256, 0, st>>>(g, K, V, img);
-  else if (d == 64 && g.BT == 32) k_kv_image<64, 32><<<grid, 256, 0, st>>>(g, K, V, img);
+cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, const FwdTiling& tl,
+                            cudaStream_t st) {
+  dim3 grid(g.N + 1, BH);  // + the tiling CTA
+  if (d == 128 && g.BT == 64) k_kv_image<128, 64><<<grid, 256, 0, st>>>(g, K, V, img, tl);
+  else if (d == 128 && g.BT == 32) k_kv_image<128, 32><<<grid, 256, 0, st>>>(g, K, V, img, tl);
+  else if (d == 64 && g.BT == 64) k_kv_image<64, 64><<<grid, 256, 0, st>>>(g, K, V, img, tl);
+  else if (d == 64 && g.BT == 32) k_kv_image<64, 32><<<grid, 256, 0, st>>>(g, K, V, img, tl);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
-// Fill (reading C9): O[t] = O^s[donor(t)] for pruned t; one 16-byte chunk per thread.
-__global__ void k_fill(int BH, int L, int d, const int* __restrict__ donor, const Rows O) {
-  size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int vpr = d / 8;
-  if (v >= static_cast<size_t>(BH) * L * vpr) return;
-  size_t rowi = v / vpr;
-  int c = static_cast<int>(v % vpr) * 8;
-  const int bh = static_cast<int>(rowi / L);
-  int t = static_cast<int>(rowi % L);
-  int dn = donor[rowi];
-  if (dn != t) {
-    bf16* oh = O.head(bh);
-    *reinterpret_cast<uint4*>(oh + t * O.sl + c) = *reinterpret_cast<const uint4*>(oh + dn * O.sl + c);
+// Fill (reading C9): O[t] = O^s[donor(t)] for pruned t. One warp per 32 tokens: the lanes read the 32
+// donors (coalesced), a ballot gives the pruned ones, and groups of d/8 lanes copy one pruned row each, U rows
+// per group in flight (all loads before the stores) -- the one-chunk-per-thread version was latency-bound at
+// ~1.4 TB/s (two dependent loads per 16 bytes, half the threads idle on kept rows).
+template <int CPR>
+__global__ void __launch_bounds__(256) k_fill(int BH, int L, const int* __restrict__ donor, const Rows O) {
+  constexpr int RPI = 32 / CPR, U = 4;  // rows per pass of the warp, passes in flight
+  const int lane = threadIdx.x & 31;
+  const size_t wid = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int wpr = (L + 31) >> 5;  // warps per head
+  if (wid >= static_cast<size_t>(BH) * wpr) return;
+  const int bh = static_cast<int>(wid / wpr), t0 = static_cast<int>(wid % wpr) * 32;
+  const int t = t0 + lane;
+  const int dn = t < L ? donor[static_cast<size_t>(bh) * L + t] : t;
+  const unsigned mask = __ballot_sync(0xffffffffu, dn != t);
+  const int n = __popc(mask), sub = lane / CPR, c = (lane % CPR) * 8;
+  bf16* oh = O.head(bh);
+  for (int base = 0; base < n; base += RPI * U) {
+    uint4 v[U];
+    int dst[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int idx = base + k * RPI + sub;
+      const int pos = idx < n ? static_cast<int>(__fns(mask, 0, idx + 1)) : 0;
+      const int src = __shfl_sync(0xffffffffu, dn, pos);
+      dst[k] = idx < n ? t0 + pos : -1;
+      if (dst[k] >= 0) v[k] = *reinterpret_cast<const uint4*>(oh + static_cast<size_t>(src) * O.sl + c);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (dst[k] >= 0) *reinterpret_cast<uint4*>(oh + static_cast<size_t>(dst[k]) * O.sl + c) = v[k];
   }
 }
 
@@ -860,8 +895,11 @@ cudaError_t debug_trace_fwd(void* dev_buf, int cta) {
 }
 
 cudaError_t launch_fill(int BH, int L, int d, const int* donor, Rows O, cudaStream_t st) {
-  size_t total = static_cast<size_t>(BH) * L * (d / 8);
-  k_fill<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(BH, L, d, donor, O);
+  const size_t warps = static_cast<size_t>(BH) * ((L + 31) / 32);
+  const unsigned grid = static_cast<unsigned>((warps + 7) / 8);
+  if (d == 128) k_fill<16><<<grid, 256, 0, st>>>(BH, L, donor, O);
+  else if (d == 64) k_fill<8><<<grid, 256, 0, st>>>(BH, L, donor, O);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -60,17 +60,24 @@ struct FwdArgs {
   const uint8_t* kv_img;  // workspace: K|V block images (launch_kv_image)
   const int* perm;        // [BH][ntiles][G] query blocks of each tile (launch_group), or NULL: packed tiles
   int ntiles;
-  int* tab;               // workspace: [fwd_max_tiles][16] packed tile entries (written by launch_fwd_union)
-  int* tcount;            // workspace: their count
-  int pack_min;           // smallest packed slot: 8 rows, or SR (one slot per block: consecutive blocks per tile)
-  int small_first;        // packed tiles of the smallest slot size first
+  const int* tab;         // workspace: [fwd_max_tiles][16] packed tile entries (FwdTiling, launch_kv_image)
+  const int* tcount;      // workspace: their count
+  int pack_min;           // smallest packed slot (16 rows by default), or SR (one slot per block)
   uint32_t* ulists;       // workspace: [BH][ntiles][N] union entries per tile (launch_fwd_union)
   int* ucount;            // workspace: [BH][ntiles] their counts
   int* work_ctr;          // workspace: tile counter of the persistent forward
 };
 int fwd_max_tiles(int N, int SR);  // upper bound of the packed forward tiles per head
 cudaError_t launch_fwd_union(const FwdArgs& a, uint32_t* ulists, int* ucount, cudaStream_t st);
-cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, cudaStream_t st);
+// packed forward tiling (built by an extra CTA of the K|V image launch, attn_fwd.cu build_fwd_tiling)
+struct FwdTiling {
+  const int* kept_off;
+  int SR, pack_min, small_first, max_tiles;
+  int* tab;     // [max_tiles][16] query block | row offset << 16, -1 = empty
+  int* tcount;  // tiles per head
+};
+cudaError_t launch_kv_image(const Geo& g, int BH, int d, Rows K, Rows V, uint8_t* img, const FwdTiling& tl,
+                            cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdArgs& a, cudaStream_t st);
 cudaError_t debug_trace_fwd(void* dev_buf, int cta);
 cudaError_t debug_trace_bwd(void* dev_buf, int cta);
