@@ -209,7 +209,7 @@ long long ds_capacity(const bsa::Geo& g, size_t BH, int SR) {
   return std::min(dens, bytes_cap);
 }
 struct BwdWs {
-  size_t qs, img, dv, dq, ctr, qoff, ptot, slot, ds, total;
+  size_t qs, img, dv, dq, ctr, qoff, ord, ptot, slot, ds, total;
   long long cap;
 };
 BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
@@ -220,7 +220,8 @@ BwdWs bwd_ws(const bsa::Geo& g, size_t BH, size_t Lq, int SR, int d) {
   w.dq = w.dv + align256(BH * g.N * static_cast<size_t>(SR) * 8);
   w.ctr = w.dq + align256(BH * Lq * d * 4);
   w.qoff = w.ctr + align256(BH * 4);  // work counters of the main kernel (one per launch, <= B <= BH)
-  w.ptot = w.qoff + align256(BH * g.N * 4);
+  w.ord = w.qoff + align256(BH * g.N * 4);  // the main kernel's claim order
+  w.ptot = w.ord + align256(BH * g.N * 4);
   w.slot = w.ptot + align256((BH + 1) * 4);  // per-head pair counts, then the total
   const bool ds = g_bwd_path.load() == BSA_BWD_DS;
   w.ds = w.slot + (ds ? align256(BH * g.N * static_cast<size_t>(g.N) * 4) : 0);
@@ -595,6 +596,9 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.lsed = reinterpret_cast<float*>(base + w.dv);
   a.dQacc = reinterpret_cast<float*>(base + w.dq);
   a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
+  // longest-first claim order of the main kernel (BSA_BWD_ORDER=index: claim in index order)
+  static const bool index_order = env_flag("BSA_BWD_ORDER", "index");
+  a.item_order = index_order ? nullptr : reinterpret_cast<int*>(base + w.ord);
   a.q2k_num = q2k_num;
   a.q2k_idx = q2k_idx;
   a.q2k_off = reinterpret_cast<int*>(base + w.qoff);

@@ -76,6 +76,58 @@ __device__ __forceinline__ float ex2b(float x) {
 // memory once (coalesced 16-byte loads), then one warp per kept row folds the dO of the pruned tokens
 // whose donor it is (the gradient of the fill), forms D = rowsum(dO^s O^s) and writes its image
 // row, row statistics and the zeroed dQ accumulator row.
+// Claim order of the persistent main kernel: index order (neighbouring KV blocks of one head run together and
+// share their query blocks' images in L2), except that the shortest ~5% of the items (by k2q length, i.e.
+// chunk count) are moved to the end, in index order, so the kernel's tail is made of short items. (With items
+// claimed in index order the CTAs finished over a 55 us spread at 32k, 2.4% of the SMs' time idle; a full
+// longest-first order removed the tail but lost the L2 locality: attn_bwd 1.35 -> 1.51 ms at 32k, 22.4 -> 30.3
+// ms at 75k; tools/profiling/bwd_tail.py.) One CTA: a length histogram gives the 5% threshold, then a stable
+// partition by chunked ballot scans.
+__device__ void build_item_order(const Geo& g, int heads, int b, const int* __restrict__ k2q_num,
+                                 int* __restrict__ order, int* hist, int hist_cap /* shared ints */) {
+  __shared__ int s_thr, s_nlong, s_w[8][2], s_carry[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n_items = heads * g.N;
+  const int top = g.N < hist_cap ? g.N : hist_cap - 1;  // (lengths >= top share the top bucket)
+  const size_t base = static_cast<size_t>(b) * n_items;
+  auto bucket = [&](int i) { const int v = k2q_num[base + i]; return v < top ? v : top; };
+  for (int v = tid; v <= top; v += blockDim.x) hist[v] = 0;
+  if (tid < 2) s_carry[tid] = 0;
+  __syncthreads();
+  for (int i = tid; i < n_items; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1);
+  __syncthreads();
+  if (tid == 0) {  // threshold: the smallest length v with at least 5% of the items at or below it
+    int run = 0, v = 0;
+    for (; v < top; ++v) {
+      run += hist[v];
+      if (run * 20 >= n_items) break;
+    }
+    s_thr = v;
+    s_nlong = 0;
+  }
+  __syncthreads();
+  const int thr = s_thr;
+  for (int i = tid; i < n_items; i += blockDim.x) atomicAdd(&s_nlong, bucket(i) > thr ? 1 : 0);
+  __syncthreads();
+  const int nlong = s_nlong;
+  for (int i0 = 0; i0 < n_items; i0 += blockDim.x) {  // stable partition: long items first, then short ones
+    const int i = i0 + tid;
+    const bool valid = i < n_items, is_long = valid && bucket(i) > thr;
+    const unsigned bl = __ballot_sync(0xffffffffu, is_long), bs = __ballot_sync(0xffffffffu, valid && !is_long);
+    if (lane == 0) { s_w[warp][0] = __popc(bl); s_w[warp][1] = __popc(bs); }
+    __syncthreads();
+    if (valid) {
+      const int k = is_long ? 0 : 1;
+      int pos = s_carry[k] + __popc((is_long ? bl : bs) & ((1u << lane) - 1u));
+      for (int w = 0; w < warp; ++w) pos += s_w[w][k];
+      order[base + (is_long ? pos : nlong + pos)] = i;
+    }
+    __syncthreads();
+    if (tid < 2)
+      for (int w = 0; w < 8; ++w) s_carry[tid] += s_w[w][tid];
+    __syncthreads();
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR, const int* __restrict__ kept_off,
                                                   const int* __restrict__ kept_tok, const int* __restrict__ donor,
@@ -83,13 +135,19 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
                                                   const float* __restrict__ lse,
                                                   uint8_t* __restrict__ qdo_img, float* __restrict__ lsed,
                                                   float* __restrict__ dQacc, const int* __restrict__ pair_total,
-                                                  long long ds_cap, const Rows dQ) {
+                                                  long long ds_cap, const Rows dQ, const int* __restrict__ k2q_num,
+                                                  int* __restrict__ item_order, int launch_heads) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
   constexpr int NCB = D / 64;
   constexpr int MAXT = 128;    // tokens per block (checked by the API)
   __shared__ __align__(16) bf16 s_do[MAXT * D];
   __shared__ int s_tok[MAXT], s_don[MAXT];
   const int blk = blockIdx.x, bh = blockIdx.y;
+  if (blk == g.N) {  // the extra CTAs: the main kernel's claim order of launch bh (if there is one)
+    if (bh < BH / launch_heads)
+      build_item_order(g, launch_heads, bh, k2q_num, item_order, reinterpret_cast<int*>(s_do), MAXT * D / 2);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t bi = static_cast<size_t>(bh) * g.N + blk;
   const size_t head = static_cast<size_t>(bh) * g.L;
@@ -249,6 +307,7 @@ struct BwdParams {
                        // head coordinate of the K/V/dK/dV tensor maps
   int items;           // work items of this launch: heads x N KV blocks, item = hc * N + j
   int* work_ctr;       // next unclaimed item (zeroed before the launch)
+  const int* item_order;  // [launch][items] claim order (build_item_order), or NULL: index order
   float scale_log2;
   float scale;
   // dS path (DESIGN.md §5 "Backward"): when the selection's admitted (query block, KV block) pairs fit the
@@ -431,7 +490,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_attn_bwd(const __grid_consta
         const int rs = it % ITEM_RING;
         if (it >= ITEM_RING) bwait(&bar_item_empty[rs], ((it / ITEM_RING) - 1) & 1);
         const int v = atomicAdd(p.work_ctr, 1);
-        s_item[rs] = v < p.items ? v : -1;
+        s_item[rs] = v >= p.items ? -1 : (p.item_order ? p.item_order[static_cast<size_t>(p.bh0) * g.N + v] : v);
         mbar_arrive(&bar_item_full[rs]);
       }
       __syncwarp();
@@ -1289,14 +1348,25 @@ cudaError_t launch_bwd_dq(const BwdArgs& a, cudaStream_t st) {
 }
 
 
+// launches of the main kernel: one over all heads when the K/V/dK/dV head strides are uniform, else one per batch
+static int bwd_launch_heads(const BwdArgs& a) {
+  const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
+                   heads_uniform(a.dV, a.B);
+  return one ? a.BH : a.Hh;
+}
+
 cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
-  const dim3 prep_blocks(a.g.N, a.BH);  // one CTA per (b,h, query block)
+  // one CTA per (b,h, query block), plus one per main-kernel launch for its claim order
+  const dim3 prep_blocks(a.g.N + (a.item_order ? 1 : 0), a.BH);
+  const int lh = bwd_launch_heads(a);
   if (a.d == 128)
     k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ);
+                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ,
+                                                 a.k2q_num, a.item_order, lh);
   else
     k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
-                                                a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ);
+                                                a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ,
+                                                a.k2q_num, a.item_order, lh);
   return cudaGetLastError();
 }
 
@@ -1324,9 +1394,8 @@ cudaError_t launch_bwd_main(const BwdArgs& a, cudaStream_t st) {
       !make_map_rows_f32(&p.mDQh, a.dQacc, a.d, dq_rows_total, 16) ||
       !make_map_rows_f32(&p.mDQq, a.dQacc, a.d, dq_rows_total, 8))
     return cudaErrorInvalidValue;
-  const bool one = heads_uniform(a.K, a.B) && heads_uniform(a.V, a.B) && heads_uniform(a.dK, a.B) &&
-                   heads_uniform(a.dV, a.B);
-  const int launches = one ? 1 : a.B, heads = one ? a.BH : a.Hh;
+  const int heads = bwd_launch_heads(a), launches = a.BH / heads;
+  p.item_order = a.item_order;
   // one work counter per launch, zeroed on the stream (the persistent CTAs claim items from it)
   cudaError_t ez = cudaMemsetAsync(a.work_ctr, 0, sizeof(int) * launches, st);
   if (ez != cudaSuccess) return ez;
