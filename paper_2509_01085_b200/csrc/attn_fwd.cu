@@ -148,6 +148,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
 
   const Geo& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef BSA_TRACE
+  // per-CTA start / end stamps (debug builds; bsa_debug_trace_fwd(buf, -1)): tools/profiling/fwd_tail.py
+  auto cta_stamp = [&](int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (g_fwd_trace != nullptr && g_fwd_trace_cta == -1) g_fwd_trace[2 * blockIdx.x + k] = t;
+  };
+  if (tid == 0) cta_stamp(0);
+#endif
   const int G = p.G, SR = p.SR;
   const int NT = p.perm ? p.ntiles : *p.tcount;  // tiles per head
   const int total_tiles = NT * p.BH;
@@ -518,6 +527,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_attn_fwd(const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+#ifdef BSA_TRACE
+  if (tid == 0) cta_stamp(1);
+#endif
   if (warp == W_ALLOC) tmem_dealloc(tbase, SM::TMEM_COLS);
 }
 
