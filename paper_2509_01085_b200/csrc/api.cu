@@ -598,7 +598,13 @@ int bsa_attn_bwd(const bsa_geom* g, double r, int32_t B, int32_t Hh, int32_t d, 
   a.work_ctr = reinterpret_cast<int*>(base + w.ctr);
   // longest-first claim order of the main kernel (BSA_BWD_ORDER=index: claim in index order)
   static const bool index_order = env_flag("BSA_BWD_ORDER", "index");
+  static const int bwd_short_pct = [] {  // BSA_BWD_SHORT_PCT: percent of the items claimed last (default 5)
+    const char* e = std::getenv("BSA_BWD_SHORT_PCT");
+    const int v = e ? std::atoi(e) : 5;
+    return v < 1 ? 1 : (v > 100 ? 100 : v);
+  }();
   a.item_order = index_order ? nullptr : reinterpret_cast<int*>(base + w.ord);
+  a.short_pct = bwd_short_pct;
   a.q2k_num = q2k_num;
   a.q2k_idx = q2k_idx;
   a.q2k_off = reinterpret_cast<int*>(base + w.qoff);

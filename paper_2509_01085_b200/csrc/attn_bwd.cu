@@ -84,7 +84,7 @@ __device__ __forceinline__ float ex2b(float x) {
 // ms at 75k; tools/profiling/bwd_tail.py.) One CTA: a length histogram gives the 5% threshold, then a stable
 // partition by chunked ballot scans.
 __device__ void build_item_order(const Geo& g, int heads, int b, const int* __restrict__ k2q_num,
-                                 int* __restrict__ order, int* hist, int hist_cap /* shared ints */) {
+                                 int* __restrict__ order, int* hist, int hist_cap /* shared ints */, int short_pct) {
   __shared__ int s_thr, s_nlong, s_w[8][2], s_carry[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n_items = heads * g.N;
   const int top = g.N < hist_cap ? g.N : hist_cap - 1;  // (lengths >= top share the top bucket)
@@ -95,11 +95,11 @@ __device__ void build_item_order(const Geo& g, int heads, int b, const int* __re
   __syncthreads();
   for (int i = tid; i < n_items; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1);
   __syncthreads();
-  if (tid == 0) {  // threshold: the smallest length v with at least 5% of the items at or below it
+  if (tid == 0) {  // threshold: the smallest length v with at least short_pct % of the items at or below it
     int run = 0, v = 0;
     for (; v < top; ++v) {
       run += hist[v];
-      if (run * 20 >= n_items) break;
+      if (run * 100 >= short_pct * n_items) break;
     }
     s_thr = v;
     s_nlong = 0;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
                                                   uint8_t* __restrict__ qdo_img, float* __restrict__ lsed,
                                                   float* __restrict__ dQacc, const int* __restrict__ pair_total,
                                                   long long ds_cap, const Rows dQ, const int* __restrict__ k2q_num,
-                                                  int* __restrict__ item_order, int launch_heads) {
+                                                  int* __restrict__ item_order, int launch_heads, int short_pct) {
   constexpr int PER = D / 32;  // channels per lane (4 or 2)
   constexpr int NCB = D / 64;
   constexpr int MAXT = 128;    // tokens per block (checked by the API)
@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(256) k_bwd_prep(Geo g, int BH, int Lq, int SR,
   const int blk = blockIdx.x, bh = blockIdx.y;
   if (blk == g.N) {  // the extra CTAs: the main kernel's claim order of launch bh (if there is one)
     if (bh < BH / launch_heads)
-      build_item_order(g, launch_heads, bh, k2q_num, item_order, reinterpret_cast<int*>(s_do), MAXT * D / 2);
+      build_item_order(g, launch_heads, bh, k2q_num, item_order, reinterpret_cast<int*>(s_do), MAXT * D / 2,
+                       short_pct);
     return;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1362,11 +1363,11 @@ cudaError_t launch_bwd_prep(const BwdArgs& a, cudaStream_t st) {
   if (a.d == 128)
     k_bwd_prep<128><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
                                                  a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ,
-                                                 a.k2q_num, a.item_order, lh);
+                                                 a.k2q_num, a.item_order, lh, a.short_pct);
   else
     k_bwd_prep<64><<<prep_blocks, 256, 0, st>>>(a.g, a.BH, a.Lq, a.SR, a.kept_off, a.kept_tok, a.donor, a.Qs, a.dO,
                                                 a.O, a.lse, a.qdo_img, a.lsed, a.dQacc, a.pair_total, a.ds_cap, a.dQ,
-                                                a.k2q_num, a.item_order, lh);
+                                                a.k2q_num, a.item_order, lh, a.short_pct);
   return cudaGetLastError();
 }
 

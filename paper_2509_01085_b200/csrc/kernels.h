@@ -115,7 +115,8 @@ struct BwdArgs {
   float* lsed;       // [BH, N, SR, 2]: per query block and row, LSE*log2(e) and D
   float* dQacc;  // [BH, Lq, d]
   int* work_ctr;  // [B] item counters of the persistent main kernel (one per launch)
-  int* item_order;  // [BH * N] its claim order, longest k2q list first (built by launch_bwd_prep), or NULL
+  int* item_order;  // [BH * N] its claim order: the shortest short_pct % of the k2q lists last (launch_bwd_prep)
+  int short_pct;
   // dS path (attn_bwd.cu): selection lists, pair slots, the path switch and the dS tile store
   const int* q2k_num;
   const int* q2k_idx;
